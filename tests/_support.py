@@ -1,0 +1,35 @@
+"""Test helpers: load (building if needed) the oracle and the product."""
+import glob
+import importlib
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def load_oracle():
+    """The CPU oracle (test infrastructure only)."""
+    build = os.path.join(ROOT, "oracle", "_build")
+    if not glob.glob(os.path.join(build, "_oracle*.so")):
+        subprocess.check_call(["make", "-C", os.path.join(ROOT, "oracle")])
+    if build not in sys.path:
+        sys.path.insert(0, build)
+    return importlib.import_module("_oracle")
+
+
+def load_product():
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import paper_1804_00995_b200 as g
+
+    return g
+
+
+def rel_fro(a, b):
+    """Relative Frobenius error ||a-b||_F / ||b||_F."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
