@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — driver-contract benchmark for the B200 dense BEM hot path.
+
+Default workload (BASELINE.json configs[1], "cfg2"): unit-sphere icosphere L5
+(10242 vertices, 20480 triangles), P1 Lagrange, 3-point (edge-midpoint) rule,
+Helmholtz single layer with k = 2 pi / (10 hbar); one step = dense assembly of
+the 10242 x 10242 complex128 matrix (K1+K2, device-resident tables) followed
+by one stored matvec y = A x (K4, x complex N(0,1) from seed 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config 1|2|3|4|5]
+
+Metric: reference-equivalent quadrature-pair kernel evaluations per second
+(M_x * M_y per assembly / step time), plus matrix entries/s and matvec GB/s.
+Multi-GPU: replicas only — every rank runs the full step; value
+is the whole-job aggregate over ranks with the max-over-ranks device time.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+# Algorithmic FP64 work per unique location pair: the
+# production pair formula (gk_math.cuh green<>: 33 FP64 instructions = 51
+# flops with DFMA = 2) plus one complex x real accumulate (2 DFMA = 4 flops).
+F_PAIR_FLOPS = {True: 55.0, False: 23.0}  # Helmholtz / Laplace ("[1/r]": 11 instr = 19 flops + 4)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------------
+def config_problem(g, cfg):
+    """Mesh/space/kernel of a BASELINE config."""
+    spec = {
+        1: dict(n=642, gauss=3, fam="P1", helm=False, perturb=None, seed=0, real_x=True),
+        2: dict(n=10242, gauss=3, fam="P1", helm=True, perturb=None, seed=1, real_x=False),
+        3: dict(n=10242, gauss=6, fam="P0", helm=True, perturb=2, seed=1, real_x=False),
+        4: dict(n=40962, gauss=3, fam="P0", helm=True, perturb=None, seed=3, real_x=False),
+        5: dict(n=163842, gauss=3, fam="points", helm=True, perturb=None, seed=4, real_x=False),
+    }[cfg]
+    mesh = g.build_sphere(spec["n"], 1.0)
+    if spec["perturb"] is not None:
+        mesh = g.perturb_radial(mesh, spec["perturb"], 0.02)
+    hbar = g.edge_stats(mesh).mean_len
+    k = 2 * math.pi / (10 * hbar) if spec["helm"] else 0.0
+    name = "[exp(ikr)/r]" if spec["helm"] else "[1/r]"
+    dom = g.make_domain(mesh, spec["gauss"])
+    space = g.make_fem(mesh, spec["fam"]) if spec["fam"] != "points" else None
+    return spec, mesh, dom, space, g.green_kernel(name, k), k, hbar, name
+
+
+def workload_name(cfg, spec, mesh):
+    nv, ne = mesh.vertex_count(), mesh.element_count()
+    return {
+        1: f"cfg1: Laplace single layer, P1, 3-pt, icosphere L3 ({nv} v/{ne} t), 642^2 real-valued complex128 + matvec",
+        2: f"cfg2: Helmholtz single layer, P1, 3-pt, icosphere L5 ({nv} v/{ne} t), 10242^2 complex128 + matvec",
+        3: f"cfg3: Helmholtz single layer, P0, 6-pt, perturbed L5 ({ne} t), 20480^2 complex128 + matvec (dense part)",
+        4: f"cfg4: Helmholtz single layer, P0, 3-pt, icosphere L6 ({ne} t), 81920^2 complex128 (107 GB) + 10 matvecs",
+        5: f"cfg5: matrix-free Helmholtz Green matvec, 983040 points of L7 ({ne} t)",
+    }[cfg]
+
+
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def profile_traffic(cfg):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"cfg{cfg}", {}).get("k_assemble_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------
+def cpu_sample_rows(oracle, mesh, gauss, fam, target_points):
+    """Evenly spaced test dofs whose supporting x points total ~target_points."""
+    start, dof, _ = oracle.eval_rows(mesh.vertices, mesh.elements, fam, gauss)
+    start = np.asarray(start)
+    dof = np.asarray(dof)
+    ndof = mesh.vertex_count() if fam == 1 else mesh.element_count()
+    per_dof = np.bincount(dof, minlength=ndof)
+    count = max(1, int(target_points / max(1.0, per_dof.mean())))
+    rows = sorted(set(np.linspace(0, ndof - 1, count).astype(int).tolist()))
+    sel = np.isin(dof, rows)
+    pt_of = np.repeat(np.arange(len(start) - 1), np.diff(start))
+    npts = len(np.unique(pt_of[sel]))
+    return rows, npts
+
+
+def run_cpu(oracle, mesh, spec, k, name, rows, threads, cap=1e13):
+    fam = 1 if spec["fam"] == "P1" else 0
+    t = time.perf_counter()
+    oracle.bem_dense(mesh.vertices, mesh.elements, spec["gauss"], fam, mesh.vertices, mesh.elements, spec["gauss"],
+                     fam, name, k, rows=rows, threads=threads, cap=cap)
+    return time.perf_counter() - t
+
+
+# ---------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    if args.impl == "reference":
+        return reference_arm(args, rank, world, dist)
+
+    import paper_1804_00995_b200 as g
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec, mesh, dom, space, kern, k, hbar, kname = config_problem(g, args.config)
+    if args.config == 5:
+        return bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k, hbar)
+
+    opts = g.BemOptions()
+    opts.memory_cap_bytes = 10 ** 15  # the reference's 8e9 cap refuses cfg 3/4 (SURVEY trap 5)
+    plan = g.AssemblyPlan(dom, dom, space, kern, space, opts)
+    info = plan.info()
+    n = info["rows"]
+    A = torch.empty(n * n, dtype=torch.complex128, device=dev)
+    xs = g.normal(spec["seed"], n) if spec["real_x"] else g.complex_normal(spec["seed"], n)
+    x = torch.tensor(np.asarray(xs, dtype=np.complex128), device=dev)
+    y = torch.empty(n, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    nmv = 10 if args.config == 4 else 1
+    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        plan.assemble(A.data_ptr(), n, sp)
+        if ev:
+            ev[1].record(stream)
+        for _ in range(nmv):
+            g.matvec(A.data_ptr(), n, n, n, x.data_ptr(), y.data_ptr(), sp)
+        if ev:
+            ev[2].record(stream)
+
+    fp64_peak_gflops = g.diag_fp64_peak(20000, sp)  # DFMA microbenchmark, this run
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    asm_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
+    if dist:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    pairs_ref = info["pairs_reference"]
+    value = world * pairs_ref / (ms_step * 1e-3)
+
+    out = None
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+        helm = k != 0.0
+        alg_flops = info["pairs_unique"] * F_PAIR_FLOPS[helm]
+        achieved = alg_flops / (asm_ms * 1e-3) / 1e12
+        peak = fp64_peak_gflops / 1e3
+        mv_bytes = 16.0 * n * n + 32.0 * n
+        clocks = clk.summary()
+        out = {
+            "metric": "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per assembly, fp64)",
+            "value": value,
+            "unit": "pairs/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64 (complex128)",
+            "data": "synthetic (seeded icosphere mesh, SplitMix64/Box-Muller vectors)",
+            "config": {"workload": workload_name(args.config, spec, mesh), "N": n, "M": int(math.isqrt(pairs_ref)),
+                       "k": k, "hbar": hbar, "parallelism": f"replicas x{world}",
+                       "l2": "inputs larger than L2: A = %.2f GB written+read per step; plan tables %.1f MB"
+                             % (16 * n * n / 1e9, info["device_bytes"] / 1e6)},
+            "entries_per_s": world * n * n / (ms_step * 1e-3),
+            "assembly_ms": asm_ms,
+            "matvec_ms": mv_ms,
+            "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
+            "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
+            "pairs_evaluated_per_unique": info["pairs_evaluated"] / info["pairs_unique"],
+            "roofline": {"bound": "fp64", "kernel": "k_assemble (K1+K2)", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": profile_traffic(args.config),
+                         "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no FP64)",
+                         "work": "pairs_unique x %.0f FP64 flops/pair (DESIGN.md F_pair)" % F_PAIR_FLOPS[helm]},
+            "roofline_matvec": {"bound": "hbm", "achieved": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak": hbm,
+                                "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        if not args.no_e2e and args.config in (1, 2):
+            out["e2e"] = e2e_dense(g, torch, dom, space, kern, opts, n, pairs_ref, steps=max(2, min(args.steps, 3)))
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(spec, mesh, k, kname, ms_step)
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def e2e_dense(g, torch, dom, space, kern, opts, n, pairs_ref, steps):
+    """Same metric through the public drop-in (gk_bem_dense): host mesh tables in,
+    host (pinned) matrix out, every copy inside the timed region."""
+    host = torch.empty(n * n, dtype=torch.complex128, pin_memory=True)
+    g.bem_dense_into(dom, dom, space, kern, space, opts, host.data_ptr(), n)  # warm-up
+    ts = []
+    h2d = 0
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        h2d = g.bem_dense_into(dom, dom, space, kern, space, opts, host.data_ptr(), n)
+        ts.append(time.perf_counter() - t)
+    t = float(np.median(ts))
+    return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": 16 * n * n, "s_per_step": t,
+            "path": "gk_bem_dense (C-ABI, host sides -> pinned host matrix)"}
+
+
+def cpu_baseline(spec, mesh, k, name, gpu_ms_step):
+    from tests._support import load_oracle
+
+    oracle = load_oracle()
+    fam = 1 if spec["fam"] == "P1" else 0
+    M = mesh.element_count() * spec["gauss"]
+    rows, npts = cpu_sample_rows(oracle, mesh, spec["gauss"], fam, target_points=min(M, 1536))
+    secs = run_cpu(oracle, mesh, spec, k, name, rows, threads=1)
+    pairs = npts * M
+    return {"value": pairs / secs, "unit": "pairs/s", "cores": 1, "kind": "port",
+            "sample": f"oracle bem_product restatement, {len(rows)} complete test rows ({npts} x-points x {M} "
+                      f"y-points = {pairs:.3g} pairs) in {secs:.1f} s, 1 thread (reference concurrency)"}
+
+
+def reference_arm(args, rank, world, dist):
+    """The reference's CPU path timed on the host cores: the oracle (C++
+    restatement, the reference cannot be built here) with all host threads."""
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    import paper_1804_00995_b200 as g
+    from tests._support import load_oracle
+
+    oracle = load_oracle()
+    spec, mesh, dom, space, kern, k, hbar, kname = config_problem(g, args.config)
+    threads = os.cpu_count() or 1
+    fam = 1 if spec["fam"] == "P1" else 0
+    M = mesh.element_count() * spec["gauss"]
+    rows, npts = cpu_sample_rows(oracle, mesh, spec["gauss"], fam, target_points=min(M, 2048))
+    for _ in range(max(1, args.warmup)):
+        run_cpu(oracle, mesh, spec, k, kname, rows[:8], threads)
+    ts = [run_cpu(oracle, mesh, spec, k, kname, rows, threads) for _ in range(args.steps)]
+    t = float(np.mean(ts))
+    value = npts * M / t
+    out = {"impl": "reference", "metric": "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per assembly, fp64)",
+           "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64 (complex128)", "data": "synthetic",
+           "config": {"workload": workload_name(args.config, spec, mesh), "N": space.free_count() if space else None},
+           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                            "sample": f"oracle bem_product restatement (OpenMP over trial columns), {len(rows)} "
+                                      f"complete test rows = {npts} x-points x {M} y-points per step"},
+           "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k, hbar):
+    pts, w, _ = g.quadrature(dom)
+    q = np.asarray(w) * g.complex_normal(spec["seed"], len(w))
+    plan = g.GreenPlan(pts, pts, kern)
+    info = plan.info()
+    qd = torch.tensor(q, device=dev)
+    y = torch.empty(len(w), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    res = {}
+    for prec, label in ((g.FP64, "fp64"), (g.FP32, "fp32")):
+        plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / args.steps
+        res[label] = {"ms": ms, "pairs_per_s": len(w) ** 2 / (ms * 1e-3),
+                      "unique_pairs_per_s": info["unique_targets"] * info["unique_sources"] / (ms * 1e-3)}
+    if rank == 0:
+        print(json.dumps({"metric": "matrix-free Green matvec pair evals/s (reference-equivalent)",
+                          "value": res["fp64"]["pairs_per_s"], "unit": "pairs/s", "n_gpus": world,
+                          "steps": args.steps, "detail": res, "info": info, "higher_is_better": True}))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,37 @@
+/*
+ * galerk_b200 diagnostics — measurement helpers used by bench.py and the
+ * profiling notes.  Not part of the reference-facing interface.
+ */
+#ifndef GALERK_B200_DIAG_H
+#define GALERK_B200_DIAG_H
+
+#include <stdint.h>
+
+#include "galerk_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* FP64 pipe peak: a DFMA-only kernel (8 independent chains per thread, all
+ * SMs).  Returns achieved GFLOP/s (2 flops per DFMA) over `iters` iterations,
+ * timed with CUDA events on `stream`. */
+gk_status gk_diag_fp64_peak(int64_t iters, double* gflops, gk_stream stream);
+
+/* The canonical F_pair probe: the reference formula of
+ * kernels.cpp:94-114 compiled with libdevice (sqrt, sin, cos, complex / real
+ * division, r*r <= eps^2 mask) plus one complex x real accumulate, evaluated
+ * for every (target, source) pair of n x n points (device SoA arrays).
+ * ncu's FP64 instruction counters over this launch divided by n*n give F_pair.
+ * out: device [n] complex accumulators. */
+gk_status gk_diag_probe_pairs(int64_t n, const double* x, const double* y, const double* z, double k,
+                              double eps, gk_cplx* out, gk_stream stream);
+
+/* The same pair count through the production pair function (gk_math.cuh). */
+gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const double* z, double k,
+                             double eps, gk_cplx* out, gk_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,419 @@
+// extern "C" boundary (include/galerk_b200.h): argument checking, the
+// reference's error semantics, plan lifetime, device residency.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <unordered_map>
+
+#include "gk_internal.hpp"
+
+namespace gk {
+
+namespace {
+thread_local std::string t_last_error;
+}
+
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+void cuda_check(int err, const char* what) {
+  if (err != cudaSuccess) {
+    const char* s = cudaGetErrorString(static_cast<cudaError_t>(err));
+    throw CudaError(std::string(what) + ": " + (s ? s : "unknown CUDA error"));
+  }
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw CudaError("galerk_b200: no CUDA device available (this library has no CPU fallback)");
+}
+
+void DevBuf::alloc(size_t n) {
+  release();
+  if (n == 0) return;
+  if (cudaMalloc(&p, n) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+    throw NoMemError("device allocation of " + std::to_string(n) + " bytes failed");
+  }
+  bytes = n;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+void DevBuf::upload(const void* src, size_t n) {
+  alloc(n);
+  if (n) cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+}
+
+}  // namespace gk
+
+using namespace gk;
+
+struct gk_plan {
+  int64_t rows = 0, cols = 0;
+  bool symmetric = false, helmholtz = false;
+  double eps = 0.0, k = 0.0;
+  int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0;
+  DevBuf tile_i, tile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c,
+      yb_dof_start, yb_rec_start, yrec, xperm, yperm;
+  uint64_t device_bytes() const {
+    const DevBuf* b[] = {&tile_i, &tile_j, &xb_dof_start, &xb_loc_start, &xl_x, &xl_y, &xl_z, &xsup_start,
+                         &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &xperm, &yperm};
+    uint64_t s = 0;
+    for (auto* p : b) s += p->bytes;
+    return s;
+  }
+};
+
+struct gk_green_plan {
+  int64_t nt_orig = 0, ns_orig = 0, nt = 0, ns = 0;
+  bool helmholtz = false;
+  double eps = 0.0, k = 0.0;
+  DevBuf tx, ty, tz, txf, tyf, tzf, sx, sy, sz, sxf, syf, szf, src_start, src_list, tgt_loc, Q, Y;
+};
+
+namespace {
+
+void check_kernel(const gk_kernel* k) {
+  if (!k) throw std::invalid_argument("bem_dense: null kernel");
+  if (k->components != 1)
+    throw std::invalid_argument("assembly: incompatible operand components (1," + std::to_string(k->components) +
+                                ",1)");
+  if (k->kind != GK_LAPLACE && k->kind != GK_HELMHOLTZ)
+    throw std::invalid_argument(
+        "bem_dense: only the built-in scalar Green kernels run on the GPU path (custom kernels are not supported)");
+  if (!std::isfinite(k->k)) throw std::invalid_argument("bem_dense: wavenumber must be finite");
+}
+
+void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) {
+  // assembly.cpp:196-203
+  const uint64_t need = 16ull * ((uint64_t)test.nfree * (uint64_t)trial.nfree + (uint64_t)o.chunk * trial.npts +
+                                 (uint64_t)o.chunk * (uint64_t)trial.nfree);
+  if (need > o.memory_cap_bytes)
+    throw std::runtime_error("bem_dense: estimated memory " + std::to_string(need / 1000000) +
+                             " MB exceeds the cap of " + std::to_string(o.memory_cap_bytes / 1000000) +
+                             " MB; use the tol (H-matrix) variant");
+}
+
+std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
+                                   const gk_options* opts) {
+  if (!test || !trial) throw std::invalid_argument("bem_dense: null side");
+  check_kernel(kernel);
+  gk_options o;
+  gk_options_default(&o);
+  if (opts) o = *opts;
+  memory_cap(*test, *trial, o);
+  require_device();
+  auto P = std::make_unique<gk_plan>();
+  P->rows = test->nfree;
+  P->cols = trial->nfree;
+  P->helmholtz = kernel->kind == GK_HELMHOLTZ && kernel->k != 0.0;
+  P->k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;  // "[1/r]" forces k = 0 (kernels.cpp:47-49)
+  P->eps = guard_radius(*test, *trial);
+  P->symmetric = o.symmetric == 1 || (o.symmetric < 0 && sides_identical(*test, *trial));
+  Locations X = build_locations(*test, "bem_dense(test)");
+  Locations Y;
+  if (P->symmetric) {
+    if (!sides_identical(*test, *trial))
+      throw std::invalid_argument("bem_dense: symmetric=1 requires identical test and trial sides");
+  } else {
+    Y = build_locations(*trial, "bem_dense(trial)");
+  }
+  const Locations& Yr = P->symmetric ? X : Y;
+  TileTables T = build_tiles(X, Yr, P->symmetric);
+  P->xloc = X.size();
+  P->yloc = Yr.size();
+  P->pairs_ref = test->npts * trial->npts;
+  P->pairs_unique = P->symmetric ? X.size() * (X.size() + 1) / 2 : X.size() * Yr.size();
+  P->pairs_eval = T.pairs_evaluated;
+  P->ntiles = (int64_t)T.tile_i.size();
+  P->tile_i.upload(T.tile_i);
+  P->tile_j.upload(T.tile_j);
+  P->xb_dof_start.upload(T.xb_dof_start);
+  P->xb_loc_start.upload(T.xb_loc_start);
+  P->xl_x.upload(T.xl_x);
+  P->xl_y.upload(T.xl_y);
+  P->xl_z.upload(T.xl_z);
+  P->xsup_start.upload(T.xsup_start);
+  P->xsup_u.upload(T.xsup_u);
+  P->xsup_c.upload(T.xsup_c);
+  P->yb_dof_start.upload(T.yb_dof_start);
+  P->yb_rec_start.upload(T.yb_rec_start);
+  P->yrec.upload(T.yrec);
+  P->xperm.upload(X.perm);
+  P->yperm.upload(Yr.perm);
+  return P;
+}
+
+void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
+  if (!P) throw std::invalid_argument("gk_plan_assemble: null plan");
+  if (P->rows == 0 || P->cols == 0) return;
+  if (!A) throw std::invalid_argument("gk_plan_assemble: null matrix");
+  if (lda < P->rows) throw std::invalid_argument("gk_plan_assemble: lda < rows");
+  AsmArgs a;
+  a.tile_i = P->tile_i.as<int32_t>();
+  a.tile_j = P->tile_j.as<int32_t>();
+  a.xb_dof_start = P->xb_dof_start.as<int32_t>();
+  a.xb_loc_start = P->xb_loc_start.as<int32_t>();
+  a.xl_x = P->xl_x.as<double>();
+  a.xl_y = P->xl_y.as<double>();
+  a.xl_z = P->xl_z.as<double>();
+  a.xsup_start = P->xsup_start.as<int32_t>();
+  a.xsup_u = P->xsup_u.as<int32_t>();
+  a.xsup_c = P->xsup_c.as<double>();
+  a.yb_dof_start = P->yb_dof_start.as<int32_t>();
+  a.yb_rec_start = P->yb_rec_start.as<int32_t>();
+  a.yrec = P->yrec.as<YRec>();
+  a.xperm = P->xperm.as<int32_t>();
+  a.yperm = P->yperm.as<int32_t>();
+  a.A = A;
+  a.lda = lda;
+  a.eps2 = P->eps * P->eps;
+  a.kappa = 2.0 * P->k / M_PI;
+  a.symmetric = P->symmetric ? 1 : 0;
+  launch_assemble(a, P->ntiles, P->helmholtz, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+void gk_options_default(gk_options* o) {
+  if (!o) return;
+  o->memory_cap_bytes = 8000000000ull;  // BemOptions (assembly.hpp:27-30)
+  o->chunk = 1024;
+  o->symmetric = -1;
+  o->reserved = 0;
+}
+
+gk_status gk_plan_create(const gk_side* test, const gk_side* trial, const gk_kernel* kernel, const gk_options* opts,
+                         gk_plan** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("gk_plan_create: null output");
+    *out = nullptr;
+    *out = make_plan(test, trial, kernel, opts).release();
+  });
+}
+
+gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
+  return guard([&] {
+    if (!P || !info) throw std::invalid_argument("gk_plan_get_info: null argument");
+    info->rows = P->rows;
+    info->cols = P->cols;
+    info->x_locations = P->xloc;
+    info->y_locations = P->yloc;
+    info->pairs_reference = P->pairs_ref;
+    info->pairs_unique = P->pairs_unique;
+    info->pairs_evaluated = P->pairs_eval;
+    info->tiles = P->ntiles;
+    info->symmetric = P->symmetric ? 1 : 0;
+    info->eps = P->eps;
+    info->device_bytes = P->device_bytes();
+  });
+}
+
+gk_status gk_plan_assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
+  return guard([&] { assemble(P, A, lda, stream); });
+}
+
+int32_t gk_plan_launches(const gk_plan* P) { return (P && P->ntiles > 0) ? 1 : 0; }
+
+gk_status gk_plan_destroy(gk_plan* P) {
+  return guard([&] { delete P; });
+}
+
+gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kernel* kernel, const gk_options* opts,
+                       gk_cplx* A_host, int64_t lda) {
+  return guard([&] {
+    auto P = make_plan(test, trial, kernel, opts);
+    if (P->rows == 0 || P->cols == 0) return;
+    if (!A_host) throw std::invalid_argument("gk_bem_dense: null output matrix");
+    if (lda < P->rows) throw std::invalid_argument("gk_bem_dense: lda < rows");
+    DevBuf A;
+    A.alloc(sizeof(gk_cplx) * (size_t)P->rows * (size_t)P->cols);
+    cudaStream_t s = nullptr;
+    assemble(P.get(), A.as<gk_cplx>(), P->rows, s);
+    cuda_check(cudaMemcpy2DAsync(A_host, sizeof(gk_cplx) * lda, A.p, sizeof(gk_cplx) * P->rows,
+                                 sizeof(gk_cplx) * P->rows, P->cols, cudaMemcpyDeviceToHost, s),
+               "cudaMemcpy2DAsync D2H");
+    cuda_check(cudaStreamSynchronize(s), "gk_bem_dense");
+  });
+}
+
+gk_status gk_matvec(const gk_cplx* A, int64_t rows, int64_t cols, int64_t lda, const gk_cplx* x, gk_cplx* y,
+                    gk_stream stream) {
+  return guard([&] {
+    if (rows < 0 || cols < 0) throw std::invalid_argument("gk_matvec: negative size");
+    if (rows > 0 && cols > 0 && (!A || !x)) throw std::invalid_argument("gk_matvec: null input");
+    if (rows > 0 && !y) throw std::invalid_argument("gk_matvec: null output");
+    if (lda < rows) throw std::invalid_argument("gk_matvec: lda < rows");
+    require_device();
+    launch_matvec(A, rows, cols, lda, x, y, stream);
+  });
+}
+
+int32_t gk_matvec_launches(int64_t rows, int64_t cols) { return matvec_launch_count(rows, cols); }
+
+gk_status gk_green_plan_create(int64_t nt, const double* tx, const double* ty, const double* tz, int64_t ns,
+                               const double* sx, const double* sy, const double* sz, const gk_kernel* kernel,
+                               gk_green_plan** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("gk_green_plan_create: null output");
+    *out = nullptr;
+    check_kernel(kernel);
+    if (nt < 0 || ns < 0) throw std::invalid_argument("gk_green_plan_create: negative size");
+    if ((nt > 0 && (!tx || !ty || !tz)) || (ns > 0 && (!sx || !sy || !sz)))
+      throw std::invalid_argument("gk_green_plan_create: null point array");
+    require_device();
+    auto P = std::make_unique<gk_green_plan>();
+    P->nt_orig = nt;
+    P->ns_orig = ns;
+    P->helmholtz = kernel->kind == GK_HELMHOLTZ && kernel->k != 0.0;
+    P->k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;
+    P->eps = guard_radius_pts(nt, tx, ty, tz, ns, sx, sy, sz);
+    // merge twins: reuse the side machinery with one "element" per point
+    auto uniq = [](int64_t n, const double* x, const double* y, const double* z, std::vector<double>& ux,
+                   std::vector<double>& uy, std::vector<double>& uz, std::vector<int64_t>& loc) {
+      std::vector<double> w(n, 1.0), basis(1, 1.0);
+      std::vector<int32_t> dofs(n);
+      for (int64_t i = 0; i < n; ++i) dofs[i] = (int32_t)i;
+      gk_side s{n, x, y, z, w.data(), 1, n, 1, dofs.data(), basis.data(), n};
+      Locations L = build_locations(s, "green_matvec");
+      ux = L.x;
+      uy = L.y;
+      uz = L.z;
+      loc = L.point_loc;
+    };
+    std::vector<double> ux, uy, uz, vx, vy, vz;
+    std::vector<int64_t> tloc, sloc;
+    uniq(nt, tx, ty, tz, ux, uy, uz, tloc);
+    uniq(ns, sx, sy, sz, vx, vy, vz, sloc);
+    P->nt = (int64_t)ux.size();
+    P->ns = (int64_t)vx.size();
+    std::vector<int64_t> start(P->ns + 1, 0), list(ns);
+    for (int64_t j = 0; j < ns; ++j) start[sloc[j] + 1]++;
+    for (int64_t v = 0; v < P->ns; ++v) start[v + 1] += start[v];
+    std::vector<int64_t> f(start.begin(), start.end() - 1);
+    for (int64_t j = 0; j < ns; ++j) list[f[sloc[j]]++] = j;
+    auto tof = [](const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); };
+    P->tx.upload(ux);
+    P->ty.upload(uy);
+    P->tz.upload(uz);
+    P->txf.upload(tof(ux));
+    P->tyf.upload(tof(uy));
+    P->tzf.upload(tof(uz));
+    P->sx.upload(vx);
+    P->sy.upload(vy);
+    P->sz.upload(vz);
+    P->sxf.upload(tof(vx));
+    P->syf.upload(tof(vy));
+    P->szf.upload(tof(vz));
+    P->src_start.upload(start);
+    P->src_list.upload(list);
+    P->tgt_loc.upload(tloc);
+    P->Q.alloc(sizeof(gk_cplx) * std::max<int64_t>(1, P->ns));
+    P->Y.alloc(sizeof(gk_cplx) * std::max<int64_t>(1, P->nt));
+    *out = P.release();
+  });
+}
+
+gk_status gk_green_matvec(gk_green_plan* P, const gk_cplx* q, gk_cplx* y, int32_t precision, gk_stream stream) {
+  return guard([&] {
+    if (!P) throw std::invalid_argument("gk_green_matvec: null plan");
+    if (precision != GK_FP64 && precision != GK_FP32)
+      throw std::invalid_argument("gk_green_matvec: precision must be GK_FP64 or GK_FP32");
+    if (P->nt_orig > 0 && !y) throw std::invalid_argument("gk_green_matvec: null output");
+    if (P->ns_orig > 0 && !q) throw std::invalid_argument("gk_green_matvec: null charges");
+    GreenArgs a;
+    a.nt = P->nt;
+    a.ns = P->ns;
+    a.nsrc_orig = P->ns_orig;
+    a.ntgt_orig = P->nt_orig;
+    a.tx = P->tx.as<double>();
+    a.ty = P->ty.as<double>();
+    a.tz = P->tz.as<double>();
+    a.txf = P->txf.as<float>();
+    a.tyf = P->tyf.as<float>();
+    a.tzf = P->tzf.as<float>();
+    a.sx = P->sx.as<double>();
+    a.sy = P->sy.as<double>();
+    a.sz = P->sz.as<double>();
+    a.sxf = P->sxf.as<float>();
+    a.syf = P->syf.as<float>();
+    a.szf = P->szf.as<float>();
+    a.src_start = P->src_start.as<int64_t>();
+    a.src_list = P->src_list.as<int64_t>();
+    a.tgt_loc = P->tgt_loc.as<int64_t>();
+    a.eps2 = P->eps * P->eps;
+    a.kappa = 2.0 * P->k / M_PI;
+    a.eps2f = (float)a.eps2;
+    a.kappaf = (float)a.kappa;
+    launch_green(a, q, P->Q.p, P->Y.p, y, precision, P->helmholtz, stream);
+  });
+}
+
+gk_status gk_green_plan_get_info(const gk_green_plan* P, int64_t* nt, int64_t* ns, double* eps) {
+  return guard([&] {
+    if (!P) throw std::invalid_argument("gk_green_plan_get_info: null plan");
+    if (nt) *nt = P->nt;
+    if (ns) *ns = P->ns;
+    if (eps) *eps = P->eps;
+  });
+}
+
+gk_status gk_green_plan_destroy(gk_green_plan* P) {
+  return guard([&] { delete P; });
+}
+
+gk_status gk_device_alloc(uint64_t bytes, void** ptr) {
+  return guard([&] {
+    if (!ptr) throw std::invalid_argument("gk_device_alloc: null output");
+    require_device();
+    *ptr = nullptr;
+    if (bytes && cudaMalloc(ptr, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      *ptr = nullptr;
+      throw NoMemError("gk_device_alloc: " + std::to_string(bytes) + " bytes");
+    }
+  });
+}
+
+gk_status gk_device_free(void* ptr) {
+  return guard([&] {
+    if (ptr) cuda_check(cudaFree(ptr), "cudaFree");
+  });
+}
+
+gk_status gk_copy_to_device(void* dst, const void* src, uint64_t bytes, gk_stream stream) {
+  return guard([&] {
+    if (bytes)
+      cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
+                 "cudaMemcpyAsync H2D");
+  });
+}
+
+gk_status gk_copy_to_host(void* dst, const void* src, uint64_t bytes, gk_stream stream) {
+  return guard([&] {
+    if (bytes)
+      cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)),
+                 "cudaMemcpyAsync D2H");
+  });
+}
+
+gk_status gk_stream_synchronize(gk_stream stream) {
+  return guard([&] { cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize"); });
+}
+
+const char* gk_last_error(void) { return t_last_error.c_str(); }
+
+const char* gk_version(void) { return "galerk_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// Measurement helpers (include/galerk_b200_diag.h): FP64 peak microbenchmark
+// and the F_pair probe kernels used for the roofline accounting.
+#include <cuda_runtime.h>
+
+#include "../../include/galerk_b200_diag.h"
+#include "gk_internal.hpp"
+#include "gk_math.cuh"
+
+namespace gk {
+namespace {
+
+__global__ void __launch_bounds__(256) k_dfma_peak(long long iters, double seed, double* sink) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+         a7 = a0 + 7;
+  const double m = 0.999999999, c = 1e-9;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fma(a0, m, c);
+      a1 = fma(a1, m, c);
+      a2 = fma(a2, m, c);
+      a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c);
+      a5 = fma(a5, m, c);
+      a6 = fma(a6, m, c);
+      a7 = fma(a7, m, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) sink[threadIdx.x] = s;  // never true; keeps the chains alive
+}
+
+// Reference formula (kernels.cpp:94-114) with libdevice, plus one complex x
+// real accumulate: the canonical probe for F_pair.
+__global__ void __launch_bounds__(256) k_probe(long long n, const double* __restrict__ x, const double* __restrict__ y,
+                                               const double* __restrict__ z, double k, double eps,
+                                               double2* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xi = x[i], yi = y[i], zi = z[i];
+  const double eps2 = eps * eps;
+  double re = 0.0, im = 0.0;
+  for (long long j = 0; j < n; ++j) {
+    const double dx = xi - x[j], dy = yi - y[j], dz = zi - z[j];
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double cv = cos(k * r), sv = sin(k * r);
+    if (r * r <= eps2) continue;
+    const double w = 1.0;  // complex x real accumulate with a unit weight
+    re += w * (cv / r);
+    im += w * (sv / r);
+  }
+  out[i] = make_double2(re, im);
+}
+
+__global__ void __launch_bounds__(256) k_fast(long long n, const double* __restrict__ x, const double* __restrict__ y,
+                                              const double* __restrict__ z, double kappa, double eps2,
+                                              double2* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xi = x[i], yi = y[i], zi = z[i];
+  double re = 0.0, im = 0.0;
+  for (long long j = 0; j < n; ++j) {
+    const c64 g = green<true>(xi - x[j], yi - y[j], zi - z[j], eps2, kappa);
+    re = fma(1.0, g.re, re);
+    im = fma(1.0, g.im, im);
+  }
+  out[i] = make_double2(re, im);
+}
+
+}  // namespace
+}  // namespace gk
+
+using namespace gk;
+
+extern "C" {
+
+gk_status gk_diag_fp64_peak(int64_t iters, double* gflops, gk_stream stream) {
+  return guard([&] {
+    require_device();
+    if (!gflops || iters <= 0) throw std::invalid_argument("gk_diag_fp64_peak: bad arguments");
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    DevBuf sink;
+    sink.alloc(256 * sizeof(double));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int blocks = sms * 8;
+    k_dfma_peak<<<blocks, 256, 0, s>>>(iters / 8 + 1, 1.0, sink.as<double>());  // warm-up
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    cudaEventRecord(e0, s);
+    k_dfma_peak<<<blocks, 256, 0, s>>>(iters, 1.0, sink.as<double>());
+    cudaEventRecord(e1, s);
+    cuda_check(cudaEventSynchronize(e1), "peak kernel");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double dfma = (double)blocks * 256.0 * (double)iters * 32.0;
+    *gflops = 2.0 * dfma / (ms * 1e-3) / 1e9;
+  });
+}
+
+gk_status gk_diag_probe_pairs(int64_t n, const double* x, const double* y, const double* z, double k, double eps,
+                              gk_cplx* out, gk_stream stream) {
+  return guard([&] {
+    require_device();
+    k_probe<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        n, x, y, z, k, eps, reinterpret_cast<double2*>(out));
+    cuda_check(cudaGetLastError(), "k_probe");
+  });
+}
+
+gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const double* z, double k, double eps,
+                             gk_cplx* out, gk_stream stream) {
+  return guard([&] {
+    require_device();
+    k_fast<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        n, x, y, z, 2.0 * k / M_PI, eps * eps, reinterpret_cast<double2*>(out));
+    cuda_check(cudaGetLastError(), "k_fast");
+  });
+}
+
+}  // extern "C"

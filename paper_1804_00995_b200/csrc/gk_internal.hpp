@@ -1,0 +1,188 @@
+// Internal (non-ABI) declarations shared by the galerk_b200 translation units.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/galerk_b200.h"
+
+namespace gk {
+
+// ---- errors: exceptions inside, status codes + gk_last_error() at the ABI ----
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoMemError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void set_last_error(const std::string& msg);
+
+template <class F>
+gk_status guard(F&& f) {
+  try {
+    f();
+    return GK_OK;
+  } catch (const CudaError& e) {
+    set_last_error(e.what());
+    return GK_ECUDA;
+  } catch (const NoMemError& e) {
+    set_last_error(e.what());
+    return GK_ENOMEM;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return GK_EINVAL;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return GK_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return GK_ERUNTIME;
+  }
+}
+
+void cuda_check(int err, const char* what);  // err is a cudaError_t
+void require_device();
+
+// ---- device buffers -----------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    o.bytes = 0;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n);
+  void release();
+  void upload(const void* src, size_t n);
+  template <class T>
+  void upload(const std::vector<T>& v) {
+    upload(v.data(), v.size() * sizeof(T));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// ---- unique quadrature locations of one side (host) -----------------------------
+// Points that are bit-identical (the edge-midpoint rule's twins, SURVEY trap 1)
+// are merged into one location carrying the summed (dof, w*phi) contributions.
+// The reference evaluates each twin separately and gets bit-identical kernel
+// values, so merging only reorders the additions.
+struct Locations {
+  int64_t npts = 0, nfree = 0;
+  std::vector<double> x, y, z;           // [U]
+  std::vector<int64_t> cstart;           // [U+1]
+  std::vector<int32_t> cdof;             // contributing dof (original index)
+  std::vector<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
+  std::vector<int32_t> perm, iperm;      // locality order: perm[p] = dof
+  std::vector<int64_t> dstart;           // [nfree+1] by permuted dof
+  std::vector<int32_t> dloc;             // location id
+  std::vector<double> dcoef;
+  std::vector<int64_t> point_loc;        // [npts] location of each point
+  int64_t size() const { return (int64_t)x.size(); }
+};
+Locations build_locations(const gk_side& s, const char* who);
+bool sides_identical(const gk_side& a, const gk_side& b);
+double guard_radius(const gk_side& a, const gk_side& b);  // kernels.cpp:14-19
+double guard_radius_pts(int64_t na, const double* ax, const double* ay, const double* az,
+                        int64_t nb, const double* bx, const double* by, const double* bz);
+
+// ---- assembly tiling ----------------------------------------------------------------
+constexpr int kUCap = 128;   // x locations per tile (one per thread)
+constexpr int kJCap = 48;    // y dofs per tile (H accumulator rows)
+constexpr int kIMax = 128;   // x dofs per tile
+constexpr int kAsmThreads = 128;
+
+struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
+  double x, y, z, c0, c1;
+  int32_t s0, s1;
+};
+static_assert(sizeof(YRec) == 48, "YRec layout");
+
+struct TileTables {
+  // x blocks
+  std::vector<int32_t> xb_dof_start;  // [nIb+1] permuted row ranges
+  std::vector<int32_t> xb_loc_start;  // [nIb+1]
+  std::vector<double> xl_x, xl_y, xl_z;
+  std::vector<int32_t> xsup_start;    // [nrows+1] by permuted row
+  std::vector<int32_t> xsup_u;        // local location index in its block
+  std::vector<double> xsup_c;
+  // y blocks
+  std::vector<int32_t> yb_dof_start;  // [nJb+1]
+  std::vector<int32_t> yb_rec_start;  // [nJb+1]
+  std::vector<YRec> yrec;
+  // tiles
+  std::vector<int32_t> tile_i, tile_j;
+  int64_t pairs_evaluated = 0;
+};
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric);
+
+struct AsmArgs {
+  const int32_t* tile_i;
+  const int32_t* tile_j;
+  const int32_t* xb_dof_start;
+  const int32_t* xb_loc_start;
+  const double* xl_x;
+  const double* xl_y;
+  const double* xl_z;
+  const int32_t* xsup_start;
+  const int32_t* xsup_u;
+  const double* xsup_c;
+  const int32_t* yb_dof_start;
+  const int32_t* yb_rec_start;
+  const YRec* yrec;
+  const int32_t* xperm;
+  const int32_t* yperm;
+  void* A;
+  int64_t lda;
+  double eps2;
+  double kappa;  // 2k/pi
+  int32_t symmetric;
+};
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, void* stream);
+
+// ---- matvec ---------------------------------------------------------------------------
+void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,
+                   void* stream);
+int matvec_launch_count(int64_t rows, int64_t cols);
+
+// ---- green matvec ------------------------------------------------------------------------
+struct GreenArgs {
+  int64_t nt, ns, nsrc_orig, ntgt_orig;
+  const double* tx;
+  const double* ty;
+  const double* tz;
+  const float* txf;
+  const float* tyf;
+  const float* tzf;
+  const double* sx;
+  const double* sy;
+  const double* sz;
+  const float* sxf;
+  const float* syf;
+  const float* szf;
+  const int64_t* src_start;  // [ns+1] CSR: unique source -> original sources
+  const int64_t* src_list;
+  const int64_t* tgt_loc;    // [ntgt_orig] original target -> unique target
+  double eps2;
+  double kappa;
+  float eps2f;
+  float kappaf;
+};
+void launch_green(const GreenArgs& a, const void* q, void* Q, void* Y, void* y, int precision,
+                  bool helmholtz, void* stream);
+
+}  // namespace gk

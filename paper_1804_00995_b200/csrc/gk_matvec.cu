@@ -1,0 +1,140 @@
+// K4: stored-matrix matvec y = A x (complex128, column-major), the product the
+// reference performs with Eigen::MatrixXcd * VectorXcd (test_assembly.cpp:233,
+// :277; LinearOperator::from_matrix, linsolve.hpp:20-23).
+//
+// HBM-bound: 16 bytes of A per complex MAC.  Each thread owns one row and a
+// contiguous column range (split-K); a warp reads 32 consecutive rows of a
+// column (512 contiguous bytes) with 8 independent 16-byte streaming loads in
+// flight per thread.  Partial sums land in a [splits x rows] scratch and a
+// second kernel adds them in split order: deterministic, no atomics.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "gk_internal.hpp"
+
+namespace gk {
+
+namespace {
+constexpr int kMvThreads = 256;
+constexpr int kMvUnroll = 8;
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(kMvThreads) k_matvec_partial(const double2* __restrict__ A, long long rows,
+                                                               long long cols, long long lda,
+                                                               const double2* __restrict__ x,
+                                                               double2* __restrict__ P, long long cps) {
+  const long long i = (long long)blockIdx.x * kMvThreads + threadIdx.x;
+  const long long c0 = (long long)blockIdx.y * cps;
+  const long long c1 = min(cols, c0 + cps);
+  if (i >= rows) return;
+  const double2* a = A + i + c0 * lda;
+  double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
+  long long j = c0;
+  for (; j + kMvUnroll <= c1; j += kMvUnroll) {
+    double2 v[kMvUnroll];
+#pragma unroll
+    for (int u = 0; u < kMvUnroll; ++u) v[u] = ld_stream(a + (long long)u * lda);
+#pragma unroll
+    for (int u = 0; u < kMvUnroll; ++u) {
+      const double2 xj = __ldg(x + j + u);
+      if (u & 1) {
+        re1 = fma(v[u].x, xj.x, re1);
+        re1 = fma(-v[u].y, xj.y, re1);
+        im1 = fma(v[u].x, xj.y, im1);
+        im1 = fma(v[u].y, xj.x, im1);
+      } else {
+        re0 = fma(v[u].x, xj.x, re0);
+        re0 = fma(-v[u].y, xj.y, re0);
+        im0 = fma(v[u].x, xj.y, im0);
+        im0 = fma(v[u].y, xj.x, im0);
+      }
+    }
+    a += kMvUnroll * lda;
+  }
+  for (; j < c1; ++j) {
+    const double2 v = ld_stream(a);
+    const double2 xj = __ldg(x + j);
+    re0 = fma(v.x, xj.x, re0);
+    re0 = fma(-v.y, xj.y, re0);
+    im0 = fma(v.x, xj.y, im0);
+    im0 = fma(v.y, xj.x, im0);
+    a += lda;
+  }
+  P[(long long)blockIdx.y * rows + i] = make_double2(re0 + re1, im0 + im1);
+}
+
+__global__ void k_matvec_reduce(const double2* __restrict__ P, long long rows, int splits,
+                                double2* __restrict__ y) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double re = 0.0, im = 0.0;
+  for (int s = 0; s < splits; ++s) {
+    const double2 v = P[(long long)s * rows + i];
+    re += v.x;
+    im += v.y;
+  }
+  y[i] = make_double2(re, im);
+}
+
+void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t row_blocks = (rows + kMvThreads - 1) / kMvThreads;
+  const int64_t target = (int64_t)sms * 8;  // ~8 resident CTAs of 256 threads per SM
+  splits = std::max<int64_t>(1, std::min<int64_t>((target + row_blocks - 1) / row_blocks,
+                                                  std::max<int64_t>(1, cols / 64)));
+  splits = std::min<int64_t>(splits, 65535);
+  cps = (cols + splits - 1) / splits;
+  splits = (cols + cps - 1) / cps;
+}
+
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+};
+thread_local Scratch t_scratch;
+}  // namespace
+
+int matvec_launch_count(int64_t rows, int64_t cols) { return (rows > 0 && cols > 0) ? 2 : 1; }
+
+void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y, void* stream) {
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rows <= 0) return;
+  if (cols <= 0) {
+    cuda_check(cudaMemsetAsync(y, 0, sizeof(double2) * rows, s), "cudaMemsetAsync");
+    return;
+  }
+  int64_t splits, cps;
+  plan(rows, cols, splits, cps);
+  const size_t need = sizeof(double2) * (size_t)rows * (size_t)splits;
+  if (t_scratch.bytes < need) {
+    if (t_scratch.p) {
+      cudaStreamSynchronize(s);
+      cudaFree(t_scratch.p);
+      t_scratch.p = nullptr;
+      t_scratch.bytes = 0;
+    }
+    if (cudaMalloc(&t_scratch.p, need) != cudaSuccess) throw NoMemError("gk_matvec: scratch allocation failed");
+    t_scratch.bytes = need;
+  }
+  const dim3 grid((unsigned)((rows + kMvThreads - 1) / kMvThreads), (unsigned)splits);
+  k_matvec_partial<<<grid, kMvThreads, 0, s>>>(static_cast<const double2*>(A), rows, cols, lda,
+                                               static_cast<const double2*>(x),
+                                               static_cast<double2*>(t_scratch.p), cps);
+  cuda_check(cudaGetLastError(), "k_matvec_partial launch");
+  k_matvec_reduce<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(static_cast<const double2*>(t_scratch.p), rows,
+                                                                (int)splits, static_cast<double2*>(y));
+  cuda_check(cudaGetLastError(), "k_matvec_reduce launch");
+}
+
+}  // namespace gk

@@ -1,0 +1,274 @@
+// Host-side plan construction for the dense assembly (runs once per operator;
+// the timed device work is gk_plan_assemble).  Replaces the host part of
+// make_side (assembly.cpp:144-171): the reference builds complex CSC
+// matrices (W B)^T and per-dof std::map lists; here the same information is
+// laid out for the device as unique locations + per-tile tables.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <unordered_map>
+
+#include "gk_internal.hpp"
+
+namespace gk {
+
+namespace {
+struct Key {
+  uint64_t a, b, c;
+  bool operator==(const Key& o) const { return a == o.a && b == o.b && c == o.c; }
+};
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    uint64_t h = k.a * 0x9E3779B97F4A7C15ULL;
+    h ^= (k.b + 0x632BE59BD9B4E019ULL + (h << 6) + (h >> 2));
+    h ^= (k.c + 0x85157AF5ULL + (h << 6) + (h >> 2));
+    return (size_t)(h ^ (h >> 29));
+  }
+};
+uint64_t bits(double v) {
+  v += 0.0;  // -0.0 -> +0.0 (same location)
+  uint64_t u;
+  std::memcpy(&u, &v, 8);
+  return u;
+}
+}  // namespace
+
+double guard_radius_pts(int64_t na, const double* ax, const double* ay, const double* az,
+                        int64_t nb, const double* bx, const double* by, const double* bz) {
+  if (na == 0 || nb == 0) return 0.0;  // kernels.cpp:14-19
+  double lo[3] = {ax[0], ay[0], az[0]}, hi[3] = {ax[0], ay[0], az[0]};
+  auto upd = [&](double x, double y, double z) {
+    const double p[3] = {x, y, z};
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = std::min(lo[c], p[c]);
+      hi[c] = std::max(hi[c], p[c]);
+    }
+  };
+  for (int64_t i = 0; i < na; ++i) upd(ax[i], ay[i], az[i]);
+  for (int64_t i = 0; i < nb; ++i) upd(bx[i], by[i], bz[i]);
+  const double d0 = hi[0] - lo[0], d1 = hi[1] - lo[1], d2 = hi[2] - lo[2];
+  return 1e-12 * std::sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+}
+
+double guard_radius(const gk_side& a, const gk_side& b) {
+  return guard_radius_pts(a.npts, a.x, a.y, a.z, b.npts, b.x, b.y, b.z);
+}
+
+static void validate(const gk_side& s, const char* who) {
+  if (s.npts < 0 || s.nelem < 0 || s.nfree < 0)
+    throw std::invalid_argument(std::string(who) + ": negative size");
+  if (s.g <= 0 || s.nloc <= 0) throw std::invalid_argument(std::string(who) + ": g and nloc must be positive");
+  if (s.npts != s.nelem * (int64_t)s.g)
+    throw std::invalid_argument(std::string(who) + ": npts must equal nelem * g (point e*g+q belongs to element e)");
+  if (s.npts > 0 && (!s.x || !s.y || !s.z || !s.w || !s.elem_dofs || !s.basis))
+    throw std::invalid_argument(std::string(who) + ": null array");
+  if (s.nfree > INT32_MAX) throw std::invalid_argument(std::string(who) + ": too many dofs");
+}
+
+bool sides_identical(const gk_side& a, const gk_side& b) {
+  if (&a == &b) return true;
+  if (a.npts != b.npts || a.g != b.g || a.nelem != b.nelem || a.nloc != b.nloc || a.nfree != b.nfree)
+    return false;
+  auto same = [](const void* p, const void* q, size_t n) { return p == q || std::memcmp(p, q, n) == 0; };
+  const size_t m = (size_t)a.npts * sizeof(double);
+  return same(a.x, b.x, m) && same(a.y, b.y, m) && same(a.z, b.z, m) && same(a.w, b.w, m) &&
+         same(a.elem_dofs, b.elem_dofs, (size_t)a.nelem * a.nloc * sizeof(int32_t)) &&
+         same(a.basis, b.basis, (size_t)a.g * a.nloc * sizeof(double));
+}
+
+Locations build_locations(const gk_side& s, const char* who) {
+  validate(s, who);
+  Locations L;
+  L.npts = s.npts;
+  L.nfree = s.nfree;
+  L.point_loc.resize(s.npts);
+  std::unordered_map<Key, int64_t, KeyHash> index;
+  index.reserve((size_t)s.npts);
+  for (int64_t k = 0; k < s.npts; ++k) {
+    const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
+    auto it = index.find(key);
+    if (it == index.end()) {
+      const int64_t u = (int64_t)L.x.size();
+      index.emplace(key, u);
+      L.x.push_back(s.x[k]);
+      L.y.push_back(s.y[k]);
+      L.z.push_back(s.z[k]);
+      L.point_loc[k] = u;
+    } else {
+      L.point_loc[k] = it->second;
+    }
+  }
+  const int64_t U = L.size();
+  // contributions: (dof, w_k * phi) for nonzero basis values of free dofs
+  // (femspace.cpp:476-484 skips exact zeros and constrained dofs), merged per
+  // (location, dof) in point order.
+  std::vector<int64_t> cnt(U + 1, 0);
+  for (int64_t k = 0; k < s.npts; ++k) cnt[L.point_loc[k] + 1] += s.nloc;
+  for (int64_t u = 0; u < U; ++u) cnt[u + 1] += cnt[u];
+  std::vector<int32_t> tdof(cnt[U]);
+  std::vector<double> tcoef(cnt[U]);
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1), used(U, 0);
+  for (int64_t k = 0; k < s.npts; ++k) {
+    const int64_t e = k / s.g;
+    const int q = (int)(k % s.g);
+    const int64_t u = L.point_loc[k];
+    for (int l = 0; l < s.nloc; ++l) {
+      const int32_t dof = s.elem_dofs[e * s.nloc + l];
+      const double b = s.basis[(int64_t)q * s.nloc + l];
+      if (dof < 0 || b == 0.0) continue;
+      if (dof >= s.nfree) throw std::invalid_argument(std::string(who) + ": dof index out of range");
+      const double c = s.w[k] * b;
+      int64_t base = cnt[u], n = used[u], p = base;
+      for (; p < base + n; ++p)
+        if (tdof[p] == dof) break;
+      if (p < base + n) {
+        tcoef[p] += c;
+      } else {
+        tdof[p] = dof;
+        tcoef[p] = c;
+        used[u]++;
+      }
+    }
+  }
+  (void)fill;
+  L.cstart.assign(U + 1, 0);
+  for (int64_t u = 0; u < U; ++u) L.cstart[u + 1] = L.cstart[u] + used[u];
+  L.cdof.resize(L.cstart[U]);
+  L.ccoef.resize(L.cstart[U]);
+  for (int64_t u = 0; u < U; ++u)
+    for (int64_t i = 0; i < used[u]; ++i) {
+      L.cdof[L.cstart[u] + i] = tdof[cnt[u] + i];
+      L.ccoef[L.cstart[u] + i] = tcoef[cnt[u] + i];
+    }
+  // dof order by first appearance along the location sequence (element order):
+  // P0 on a hierarchical mesh keeps the natural order; P1 vertices get a
+  // spatially coherent numbering for tiling.
+  L.iperm.assign(s.nfree, -1);
+  L.perm.clear();
+  L.perm.reserve(s.nfree);
+  for (int64_t p = 0; p < L.cstart[U]; ++p) {
+    const int32_t d = L.cdof[p];
+    if (L.iperm[d] < 0) {
+      L.iperm[d] = (int32_t)L.perm.size();
+      L.perm.push_back(d);
+    }
+  }
+  for (int64_t d = 0; d < s.nfree; ++d)
+    if (L.iperm[d] < 0) {
+      L.iperm[d] = (int32_t)L.perm.size();
+      L.perm.push_back((int32_t)d);
+    }
+  // per permuted dof: (location, coef) in location order
+  L.dstart.assign(s.nfree + 1, 0);
+  for (int64_t p = 0; p < L.cstart[U]; ++p) L.dstart[L.iperm[L.cdof[p]] + 1]++;
+  for (int64_t d = 0; d < s.nfree; ++d) L.dstart[d + 1] += L.dstart[d];
+  L.dloc.resize(L.cstart[U]);
+  L.dcoef.resize(L.cstart[U]);
+  std::vector<int64_t> f2(L.dstart.begin(), L.dstart.end() - 1);
+  for (int64_t u = 0; u < U; ++u)
+    for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
+      const int32_t pd = L.iperm[L.cdof[p]];
+      L.dloc[f2[pd]] = (int32_t)u;
+      L.dcoef[f2[pd]] = L.ccoef[p];
+      f2[pd]++;
+    }
+  return L;
+}
+
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
+  TileTables T;
+  const int64_t nrows = X.nfree, ncols = Y.nfree;
+  // ---- x blocks: consecutive permuted rows while their locations fit kUCap
+  std::vector<int64_t> owner(X.size(), -1);
+  std::vector<int32_t> local(X.size(), 0);
+  T.xb_dof_start.push_back(0);
+  T.xb_loc_start.push_back(0);
+  T.xsup_start.assign(nrows + 1, 0);
+  int64_t p = 0, blk = 0;
+  std::vector<int32_t> blk_locs;
+  while (p < nrows) {
+    const int64_t start = p;
+    blk_locs.clear();
+    while (p < nrows && p - start < kIMax) {
+      int fresh = 0;  // a row lists each location once (merged per (location, dof))
+      for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) fresh += owner[X.dloc[s]] != blk;
+      if ((int64_t)blk_locs.size() + fresh > kUCap) {
+        if (p == start)
+          throw std::invalid_argument("bem_dense: a test dof is supported by more than " +
+                                      std::to_string(kUCap) + " quadrature locations");
+        break;
+      }
+      for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
+        const int32_t u = X.dloc[s];
+        if (owner[u] != blk) {
+          owner[u] = blk;
+          local[u] = (int32_t)blk_locs.size();
+          blk_locs.push_back(u);
+        }
+        T.xsup_u.push_back(local[u]);
+        T.xsup_c.push_back(X.dcoef[s]);
+      }
+      T.xsup_start[p + 1] = (int32_t)T.xsup_u.size();
+      ++p;
+    }
+    for (int32_t u : blk_locs) {
+      T.xl_x.push_back(X.x[u]);
+      T.xl_y.push_back(X.y[u]);
+      T.xl_z.push_back(X.z[u]);
+    }
+    T.xb_dof_start.push_back((int32_t)p);
+    T.xb_loc_start.push_back((int32_t)T.xl_x.size());
+    ++blk;
+  }
+  // ---- y blocks: kJCap consecutive permuted cols; records = incident locations
+  std::vector<int64_t> ystamp(Y.size(), -1);
+  T.yb_dof_start.push_back(0);
+  T.yb_rec_start.push_back(0);
+  for (int64_t q0 = 0; q0 < ncols; q0 += kJCap) {
+    const int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+    const int64_t bj = (int64_t)T.yb_dof_start.size() - 1;
+    for (int64_t q = q0; q < q1; ++q)
+      for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
+        const int32_t v = Y.dloc[s];
+        if (ystamp[v] == bj) continue;
+        ystamp[v] = bj;
+        // slots of v inside [q0, q1)
+        std::vector<std::pair<int32_t, double>> sl;
+        for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
+          const int32_t pq = Y.iperm[Y.cdof[c]];
+          if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
+        }
+        for (size_t a = 0; a < sl.size(); a += 2) {
+          YRec r;
+          r.x = Y.x[v];
+          r.y = Y.y[v];
+          r.z = Y.z[v];
+          r.s0 = sl[a].first;
+          r.c0 = sl[a].second;
+          if (a + 1 < sl.size()) {
+            r.s1 = sl[a + 1].first;
+            r.c1 = sl[a + 1].second;
+          } else {
+            r.s1 = -1;
+            r.c1 = 0.0;
+          }
+          T.yrec.push_back(r);
+        }
+      }
+    T.yb_dof_start.push_back((int32_t)q1);
+    T.yb_rec_start.push_back((int32_t)T.yrec.size());
+  }
+  // ---- tiles (symmetric: skip tiles strictly below the diagonal)
+  const int64_t nIb = (int64_t)T.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
+  for (int64_t bi = 0; bi < nIb; ++bi)
+    for (int64_t bj = 0; bj < nJb; ++bj) {
+      if (symmetric && T.yb_dof_start[bj + 1] - 1 < T.xb_dof_start[bi]) continue;
+      T.tile_i.push_back((int32_t)bi);
+      T.tile_j.push_back((int32_t)bj);
+      T.pairs_evaluated += (int64_t)(T.xb_loc_start[bi + 1] - T.xb_loc_start[bi]) *
+                           (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
+    }
+  return T;
+}
+
+}  // namespace gk

@@ -1,0 +1,297 @@
+// Python binding of the galerk_b200 host API (csrc/host/galerk.hpp).
+// std::invalid_argument -> ValueError, std::runtime_error -> RuntimeError, so
+// Python tests read like the reference's doctest cases.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include "../host/galerk.hpp"
+#include "../../../include/galerk_b200_diag.h"
+
+namespace py = pybind11;
+using namespace galerk;
+
+using F64 = py::array_t<double, py::array::c_style | py::array::forcecast>;
+using I32 = py::array_t<int32_t, py::array::c_style | py::array::forcecast>;
+
+namespace {
+py::array_t<std::complex<double>> to_numpy(MatrixXcd&& A) {
+  auto* m = new MatrixXcd(std::move(A));
+  py::capsule own(m, [](void* p) { delete reinterpret_cast<MatrixXcd*>(p); });
+  return py::array_t<std::complex<double>>({(py::ssize_t)m->rows(), (py::ssize_t)m->cols()},
+                                           {(py::ssize_t)16, (py::ssize_t)(16 * m->rows())}, m->data(), own);
+}
+
+std::vector<Vec3> to_points(F64 p) {
+  auto a = p.unchecked<2>();
+  std::vector<Vec3> out(a.shape(0));
+  for (py::ssize_t i = 0; i < a.shape(0); ++i) out[i] = {a(i, 0), a(i, 1), a(i, 2)};
+  return out;
+}
+
+Mesh mesh_from(F64 v, I32 e) {
+  return Mesh(std::vector<double>(v.data(), v.data() + v.size()),
+              std::vector<int32_t>(e.data(), e.data() + e.size()));
+}
+
+py::array_t<double> points_array(const QuadratureSet& q) {
+  py::array_t<double> a({(py::ssize_t)q.size(), (py::ssize_t)3});
+  auto m = a.mutable_unchecked<2>();
+  for (int64_t i = 0; i < q.size(); ++i) {
+    m(i, 0) = q.x[i];
+    m(i, 1) = q.y[i];
+    m(i, 2) = q.z[i];
+  }
+  return a;
+}
+
+py::dict info_dict(const gk_plan_info& i) {
+  py::dict d;
+  d["rows"] = i.rows;
+  d["cols"] = i.cols;
+  d["x_locations"] = i.x_locations;
+  d["y_locations"] = i.y_locations;
+  d["pairs_reference"] = i.pairs_reference;
+  d["pairs_unique"] = i.pairs_unique;
+  d["pairs_evaluated"] = i.pairs_evaluated;
+  d["tiles"] = i.tiles;
+  d["symmetric"] = (bool)i.symmetric;
+  d["eps"] = i.eps;
+  d["device_bytes"] = i.device_bytes;
+  return d;
+}
+
+gk_stream as_stream(uintptr_t s) { return reinterpret_cast<gk_stream>(s); }
+
+class GreenPlan {
+ public:
+  GreenPlan(F64 targets, F64 sources, const Kernel& kernel) {
+    auto t = to_points(targets), s = to_points(sources);
+    std::vector<double> tx(t.size()), ty(t.size()), tz(t.size()), sx(s.size()), sy(s.size()), sz(s.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+      tx[i] = t[i].x;
+      ty[i] = t[i].y;
+      tz[i] = t[i].z;
+    }
+    for (size_t i = 0; i < s.size(); ++i) {
+      sx[i] = s[i].x;
+      sy[i] = s[i].y;
+      sz[i] = s[i].z;
+    }
+    const gk_kernel k = kernel.abi();
+    throw_status(gk_green_plan_create((int64_t)t.size(), tx.data(), ty.data(), tz.data(), (int64_t)s.size(),
+                                      sx.data(), sy.data(), sz.data(), &k, &p_));
+  }
+  ~GreenPlan() {
+    if (p_) gk_green_plan_destroy(p_);
+  }
+  void matvec(uintptr_t q, uintptr_t y, int precision, uintptr_t stream) {
+    throw_status(gk_green_matvec(p_, reinterpret_cast<const gk_cplx*>(q), reinterpret_cast<gk_cplx*>(y), precision,
+                                 as_stream(stream)));
+  }
+  py::dict info() const {
+    int64_t nt = 0, ns = 0;
+    double eps = 0;
+    throw_status(gk_green_plan_get_info(p_, &nt, &ns, &eps));
+    py::dict d;
+    d["unique_targets"] = nt;
+    d["unique_sources"] = ns;
+    d["eps"] = eps;
+    return d;
+  }
+
+ private:
+  gk_green_plan* p_ = nullptr;
+};
+}  // namespace
+
+PYBIND11_MODULE(_galerk, m) {
+  m.doc() = "galerk_b200: B200-native dense BEM assembly (host API over the C-ABI)";
+
+  py::class_<Vec3>(m, "Vec3").def_readonly("x", &Vec3::x).def_readonly("y", &Vec3::y).def_readonly("z", &Vec3::z);
+
+  py::class_<Mesh>(m, "Mesh")
+      .def(py::init(&mesh_from), py::arg("vertices"), py::arg("elements"))
+      .def_property_readonly("vertices",
+                             [](const Mesh& s) {
+                               return py::array_t<double>({(py::ssize_t)s.vertex_count(), (py::ssize_t)3},
+                                                          s.vertices.data());
+                             })
+      .def_property_readonly("elements",
+                             [](const Mesh& s) {
+                               return py::array_t<int32_t>({(py::ssize_t)s.element_count(), (py::ssize_t)3},
+                                                           s.elements.data());
+                             })
+      .def("vertex_count", &Mesh::vertex_count)
+      .def("element_count", &Mesh::element_count)
+      .def("element_measure", &Mesh::element_measure)
+      .def("total_measure", &Mesh::total_measure)
+      .def("bounding_box_diagonal", &Mesh::bounding_box_diagonal);
+
+  py::class_<EdgeStats>(m, "EdgeStats")
+      .def_readonly("min_len", &EdgeStats::min_len)
+      .def_readonly("max_len", &EdgeStats::max_len)
+      .def_readonly("mean_len", &EdgeStats::mean_len)
+      .def_readonly("std_len", &EdgeStats::std_len);
+
+  m.def("build_sphere", &build_sphere, py::arg("n_target"), py::arg("radius"));
+  m.def("edge_stats", &edge_stats);
+  m.def("perturb_radial", &perturb_radial, py::arg("mesh"), py::arg("seed"), py::arg("amp"));
+
+  py::class_<Domain>(m, "Domain")
+      .def_readonly("mesh", &Domain::mesh)
+      .def_readonly("gauss_count", &Domain::gauss_count);
+  m.def("make_domain", &make_domain, py::arg("mesh"), py::arg("gauss_count") = 1);
+  m.def("supported_rules", &supported_rules);
+  m.def("reference_rule", [](int dim, int count) {
+    const ReferenceRule& r = reference_rule(dim, count);
+    return py::make_tuple(r.barycentric, r.weights);
+  });
+  m.def("quadrature", [](const Domain& d) {
+    QuadratureSet q = quadrature(d);
+    return py::make_tuple(points_array(q), q.weights, q.element_of);
+  });
+
+  py::enum_<Family>(m, "Family").value("P0", Family::P0).value("P1", Family::P1);
+  py::class_<FemSpace>(m, "FemSpace")
+      .def("dof_count", &FemSpace::dof_count)
+      .def("free_count", &FemSpace::free_count)
+      .def("family", &FemSpace::family)
+      .def("element_dofs", &FemSpace::element_dofs)
+      .def_property_readonly("mesh", &FemSpace::mesh);
+  m.def("make_fem", &make_fem, py::arg("mesh"), py::arg("family"));
+
+  py::class_<Kernel>(m, "Kernel")
+      .def_static("green", &Kernel::green)
+      .def_static("custom", &Kernel::custom, py::arg("components"), py::arg("name") = "custom")
+      .def("components", &Kernel::components)
+      .def("wavenumber", &Kernel::wavenumber)
+      .def("name", &Kernel::name)
+      .def("singular_name", &Kernel::singular_name);
+  m.def("green_kernel", &green_kernel, py::arg("name"), py::arg("wavenumber"));
+
+  py::class_<BemOptions>(m, "BemOptions")
+      .def(py::init<>())
+      .def_readwrite("memory_cap_bytes", &BemOptions::memory_cap_bytes)
+      .def_readwrite("chunk", &BemOptions::chunk);
+
+  m.def(
+      "bem_dense",
+      [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
+         const BemOptions& o) {
+        MatrixXcd A;
+        {
+          py::gil_scoped_release rel;
+          A = bem_dense(dx, dy, t, k, u, o);
+        }
+        return to_numpy(std::move(A));
+      },
+      py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
+      py::arg("opts") = BemOptions{});
+  m.def(
+      "radiation_dense",
+      [](F64 pts, const Domain& dy, const Kernel& k, const FemSpace& u, const BemOptions& o) {
+        auto P = to_points(pts);
+        MatrixXcd A;
+        {
+          py::gil_scoped_release rel;
+          A = radiation_dense(P, dy, k, u, o);
+        }
+        return to_numpy(std::move(A));
+      },
+      py::arg("points"), py::arg("dom_y"), py::arg("kernel"), py::arg("trial"), py::arg("opts") = BemOptions{});
+  m.def("regularize", [](const Domain& dx, const Domain& dy, const FemSpace& t, const std::string& name,
+                         const FemSpace& u) {
+    SpMat S;
+    {
+      py::gil_scoped_release rel;
+      S = regularize(dx, dy, t, name, u);
+    }
+    return py::make_tuple(S.col_ptr, S.row_idx, S.values, py::make_tuple(S.rows, S.cols));
+  });
+
+  py::class_<AssemblyPlan>(m, "AssemblyPlan")
+      .def(py::init<const Domain&, const Domain&, const FemSpace&, const Kernel&, const FemSpace&,
+                    const BemOptions&, int>(),
+           py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
+           py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1)
+      .def(
+          "assemble",
+          [](AssemblyPlan& p, uintptr_t A, int64_t lda, uintptr_t stream) {
+            py::gil_scoped_release rel;
+            p.assemble(reinterpret_cast<gk_cplx*>(A), lda, as_stream(stream));
+          },
+          py::arg("A"), py::arg("lda"), py::arg("stream") = 0)
+      .def("info", [](const AssemblyPlan& p) { return info_dict(p.info()); })
+      .def("launches", &AssemblyPlan::launches);
+
+  m.def(
+      "matvec",
+      [](uintptr_t A, int64_t rows, int64_t cols, int64_t lda, uintptr_t x, uintptr_t y, uintptr_t stream) {
+        throw_status(gk_matvec(reinterpret_cast<const gk_cplx*>(A), rows, cols, lda,
+                               reinterpret_cast<const gk_cplx*>(x), reinterpret_cast<gk_cplx*>(y),
+                               as_stream(stream)));
+      },
+      py::arg("A"), py::arg("rows"), py::arg("cols"), py::arg("lda"), py::arg("x"), py::arg("y"),
+      py::arg("stream") = 0);
+  m.def("matvec_launches", &gk_matvec_launches);
+
+  py::class_<GreenPlan>(m, "GreenPlan")
+      .def(py::init<F64, F64, const Kernel&>(), py::arg("targets"), py::arg("sources"), py::arg("kernel"))
+      .def("matvec", &GreenPlan::matvec, py::arg("q"), py::arg("y"), py::arg("precision") = 0,
+           py::arg("stream") = 0)
+      .def("info", &GreenPlan::info);
+
+  m.def("side_tables", [](const Domain& d, const FemSpace& s) {
+    SideTables t = make_side_tables(d, s);
+    py::dict out;
+    out["points"] = points_array(t.qs);
+    out["weights"] = t.qs.weights;
+    out["g"] = t.g;
+    out["nelem"] = t.nelem;
+    out["nloc"] = t.nloc;
+    out["elem_dofs"] = t.elem_dofs;
+    out["basis"] = t.basis;
+    out["nfree"] = t.nfree;
+    return out;
+  });
+  m.def("uniform01", &uniform01);
+  m.def("normal", &normal);
+  m.def("complex_normal", [](uint64_t seed, int64_t n) {
+    auto v = complex_normal(seed, n);
+    return py::array_t<std::complex<double>>((py::ssize_t)v.size(), v.data());
+  });
+  // one-shot C-ABI drop-in with a caller-provided (pinned) host output buffer
+  m.def(
+      "bem_dense_into",
+      [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
+         const BemOptions& o, uintptr_t host_ptr, int64_t lda) {
+        py::gil_scoped_release rel;
+        const SideTables a = make_side_tables(dx, t), b = make_side_tables(dy, u);
+        const gk_side sa = a.abi(), sb = b.abi();
+        const gk_kernel kk = k.abi();
+        gk_options go;
+        gk_options_default(&go);
+        go.memory_cap_bytes = o.memory_cap_bytes;
+        go.chunk = o.chunk;
+        throw_status(gk_bem_dense(&sa, &sb, &kk, &go, reinterpret_cast<gk_cplx*>(host_ptr), lda));
+        return (int64_t)(a.qs.size() * 32 + b.qs.size() * 32 + a.elem_dofs.size() * 4 + b.elem_dofs.size() * 4);
+      },
+      py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"), py::arg("opts"),
+      py::arg("host_ptr"), py::arg("lda"));
+  m.def("diag_fp64_peak", [](int64_t iters, uintptr_t stream) {
+    double g = 0;
+    throw_status(gk_diag_fp64_peak(iters, &g, as_stream(stream)));
+    return g;
+  });
+  m.def("diag_probe_pairs", [](int64_t n, uintptr_t x, uintptr_t y, uintptr_t z, double k, double eps, uintptr_t out,
+                               bool fast, uintptr_t stream) {
+    auto f = fast ? gk_diag_fast_pairs : gk_diag_probe_pairs;
+    throw_status(f(n, reinterpret_cast<const double*>(x), reinterpret_cast<const double*>(y),
+                   reinterpret_cast<const double*>(z), k, eps, reinterpret_cast<gk_cplx*>(out), as_stream(stream)));
+  });
+  m.def("last_error", []() { return std::string(gk_last_error()); });
+  m.def("version", []() { return std::string(gk_version()); });
+  m.attr("FP64") = GK_FP64;
+  m.attr("FP32") = GK_FP32;
+}

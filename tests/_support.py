@@ -33,3 +33,20 @@ def rel_fro(a, b):
     a = np.asarray(a)
     b = np.asarray(b)
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def colmajor_from_torch(t, rows, cols, lda):
+    """Device buffer (complex128, col-major, leading dim lda) -> numpy (rows, cols)."""
+    a = t.detach().cpu().numpy().reshape(cols, lda)
+    return np.ascontiguousarray(a[:, :rows].T)
+
+
+def sphere_problem(g, n_target, gauss, family, perturb_seed=None):
+    """Product-side mesh/domain/space; returns (mesh, dom, space, hbar)."""
+    mesh = g.build_sphere(n_target, 1.0)
+    if perturb_seed is not None:
+        mesh = g.perturb_radial(mesh, perturb_seed, 0.02)
+    dom = g.make_domain(mesh, gauss)
+    space = g.make_fem(mesh, family)
+    hbar = g.edge_stats(mesh).mean_len
+    return mesh, dom, space, hbar

@@ -21,6 +21,18 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: test needs a CUDA B200 device")
 
 
+def pytest_collection_modifyitems(config, items):
+    gpu_items = [it for it in items if "gpu" in it.keywords]
+    if not gpu_items:
+        return
+    import torch
+
+    if not torch.cuda.is_available():
+        skip = pytest.mark.skip(reason="no CUDA device in this container")
+        for it in gpu_items:
+            it.add_marker(skip)
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from tests import _support

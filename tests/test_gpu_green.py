@@ -1,0 +1,57 @@
+"""GPU parity: matrix-free Green-kernel matvec (K5), fp64 and fp32 variants."""
+import math
+
+import numpy as np
+import pytest
+
+from tests._support import rel_fro
+
+pytestmark = pytest.mark.gpu
+FP32_TOL = 2e-4  # stated bound for the complex64/fp32 variant (relative l2)
+
+
+def _setup(galerk, n_target):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m = galerk.build_sphere(n_target, 1.0)
+    dom = galerk.make_domain(m, 3)
+    pts, w, _ = galerk.quadrature(dom)
+    hbar = galerk.edge_stats(m).mean_len
+    k = 2 * math.pi / (10 * hbar)
+    q = np.asarray(w) * galerk.complex_normal(4, len(w))
+    return torch, m, pts, q, k
+
+
+@pytest.mark.parametrize("n_target", [642, 10242])
+def test_green_matvec_fp64_and_fp32(galerk, oracle, n_target):
+    torch, m, pts, q, k = _setup(galerk, n_target)
+    plan = galerk.GreenPlan(pts, pts, galerk.green_kernel("[exp(ikr)/r]", k))
+    info = plan.info()
+    assert info["unique_targets"] == len(pts) // 2  # every point has one bit-identical twin
+    qd = torch.tensor(q, device="cuda")
+    y64 = torch.empty(len(pts), dtype=torch.complex128, device="cuda")
+    y32 = torch.empty_like(y64)
+    plan.matvec(qd.data_ptr(), y64.data_ptr(), galerk.FP64, 0)
+    plan.matvec(qd.data_ptr(), y32.data_ptr(), galerk.FP32, 0)
+    torch.cuda.synchronize()
+    ids = sorted(set(np.random.default_rng(1).choice(len(pts), 64, replace=False).tolist()) | {0, 1})
+    ref = np.array(oracle.green_matvec("[exp(ikr)/r]", k, pts, pts, q, info["eps"], ids, 8))
+    y64n, y32n = y64.cpu().numpy(), y32.cpu().numpy()
+    assert rel_fro(y64n[ids], ref) <= 1e-10
+    assert rel_fro(y32n[ids], ref) <= FP32_TOL
+    # twins get identical outputs
+    assert y64n[0] == y64n[np.flatnonzero((pts == pts[0]).all(axis=1))[-1]]
+
+
+def test_green_matvec_laplace(galerk, oracle):
+    torch, m, pts, q, _ = _setup(galerk, 162)
+    plan = galerk.GreenPlan(pts, pts[::2].copy(), galerk.green_kernel("[1/r]", 0.0))
+    qd = torch.tensor(q[::2].copy(), device="cuda")
+    y = torch.empty(len(pts), dtype=torch.complex128, device="cuda")
+    plan.matvec(qd.data_ptr(), y.data_ptr(), galerk.FP64, 0)
+    torch.cuda.synchronize()
+    ids = list(range(len(pts)))
+    ref = np.array(oracle.green_matvec("[1/r]", 0.0, pts, pts[::2].copy(), q[::2].copy(), plan.info()["eps"], ids, 8))
+    assert rel_fro(y.cpu().numpy(), ref) <= 1e-10
