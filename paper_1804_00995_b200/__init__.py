@@ -52,6 +52,9 @@ radiation_dense = _native.radiation_dense
 regularize = _native.regularize
 AssemblyPlan = _native.AssemblyPlan
 GreenPlan = _native.GreenPlan
+NearField = _native.NearField
+NEAR_REF = _native.NEAR_REF
+NEAR_2HBAR = _native.NEAR_2HBAR
 matvec = _native.matvec
 matvec_launches = _native.matvec_launches
 side_tables = _native.side_tables

@@ -1,35 +1,722 @@
-// K3: near-field singular correction (regularize, assembly.cpp:609-697).
-// Placeholder entry points until the device implementation lands.
+// K3: near-field singular correction — regularize (assembly.cpp:609-697).
+//
+// For every near element pair (close_pairs, assembly.cpp:370-401) the
+// correction is  local = semi-analytic(1/r) - Gauss x Gauss(1/r)  on the pair's
+// local dofs; duplicates are summed in pair order (setFromTriplets).
+//
+// Device layout: one warp per near pair, pairs handed out by an atomic work
+// counter (costs range from ~500 to ~50k analytic integrals per pair; the
+// processing order does not change any result).  The recursion of
+// accurate_adaptive (:581-605) runs on an explicit per-warp stack in shared
+// memory in the same depth-first order as the reference.  Each node needs the
+// 4 sub-cells x 7 points = 28 analytic_triangle_integrals calls
+// (kernels.cpp:151-207) — one per lane — and the parent's 'whole' value is the
+// child's sub-cell value, so it is carried on the stack instead of being
+// recomputed (the reference recomputes it: ~20% of its calls).  Per-triangle
+// quantities of the y element (normal, edge frames) are computed once per pair.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <map>
+#include <memory>
+
 #include "gk_internal.hpp"
+
+namespace gk {
+namespace {
+
+constexpr int kNfWarps = 4;       // warps per CTA
+constexpr int kStack = 32;        // DFS stack entries per warp (depth <= 6 -> <= 3*6+4)
+constexpr int kMaxLoc = 9;        // local matrix entries (P1 x P1)
+
+struct V3 {
+  double x, y, z;
+};
+__device__ __forceinline__ V3 mk(double a, double b, double c) { return {a, b, c}; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 operator*(double s, V3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double nrm(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+
+// y-triangle frame shared by all analytic calls of a pair
+struct YTri {
+  V3 v[3];       // A, B, C
+  V3 n;          // unit normal
+  V3 s_hat[3], m_hat[3];
+  double len[3];
+  V3 g_bary[3];  // P1 tangential barycentric gradients (femspace.cpp:254-277)
+};
+
+struct NfArgs {
+  int64_t npairs;
+  const int32_t* pair_ex;
+  const int32_t* pair_ey;
+  const double* xv;  // x mesh vertices [nv*3]
+  const int32_t* xe; // x mesh elements [ne*3]
+  const double* yv;
+  const int32_t* ye;
+  const double* xq;  // x quadrature per point: x,y,z,w  [nex*gx*4]
+  const double* yq;  // y quadrature per point
+  int gx, gy;
+  double eps;
+  double* local;     // [npairs * kMaxLoc]
+  unsigned long long* work;   // atomic pair counter
+  unsigned long long* stats;  // [0] analytic calls, [1..7] leaves per depth, [8] degenerate flag
+};
+
+__constant__ double c_r7_bary[7][3];
+__constant__ double c_r7_w[7];
+__constant__ double c_xrule_bary[7][3];
+__constant__ double c_yrule_bary[7][3];
+
+struct Node {
+  double corners[9];
+  double whole[kMaxLoc];
+  double frac, tol;
+  int depth;
+};
+
+struct WarpSmem {
+  Node stack[kStack];
+  double vals[32][kMaxLoc];
+  double subs[4][kMaxLoc];
+  double acc[kMaxLoc];
+  YTri tri;
+};
+
+__device__ void analytic(const YTri& T, V3 x, double& newton, V3& moment, V3& rho) {
+  // kernels.cpp:151-207 with the y-triangle frame precomputed
+  const double w0 = dot(x - T.v[0], T.n), aw0 = fabs(w0);
+  rho = x - w0 * T.n;
+  double nw = 0.0;
+  V3 mom = mk(0, 0, 0);
+  double rv[3];
+  for (int i = 0; i < 3; ++i) rv[i] = nrm(x - T.v[i]);  // rp of edge i == rm of edge i+1
+  for (int i = 0; i < 3; ++i) {
+    const int ip = i == 2 ? 0 : i + 1;
+    if (T.len[i] <= 1e-300) continue;
+    const V3 pm = T.v[i], pp = T.v[ip];
+    const double t = dot(pm - rho, T.m_hat[i]);
+    const double sm = dot(pm - rho, T.s_hat[i]);
+    const double sp = dot(pp - rho, T.s_hat[i]);
+    const double rm = rv[i], rp = rv[ip];
+    const double r0sq = t * t + w0 * w0;
+    double f = 0.0;
+    if (r0sq > 1e-28 * T.len[i] * T.len[i]) {
+      if (sm >= 0.0)
+        f = log((rp + sp) / (rm + sm));
+      else if (sp <= 0.0)
+        f = log((rm - sm) / (rp - sp));
+      else
+        f = log((rp + sp) * (rm - sm) / r0sq);
+    }
+    const double beta = atan(t * sp / (r0sq + aw0 * rp)) - atan(t * sm / (r0sq + aw0 * rm));
+    nw += t * f - aw0 * beta;
+    const double mo = r0sq * f + sp * rp - sm * rm;
+    mom = mom + mo * (0.5 * T.m_hat[i]);
+  }
+  newton = nw;
+  moment = mom;
+}
+
+// barycentric corners of sub-cell s (assembly.cpp:587-594):
+// sub[0]=(c0,m01,m20) sub[1]=(c1,m12,m01) sub[2]=(c2,m20,m12) sub[3]=(m01,m12,m20)
+__device__ __forceinline__ void sub_corners(const double* c, int s, double o[9]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double c0 = c[k], c1 = c[3 + k], c2 = c[6 + k];
+    const double m01 = 0.5 * (c0 + c1), m12 = 0.5 * (c1 + c2), m20 = 0.5 * (c2 + c0);
+    o[k] = s == 0 ? c0 : s == 1 ? c1 : s == 2 ? c2 : m01;
+    o[3 + k] = s == 0 ? m01 : s == 1 ? m12 : s == 2 ? m20 : m12;
+    o[6 + k] = s == 0 ? m20 : s == 1 ? m01 : s == 2 ? m12 : m20;
+  }
+}
+
+template <int NT, int NTR>
+__device__ __forceinline__ void exact_values(const YTri& T, double newton, V3 moment, V3 rho, double d[NTR]) {
+  if (NTR == 1) {
+    d[0] = newton;
+  } else {
+    // lam_at_rho (assembly.cpp:455-466): (E^T E) uv = E^T (rho - A), pivoted LDLT
+    const V3 e0 = T.v[1] - T.v[0], e1 = T.v[2] - T.v[0], dd = rho - T.v[0];
+    double m00 = dot(e0, e0), m01 = dot(e0, e1), m11 = dot(e1, e1);
+    double r0 = dot(e0, dd), r1 = dot(e1, dd);
+    const bool sw = fabs(m11) > fabs(m00);
+    if (sw) {
+      double tt = m00;
+      m00 = m11;
+      m11 = tt;
+      tt = r0;
+      r0 = r1;
+      r1 = tt;
+    }
+    const double d0 = m00, l10 = m01 / d0, d1 = m11 - l10 * l10 * d0;
+    const double z0 = r0, z1 = r1 - l10 * z0;
+    const double y1 = z1 / d1, y0 = z0 / d0;
+    double u1 = y1, u0 = y0 - l10 * u1;
+    if (sw) {
+      const double tt = u0;
+      u0 = u1;
+      u1 = tt;
+    }
+    const double lam[3] = {1.0 - u0 - u1, u0, u1};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) d[j] = lam[j] * newton + dot(T.g_bary[j], moment);
+  }
+}
+
+template <int NT, int NTR>
+__global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  constexpr int NL = NT * NTR;
+  while (true) {
+    unsigned long long p = 0;
+    if (lane == 0) p = atomicAdd(a.work, 1ull);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= (unsigned long long)a.npairs) break;
+    const int ex = a.pair_ex[p], ey = a.pair_ey[p];
+    // ---- y triangle frame (lane 0), kernels.cpp:153-175
+    if (lane == 0) {
+      YTri& T = S.tri;
+      for (int c = 0; c < 3; ++c) {
+        const int vi = a.ye[3 * ey + c];
+        T.v[c] = mk(a.yv[3 * vi], a.yv[3 * vi + 1], a.yv[3 * vi + 2]);
+      }
+      const V3 cr = cross(T.v[1] - T.v[0], T.v[2] - T.v[0]);
+      const double area2 = nrm(cr);
+      const double diam = fmax(fmax(nrm(T.v[1] - T.v[0]), nrm(T.v[2] - T.v[1])), nrm(T.v[0] - T.v[2]));
+      if (area2 <= 1e-14 * diam * diam) atomicExch(a.stats + 8, 1ull);
+      T.n = (1.0 / area2) * cr;
+      T.n = mk(cr.x / area2, cr.y / area2, cr.z / area2);
+      for (int i = 0; i < 3; ++i) {
+        const V3 pm = T.v[i], pp = T.v[i == 2 ? 0 : i + 1];
+        const double len = nrm(pp - pm);
+        T.len[i] = len;
+        const V3 d = pp - pm;
+        T.s_hat[i] = mk(d.x / len, d.y / len, d.z / len);
+        T.m_hat[i] = cross(T.s_hat[i], T.n);
+      }
+      if (NTR == 3) {
+        const V3 e1 = T.v[1] - T.v[0], e2 = T.v[2] - T.v[0];
+        const double g00 = dot(e1, e1), g01 = dot(e1, e2), g11 = dot(e2, e2);
+        const double det = g00 * g11 - g01 * g01;
+        const double i00 = g11 / det, i01 = -g01 / det, i11 = g00 / det;
+        T.g_bary[1] = mk(e1.x * i00 + e2.x * i01, e1.y * i00 + e2.y * i01, e1.z * i00 + e2.z * i01);
+        T.g_bary[2] = mk(e1.x * i01 + e2.x * i11, e1.y * i01 + e2.y * i11, e1.z * i01 + e2.z * i11);
+        T.g_bary[0] = mk(0, 0, 0) - T.g_bary[1] - T.g_bary[2];
+      }
+    }
+    __syncwarp();
+    const YTri& T = S.tri;
+    V3 xv[3];
+    for (int c = 0; c < 3; ++c) {
+      const int vi = a.xe[3 * ex + c];
+      xv[c] = mk(a.xv[3 * vi], a.xv[3 * vi + 1], a.xv[3 * vi + 2]);
+    }
+    const double measure_x = 0.5 * nrm(cross(xv[1] - xv[0], xv[2] - xv[0]));
+
+    // ---- Gauss x Gauss part (assembly.cpp:659-674, YContext::gauss :504-543)
+    if (lane < a.gx) {
+      const double* xq = a.xq + ((int64_t)ex * a.gx + lane) * 4;
+      const V3 x = mk(xq[0], xq[1], xq[2]);
+      const double w = xq[3];
+      double d[NTR];
+#pragma unroll
+      for (int j = 0; j < NTR; ++j) d[j] = 0.0;
+      for (int l = 0; l < a.gy; ++l) {
+        const double* yq = a.yq + ((int64_t)ey * a.gy + l) * 4;
+        const double r = nrm(x - mk(yq[0], yq[1], yq[2]));
+        if (r <= a.eps) continue;
+        const double kv = 1.0 / r;
+#pragma unroll
+        for (int j = 0; j < NTR; ++j) {
+          const double psi = NTR == 1 ? 1.0 : c_yrule_bary[l][j];
+          d[j] += yq[3] * kv * psi;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const double tv = NT == 1 ? 1.0 : c_xrule_bary[lane][i];
+#pragma unroll
+        for (int j = 0; j < NTR; ++j) S.vals[lane][i * NTR + j] = -(w * (tv * d[j]));
+      }
+    }
+    __syncwarp();
+    if (lane < NL) {  // local(i,j) -= w * acc, in x-point order
+      double s = 0.0;
+      for (int k = 0; k < a.gx; ++k) s += S.vals[k][lane];
+      S.acc[lane] = s;  // holds the Gauss part until the adaptive part is added
+    }
+    __syncwarp();
+
+    // ---- probe = accurate_cell(whole) (lanes 0..6)
+    double pv[NL];
+    {
+      if (lane < 7) {
+        const double* b = c_r7_bary[lane];
+        const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
+        const double w = c_r7_w[lane] * (measure_x * 1.0);
+        double nw;
+        V3 mo, rho;
+        analytic(T, x, nw, mo, rho);
+        double d[NTR];
+        exact_values<NT, NTR>(T, nw, mo, rho, d);
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int j = 0; j < NTR; ++j) S.vals[lane][i * NTR + j] = w * ((NT == 1 ? 1.0 : b[i]) * d[j]);
+      }
+      __syncwarp();
+      double pmax = 0.0;
+#pragma unroll
+      for (int t = 0; t < NL; ++t) {
+        double s = 0.0;
+        for (int q = 0; q < 7; ++q) s += S.vals[q][t];
+        pv[t] = s;
+        pmax = fmax(pmax, fabs(s));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        Node& r = S.stack[0];
+        const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        for (int c = 0; c < 9; ++c) r.corners[c] = I[c];
+        for (int t = 0; t < NL; ++t) r.whole[t] = pv[t];
+        r.frac = 1.0;
+        r.tol = 1e-8 * fmax(pmax, 1e-300);
+        r.depth = 0;
+      }
+    }
+    double adapt[NL];
+#pragma unroll
+    for (int t = 0; t < NL; ++t) adapt[t] = 0.0;
+    int sp = 1;
+    unsigned long long calls = 7;
+    __syncwarp();
+    // ---- accurate_adaptive (assembly.cpp:581-605), explicit DFS stack
+    while (sp > 0) {
+      --sp;
+      const Node nd = S.stack[sp];
+      __syncwarp();
+      const double frac = 0.25 * nd.frac;
+      if (lane < 28) {
+        const int sub = lane / 7, q = lane - 7 * sub;
+        double cr[9];
+        sub_corners(nd.corners, sub, cr);
+        double b[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          b[c] = c_r7_bary[q][0] * cr[c] + c_r7_bary[q][1] * cr[3 + c] + c_r7_bary[q][2] * cr[6 + c];
+        const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
+        const double w = c_r7_w[q] * (measure_x * frac);
+        double nw;
+        V3 mo, rho;
+        analytic(T, x, nw, mo, rho);
+        double d[NTR];
+        exact_values<NT, NTR>(T, nw, mo, rho, d);
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int j = 0; j < NTR; ++j) S.vals[lane][i * NTR + j] = w * ((NT == 1 ? 1.0 : b[i]) * d[j]);
+      }
+      calls += 28;
+      __syncwarp();
+      for (int e = lane; e < 4 * NL; e += 32) {  // sub-cell sums in q order (accurate_cell :562-575)
+        const int sub = e / NL, t = e - sub * NL;
+        double s = 0.0;
+        for (int q = 0; q < 7; ++q) s += S.vals[sub * 7 + q][t];
+        S.subs[sub][t] = s;
+      }
+      __syncwarp();
+      double split[NL];
+      double dmax = 0.0;
+#pragma unroll
+      for (int t = 0; t < NL; ++t) {
+        split[t] = 0.0 + S.subs[0][t] + S.subs[1][t] + S.subs[2][t] + S.subs[3][t];
+        dmax = fmax(dmax, fabs(split[t] - nd.whole[t]));
+      }
+      if (dmax <= nd.tol || nd.depth >= 6) {
+#pragma unroll
+        for (int t = 0; t < NL; ++t) adapt[t] += split[t];
+        if (lane == 0) atomicAdd(a.stats + 1 + min(nd.depth, 6), 1ull);
+      } else {
+        if (lane < 4) {  // push children 3..0 so that sub 0 is processed first
+          const int s = 3 - lane;
+          Node& ch = S.stack[sp + lane];
+          double cr[9];
+          sub_corners(nd.corners, s, cr);
+#pragma unroll
+          for (int c = 0; c < 9; ++c) ch.corners[c] = cr[c];
+          for (int t = 0; t < NL; ++t) ch.whole[t] = S.subs[s][t];
+          ch.frac = frac;
+          ch.tol = 0.5 * nd.tol;
+          ch.depth = nd.depth + 1;
+        }
+        sp += 4;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      for (int t = 0; t < NL; ++t) a.local[p * kMaxLoc + t] = S.acc[t] + adapt[t];
+      atomicAdd(a.stats, calls);
+    }
+    __syncwarp();
+  }
+}
+
+// A[row + col*lda].re += sum of the entry's contributions in pair order
+__global__ void k_nf_reduce(int64_t n, const int64_t* __restrict__ start, const int64_t* __restrict__ src,
+                            const double* __restrict__ local, double* __restrict__ vals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = local[src[start[e]]];
+  for (int64_t p = start[e] + 1; p < start[e + 1]; ++p) s += local[src[p]];
+  vals[e] = s;
+}
+
+__global__ void k_nf_apply(int64_t n, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                           const double* __restrict__ vals, double2* __restrict__ A, long long lda) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double2* a = A + row[e] + (long long)col[e] * lda;
+  a->x += vals[e];
+}
+
+// ---- host helpers ---------------------------------------------------------------
+struct HV3 {
+  double x, y, z;
+};
+HV3 hsub(HV3 a, HV3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+double hnrm(HV3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+HV3 hcross(HV3 a, HV3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+
+struct HostMesh {
+  const double* v;
+  const int32_t* e;
+  int64_t nv, ne;
+  HV3 vert(int64_t e_, int c) const {
+    const int i = e[3 * e_ + c];
+    return {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+  }
+  HV3 centroid(int64_t k) const {  // mesh.cpp:73-78
+    HV3 c{0, 0, 0};
+    for (int i = 0; i < 3; ++i) {
+      const HV3 p = vert(k, i);
+      c = {c.x + p.x, c.y + p.y, c.z + p.z};
+    }
+    return {c.x / 3.0, c.y / 3.0, c.z / 3.0};
+  }
+  double circumradius(int64_t k) const {  // assembly.cpp:358-366
+    const HV3 a = vert(k, 0), b = vert(k, 1), c = vert(k, 2);
+    const double area = 0.5 * hnrm(hcross(hsub(b, a), hsub(c, a)));
+    if (area <= 0.0) {
+      const HV3 cc = centroid(k);
+      double r = 0.0;
+      for (int i = 0; i < 3; ++i) r = std::max(r, hnrm(hsub(vert(k, i), cc)));
+      return r;
+    }
+    return hnrm(hsub(a, b)) * hnrm(hsub(b, c)) * hnrm(hsub(c, a)) / (4.0 * area);
+  }
+};
+
+std::vector<double> host_rule(int n, bool weights) {
+  // triangle rules as in csrc/host/galerk.cpp (1/3/6/7 points)
+  std::vector<double> b, w;
+  auto orbit = [&](double a, double wt) {
+    const double c = 1.0 - 2.0 * a;
+    const double pts[3][3] = {{a, a, c}, {a, c, a}, {c, a, a}};
+    for (auto& p : pts) b.insert(b.end(), p, p + 3), w.push_back(wt);
+  };
+  if (n == 1) {
+    b = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+    w = {1.0};
+  } else if (n == 3) {
+    b = {0.5, 0.5, 0.0, 0.0, 0.5, 0.5, 0.5, 0.0, 0.5};
+    w = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+  } else if (n == 6) {
+    orbit(0.44594849091596488632, 0.22338158967801146570);
+    orbit(0.091576213509770743460, 0.10995174365532186764);
+  } else if (n == 7) {
+    const double s15 = std::sqrt(15.0);
+    b = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+    w = {9.0 / 40.0};
+    orbit((6.0 - s15) / 21.0, (155.0 - s15) / 1200.0);
+    orbit((6.0 + s15) / 21.0, (155.0 + s15) / 1200.0);
+  } else {
+    throw std::invalid_argument("regularize: unsupported quadrature rule");
+  }
+  return weights ? w : b;
+}
+
+std::vector<double> host_quadrature(const HostMesh& m, int g) {  // quadrature.cpp:167-189, x,y,z,w
+  const std::vector<double> b = host_rule(g, false), w = host_rule(g, true);
+  std::vector<double> out((size_t)m.ne * g * 4);
+  for (int64_t e = 0; e < m.ne; ++e) {
+    const HV3 a = m.vert(e, 0), bb = m.vert(e, 1), c = m.vert(e, 2);
+    const double measure = 0.5 * hnrm(hcross(hsub(bb, a), hsub(c, a)));
+    const HV3 vs[3] = {a, bb, c};
+    for (int q = 0; q < g; ++q) {
+      HV3 p{0, 0, 0};
+      for (int k = 0; k < 3; ++k) {
+        const double s = b[3 * q + k];
+        p = {p.x + s * vs[k].x, p.y + s * vs[k].y, p.z + s * vs[k].z};
+      }
+      double* o = &out[((size_t)e * g + q) * 4];
+      o[0] = p.x;
+      o[1] = p.y;
+      o[2] = p.z;
+      o[3] = w[q] * measure;
+    }
+  }
+  return out;
+}
+
+}  // namespace
+}  // namespace gk
 
 using namespace gk;
 
-struct gk_nearfield {};
+struct gk_nearfield {
+  int fx = 0, fy = 0, gx = 0, gy = 0, nt = 1, ntr = 1;
+  int64_t npairs = 0, nentries = 0;
+  double eps = 0.0;
+  DevBuf pair_ex, pair_ey, xv, xe, yv, ye, xq, yq, local, work, stats, ent_row, ent_col, ent_start, ent_src, vals;
+  std::vector<int32_t> h_row, h_col;
+  bool computed = false;
+};
 
 extern "C" {
-gk_status gk_nearfield_create(const gk_mesh_side*, const gk_mesh_side*, const char*, int32_t, double,
-                              gk_nearfield** out) {
+
+gk_status gk_nearfield_create(const gk_mesh_side* test, const gk_mesh_side* trial, const char* singular_name,
+                              int32_t near_rule, double hbar, gk_nearfield** out) {
   return guard([&] {
-    if (out) *out = nullptr;
-    throw std::runtime_error("gk_nearfield_create: device near-field correction not built yet");
+    if (!out) throw std::invalid_argument("gk_nearfield_create: null output");
+    *out = nullptr;
+    const std::string name = singular_name ? singular_name : "";
+    if (name != "[1/r]") {  // assembly.cpp:611-614
+      if (name == "grady[1/r]")
+        throw std::invalid_argument("regularize: grady[1/r] (MFIE/CFIE) is outside the B200 hot path");
+      throw std::invalid_argument("regularize: unsupported singular kernel '" + name + "'");
+    }
+    if (!test || !trial) throw std::invalid_argument("regularize: null side");
+    for (const gk_mesh_side* s : {test, trial}) {
+      if (s->family != 0 && s->family != 1)
+        throw std::invalid_argument("regularize: unsupported trial family/operator combination");
+      if (s->ne <= 0 || !s->vertices || !s->elements) throw std::invalid_argument("regularize: empty mesh");
+    }
+    if (near_rule != GK_NEAR_REF && near_rule != GK_NEAR_2HBAR)
+      throw std::invalid_argument("regularize: unknown near-field rule");
+    require_device();
+    auto N = std::make_unique<gk_nearfield>();
+    N->fx = test->family;
+    N->fy = trial->family;
+    N->gx = test->g;
+    N->gy = trial->g;
+    N->nt = N->fx == 0 ? 1 : 3;
+    N->ntr = N->fy == 0 ? 1 : 3;
+    const HostMesh mx{test->vertices, test->elements, test->nv, test->ne};
+    const HostMesh my{trial->vertices, trial->elements, trial->nv, trial->ne};
+    const std::vector<double> xq = host_quadrature(mx, N->gx), yq = host_quadrature(my, N->gy);
+    // eps over both point sets (kernels.cpp:14-19)
+    {
+      const int64_t na = mx.ne * N->gx, nb = my.ne * N->gy;
+      std::vector<double> ax(na), ay(na), az(na), bx(nb), by(nb), bz(nb);
+      for (int64_t i = 0; i < na; ++i) ax[i] = xq[4 * i], ay[i] = xq[4 * i + 1], az[i] = xq[4 * i + 2];
+      for (int64_t i = 0; i < nb; ++i) bx[i] = yq[4 * i], by[i] = yq[4 * i + 1], bz[i] = yq[4 * i + 2];
+      N->eps = guard_radius_pts(na, ax.data(), ay.data(), az.data(), nb, bx.data(), by.data(), bz.data());
+    }
+    // close_pairs (assembly.cpp:370-401): hash grid of y centroids, 27-cell probe
+    std::vector<HV3> xc(mx.ne), yc(my.ne);
+    std::vector<double> xr(mx.ne), yr(my.ne);
+    double rmax = 0.0;
+    for (int64_t e = 0; e < mx.ne; ++e) xc[e] = mx.centroid(e), xr[e] = mx.circumradius(e), rmax = std::max(rmax, xr[e]);
+    for (int64_t e = 0; e < my.ne; ++e) yc[e] = my.centroid(e), yr[e] = my.circumradius(e), rmax = std::max(rmax, yr[e]);
+    double cell = std::max(3.0 * rmax, 1e-300);
+    if (near_rule == GK_NEAR_2HBAR) cell = std::max(cell, 2.0 * hbar);
+    auto key = [cell](const HV3& p) {
+      return std::array<int64_t, 3>{(int64_t)std::floor(p.x / cell), (int64_t)std::floor(p.y / cell),
+                                    (int64_t)std::floor(p.z / cell)};
+    };
+    std::map<std::array<int64_t, 3>, std::vector<int>> grid;
+    for (int64_t e = 0; e < my.ne; ++e) grid[key(yc[e])].push_back((int)e);
+    std::vector<int32_t> pex, pey;
+    for (int64_t i = 0; i < mx.ne; ++i) {
+      const auto k = key(xc[i]);
+      for (int64_t dx = -1; dx <= 1; ++dx)
+        for (int64_t dy = -1; dy <= 1; ++dy)
+          for (int64_t dz = -1; dz <= 1; ++dz) {
+            const auto it = grid.find({k[0] + dx, k[1] + dy, k[2] + dz});
+            if (it == grid.end()) continue;
+            for (int e : it->second) {
+              const double radius = near_rule == GK_NEAR_REF ? 3.0 * std::max(xr[i], yr[e]) : 2.0 * hbar;
+              if (hnrm(hsub(yc[e], xc[i])) <= radius) {
+                pex.push_back((int32_t)i);
+                pey.push_back(e);
+              }
+            }
+          }
+    }
+    N->npairs = (int64_t)pex.size();
+    // summed entries (setFromTriplets): col-major order, contributions in pair order
+    std::map<std::pair<int32_t, int32_t>, std::vector<int64_t>> ent;
+    for (int64_t p = 0; p < N->npairs; ++p)
+      for (int i = 0; i < N->nt; ++i)
+        for (int j = 0; j < N->ntr; ++j) {
+          const int32_t r = N->fx == 0 ? pex[p] : test->elements[3 * pex[p] + i];
+          const int32_t c = N->fy == 0 ? pey[p] : trial->elements[3 * pey[p] + j];
+          if (r >= test->nfree || c >= trial->nfree) throw std::invalid_argument("regularize: dof out of range");
+          ent[{c, r}].push_back(p * kMaxLoc + i * N->ntr + j);
+        }
+    N->nentries = (int64_t)ent.size();
+    std::vector<int64_t> start{0}, src;
+    for (auto& [k, v] : ent) {
+      N->h_col.push_back(k.first);
+      N->h_row.push_back(k.second);
+      src.insert(src.end(), v.begin(), v.end());
+      start.push_back((int64_t)src.size());
+    }
+    N->pair_ex.upload(pex);
+    N->pair_ey.upload(pey);
+    N->xv.upload(test->vertices, sizeof(double) * 3 * test->nv);
+    N->xe.upload(test->elements, sizeof(int32_t) * 3 * test->ne);
+    N->yv.upload(trial->vertices, sizeof(double) * 3 * trial->nv);
+    N->ye.upload(trial->elements, sizeof(int32_t) * 3 * trial->ne);
+    N->xq.upload(xq);
+    N->yq.upload(yq);
+    N->local.alloc(sizeof(double) * kMaxLoc * std::max<int64_t>(1, N->npairs));
+    N->work.alloc(sizeof(unsigned long long));
+    N->stats.alloc(sizeof(unsigned long long) * 9);
+    N->ent_row.upload(N->h_row);
+    N->ent_col.upload(N->h_col);
+    N->ent_start.upload(start);
+    N->ent_src.upload(src);
+    N->vals.alloc(sizeof(double) * std::max<int64_t>(1, N->nentries));
+    // rule tables
+    const std::vector<double> b7 = host_rule(7, false), w7 = host_rule(7, true);
+    double bx[21] = {0}, by[21] = {0};
+    const std::vector<double> rbx = host_rule(N->gx, false), rby = host_rule(N->gy, false);
+    std::copy(rbx.begin(), rbx.end(), bx);
+    std::copy(rby.begin(), rby.end(), by);
+    cuda_check(cudaMemcpyToSymbol(c_r7_bary, b7.data(), sizeof(double) * 21), "rule7");
+    cuda_check(cudaMemcpyToSymbol(c_r7_w, w7.data(), sizeof(double) * 7), "rule7w");
+    cuda_check(cudaMemcpyToSymbol(c_xrule_bary, bx, sizeof(double) * 21), "xrule");
+    cuda_check(cudaMemcpyToSymbol(c_yrule_bary, by, sizeof(double) * 21), "yrule");
+    *out = N.release();
   });
 }
-gk_status gk_nearfield_get_info(const gk_nearfield*, int64_t*, int64_t*) {
-  return guard([&] { throw std::runtime_error("gk_nearfield: not built"); });
+
+gk_status gk_nearfield_get_info(const gk_nearfield* N, int64_t* pairs, int64_t* entries) {
+  return guard([&] {
+    if (!N) throw std::invalid_argument("gk_nearfield_get_info: null handle");
+    if (pairs) *pairs = N->npairs;
+    if (entries) *entries = N->nentries;
+  });
 }
-gk_status gk_nearfield_compute(gk_nearfield*, gk_stream) {
-  return guard([&] { throw std::runtime_error("gk_nearfield: not built"); });
+
+gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
+  return guard([&] {
+    if (!N) throw std::invalid_argument("gk_nearfield_compute: null handle");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaMemsetAsync(N->work.p, 0, N->work.bytes, s), "memset");
+    cuda_check(cudaMemsetAsync(N->stats.p, 0, N->stats.bytes, s), "memset");
+    if (N->npairs > 0) {
+      NfArgs a;
+      a.npairs = N->npairs;
+      a.pair_ex = N->pair_ex.as<int32_t>();
+      a.pair_ey = N->pair_ey.as<int32_t>();
+      a.xv = N->xv.as<double>();
+      a.xe = N->xe.as<int32_t>();
+      a.yv = N->yv.as<double>();
+      a.ye = N->ye.as<int32_t>();
+      a.xq = N->xq.as<double>();
+      a.yq = N->yq.as<double>();
+      a.gx = N->gx;
+      a.gy = N->gy;
+      a.eps = N->eps;
+      a.local = N->local.as<double>();
+      a.work = N->work.as<unsigned long long>();
+      a.stats = N->stats.as<unsigned long long>();
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const size_t smem = sizeof(WarpSmem) * kNfWarps;
+      auto launch = [&](auto kern) {
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kNfWarps, smem);
+        const int64_t want = (N->npairs + kNfWarps - 1) / kNfWarps;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(1, per_sm)));
+        kern<<<grid, 32 * kNfWarps, smem, s>>>(a);
+      };
+      if (N->nt == 1 && N->ntr == 1)
+        launch(k_nearfield<1, 1>);
+      else if (N->nt == 3 && N->ntr == 3)
+        launch(k_nearfield<3, 3>);
+      else if (N->nt == 1)
+        launch(k_nearfield<1, 3>);
+      else
+        launch(k_nearfield<3, 1>);
+      cuda_check(cudaGetLastError(), "k_nearfield launch");
+    }
+    if (N->nentries > 0) {
+      k_nf_reduce<<<(unsigned)((N->nentries + 255) / 256), 256, 0, s>>>(
+          N->nentries, N->ent_start.as<int64_t>(), N->ent_src.as<int64_t>(), N->local.as<double>(),
+          N->vals.as<double>());
+      cuda_check(cudaGetLastError(), "k_nf_reduce launch");
+    }
+    N->computed = true;
+  });
 }
-gk_status gk_nearfield_apply(gk_nearfield*, gk_cplx*, int64_t, gk_stream) {
-  return guard([&] { throw std::runtime_error("gk_nearfield: not built"); });
+
+gk_status gk_nearfield_apply(gk_nearfield* N, gk_cplx* A, int64_t lda, gk_stream stream) {
+  return guard([&] {
+    if (!N || !A) throw std::invalid_argument("gk_nearfield_apply: null argument");
+    if (!N->computed) throw std::invalid_argument("gk_nearfield_apply: call gk_nearfield_compute first");
+    if (N->nentries == 0) return;
+    k_nf_apply<<<(unsigned)((N->nentries + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        N->nentries, N->ent_row.as<int32_t>(), N->ent_col.as<int32_t>(), N->vals.as<double>(),
+        reinterpret_cast<double2*>(A), lda);
+    cuda_check(cudaGetLastError(), "k_nf_apply launch");
+  });
 }
-gk_status gk_nearfield_triplets(gk_nearfield*, int32_t*, int32_t*, double*) {
-  return guard([&] { throw std::runtime_error("gk_nearfield: not built"); });
+
+gk_status gk_nearfield_triplets(gk_nearfield* N, int32_t* rows, int32_t* cols, double* vals) {
+  return guard([&] {
+    if (!N) throw std::invalid_argument("gk_nearfield_triplets: null handle");
+    if (!N->computed) throw std::invalid_argument("gk_nearfield_triplets: call gk_nearfield_compute first");
+    unsigned long long flag = 0;
+    cuda_check(cudaMemcpy(&flag, N->stats.as<unsigned long long>() + 8, sizeof(flag), cudaMemcpyDeviceToHost),
+               "stats");
+    if (flag) throw std::invalid_argument("analytic_triangle_integrals: degenerate triangle");
+    if (N->nentries == 0) return;
+    if (rows) std::copy(N->h_row.begin(), N->h_row.end(), rows);
+    if (cols) std::copy(N->h_col.begin(), N->h_col.end(), cols);
+    if (vals) cuda_check(cudaMemcpy(vals, N->vals.p, sizeof(double) * N->nentries, cudaMemcpyDeviceToHost), "vals");
+  });
 }
-gk_status gk_nearfield_stats(const gk_nearfield*, int64_t*, int64_t*) {
-  return guard([&] { throw std::runtime_error("gk_nearfield: not built"); });
+
+gk_status gk_nearfield_stats(const gk_nearfield* N, int64_t* calls, int64_t* hist) {
+  return guard([&] {
+    if (!N) throw std::invalid_argument("gk_nearfield_stats: null handle");
+    unsigned long long s[9];
+    cuda_check(cudaMemcpy(s, N->stats.p, sizeof(s), cudaMemcpyDeviceToHost), "stats");
+    if (calls) *calls = (int64_t)s[0];
+    if (hist) {
+      for (int d = 0; d < 7; ++d) hist[d] = (int64_t)s[1 + d];
+      hist[7] = 0;
+    }
+  });
 }
-gk_status gk_nearfield_destroy(gk_nearfield* nf) {
-  return guard([&] { delete nf; });
+
+gk_status gk_nearfield_destroy(gk_nearfield* N) {
+  return guard([&] { delete N; });
 }
-}
+
+}  // extern "C"

@@ -103,6 +103,57 @@ class GreenPlan {
  private:
   gk_green_plan* p_ = nullptr;
 };
+
+gk_mesh_side mesh_side(const Domain& d, const FemSpace& s) {
+  gk_mesh_side m;
+  m.nv = d.mesh.vertex_count();
+  m.vertices = d.mesh.vertices.data();
+  m.ne = d.mesh.element_count();
+  m.elements = d.mesh.elements.data();
+  m.family = s.family() == Family::P0 ? 0 : 1;
+  m.g = d.gauss_count;
+  m.nfree = s.free_count();
+  return m;
+}
+
+// Device near-field correction (regularize) with in-place apply.
+class NearField {
+ public:
+  NearField(const Domain& dx, const Domain& dy, const FemSpace& t, const std::string& name, const FemSpace& u,
+            int rule, double hbar) {
+    const gk_mesh_side a = mesh_side(dx, t), b = mesh_side(dy, u);
+    throw_status(gk_nearfield_create(&a, &b, name.c_str(), rule, hbar, &p_));
+  }
+  ~NearField() {
+    if (p_) gk_nearfield_destroy(p_);
+  }
+  void compute(uintptr_t stream) { throw_status(gk_nearfield_compute(p_, as_stream(stream))); }
+  void apply(uintptr_t A, int64_t lda, uintptr_t stream) {
+    throw_status(gk_nearfield_apply(p_, reinterpret_cast<gk_cplx*>(A), lda, as_stream(stream)));
+  }
+  py::tuple info() const {
+    int64_t pairs = 0, entries = 0;
+    throw_status(gk_nearfield_get_info(p_, &pairs, &entries));
+    return py::make_tuple(pairs, entries);
+  }
+  py::tuple triplets() {
+    int64_t pairs = 0, entries = 0;
+    throw_status(gk_nearfield_get_info(p_, &pairs, &entries));
+    std::vector<int32_t> r(entries), c(entries);
+    std::vector<double> v(entries);
+    throw_status(gk_stream_synchronize(nullptr));
+    throw_status(gk_nearfield_triplets(p_, r.data(), c.data(), v.data()));
+    return py::make_tuple(r, c, v);
+  }
+  py::tuple stats() const {
+    int64_t calls = 0, hist[8] = {0};
+    throw_status(gk_nearfield_stats(p_, &calls, hist));
+    return py::make_tuple(calls, std::vector<int64_t>(hist, hist + 8));
+  }
+
+ private:
+  gk_nearfield* p_ = nullptr;
+};
 }  // namespace
 
 PYBIND11_MODULE(_galerk, m) {
@@ -241,6 +292,19 @@ PYBIND11_MODULE(_galerk, m) {
       .def("matvec", &GreenPlan::matvec, py::arg("q"), py::arg("y"), py::arg("precision") = 0,
            py::arg("stream") = 0)
       .def("info", &GreenPlan::info);
+
+  py::class_<NearField>(m, "NearField")
+      .def(py::init<const Domain&, const Domain&, const FemSpace&, const std::string&, const FemSpace&, int,
+                    double>(),
+           py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("singular_name"), py::arg("trial"),
+           py::arg("rule") = 0, py::arg("hbar") = 0.0)
+      .def("compute", &NearField::compute, py::arg("stream") = 0, py::call_guard<py::gil_scoped_release>())
+      .def("apply", &NearField::apply, py::arg("A"), py::arg("lda"), py::arg("stream") = 0)
+      .def("info", &NearField::info)
+      .def("triplets", &NearField::triplets)
+      .def("stats", &NearField::stats);
+  m.attr("NEAR_REF") = GK_NEAR_REF;
+  m.attr("NEAR_2HBAR") = GK_NEAR_2HBAR;
 
   m.def("side_tables", [](const Domain& d, const FemSpace& s) {
     SideTables t = make_side_tables(d, s);
