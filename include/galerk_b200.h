@@ -114,6 +114,9 @@ typedef struct gk_plan_info {
   int32_t symmetric;
   double eps;                   /* singular_guard_radius (kernels.cpp:14-19)     */
   uint64_t device_bytes;        /* plan tables resident on the device            */
+  double x_halo;                /* sum over x blocks of their locations / U_x    */
+  double y_halo;                /* sum over y blocks of their records / U_y      */
+  int32_t natural_order;        /* 1 if the dof order kept the input numbering   */
 } gk_plan_info;
 
 /* Builds the location/dof tables (host) and uploads them (device).  Applies

@@ -31,6 +31,12 @@ gk_status gk_diag_probe_pairs(int64_t n, const double* x, const double* y, const
 gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const double* z, double k,
                              double eps, gk_cplx* out, gk_stream stream);
 
+/* Host-only dry run of gk_plan_create (no device needed): fills the plan
+ * statistics (locations, tiles, evaluated vs unique pairs) so the tiling can
+ * be inspected and tested on a CPU-only machine. */
+gk_status gk_diag_plan_info(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
+                            const gk_options* opts, gk_plan_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ normal = _native.normal
 complex_normal = _native.complex_normal
 bem_dense_into = _native.bem_dense_into
 diag_fp64_peak = _native.diag_fp64_peak
+plan_info_dry = _native.plan_info_dry
 diag_probe_pairs = _native.diag_probe_pairs
 last_error = _native.last_error
 version = _native.version

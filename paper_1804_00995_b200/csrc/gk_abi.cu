@@ -7,6 +7,7 @@
 #include <memory>
 #include <unordered_map>
 
+#include "../../include/galerk_b200_diag.h"
 #include "gk_internal.hpp"
 
 namespace gk {
@@ -62,6 +63,8 @@ struct gk_plan {
   bool symmetric = false, helmholtz = false;
   double eps = 0.0, k = 0.0;
   int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0;
+  double x_halo = 0.0, y_halo = 0.0;
+  bool natural = false;
   DevBuf tile_i, tile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c,
       yb_dof_start, yb_rec_start, yrec, xperm, yperm;
   uint64_t device_bytes() const {
@@ -104,14 +107,14 @@ void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) 
 }
 
 std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
-                                   const gk_options* opts) {
+                                   const gk_options* opts, bool dry_run = false) {
   if (!test || !trial) throw std::invalid_argument("bem_dense: null side");
   check_kernel(kernel);
   gk_options o;
   gk_options_default(&o);
   if (opts) o = *opts;
   memory_cap(*test, *trial, o);
-  require_device();
+  if (!dry_run) require_device();
   auto P = std::make_unique<gk_plan>();
   P->rows = test->nfree;
   P->cols = trial->nfree;
@@ -134,7 +137,11 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->pairs_ref = test->npts * trial->npts;
   P->pairs_unique = P->symmetric ? X.size() * (X.size() + 1) / 2 : X.size() * Yr.size();
   P->pairs_eval = T.pairs_evaluated;
+  P->x_halo = T.x_halo;
+  P->y_halo = T.y_halo;
+  P->natural = X.natural;
   P->ntiles = (int64_t)T.tile_i.size();
+  if (dry_run) return P;
   P->tile_i.upload(T.tile_i);
   P->tile_j.upload(T.tile_j);
   P->xb_dof_start.upload(T.xb_dof_start);
@@ -203,6 +210,15 @@ gk_status gk_plan_create(const gk_side* test, const gk_side* trial, const gk_ker
   });
 }
 
+gk_status gk_diag_plan_info(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
+                            const gk_options* opts, gk_plan_info* info) {
+  gk_status st = GK_OK;
+  std::unique_ptr<gk_plan> P;
+  st = guard([&] { P = make_plan(test, trial, kernel, opts, /*dry_run=*/true); });
+  if (st != GK_OK) return st;
+  return gk_plan_get_info(P.get(), info);
+}
+
 gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
   return guard([&] {
     if (!P || !info) throw std::invalid_argument("gk_plan_get_info: null argument");
@@ -217,6 +233,9 @@ gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
     info->symmetric = P->symmetric ? 1 : 0;
     info->eps = P->eps;
     info->device_bytes = P->device_bytes();
+    info->x_halo = P->x_halo;
+    info->y_halo = P->y_halo;
+    info->natural_order = P->natural ? 1 : 0;
   });
 }
 

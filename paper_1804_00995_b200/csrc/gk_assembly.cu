@@ -6,13 +6,16 @@
 // A += (W_x Phi)^T kr (assembly.cpp:218).
 //
 // Tile = (x block I, y block J).  Thread t owns x location u_t of the block
-// (twins merged, <= 128 per block).  All threads walk the same list of y
-// records (warp-uniform loads), evaluate G(u_t, v) once per unique location
-// pair, and accumulate coef * G into H[slot][u_t] in shared memory — the
-// y-side contraction, owner-computes per thread column, no atomics.  After a
-// barrier each thread gathers whole entries A_ij = sum_u c_ui H[j][u] (the
-// x-side contraction in a fixed order) and writes them; with identical sides
-// only the upper triangle of tiles is computed and mirrored (G symmetric).
+// (twins merged, <= 128 per block).  The block's y records (unique y
+// locations with their <= 2 (slot, coef) pairs, sorted by first slot) and the
+// x support lists are staged in shared memory.  All threads walk the same
+// record list (broadcast reads), evaluate G(u_t, v) once per unique location
+// pair, keep a run accumulator for the current first slot in registers and
+// add the second slot into H[slot][u_t] — the y-side contraction,
+// owner-computes per thread column, no atomics.  After a barrier each thread
+// gathers whole entries A_ij = sum_u c_ui H[j][u] (x-side contraction, fixed
+// order) and writes them; with identical sides only tiles on or above the
+// diagonal are computed and mirrored (G is symmetric).
 #include <cuda_runtime.h>
 
 #include "gk_internal.hpp"
@@ -22,90 +25,130 @@ namespace gk {
 
 namespace {
 
-__device__ __forceinline__ YRec load_rec(const YRec* p) {
-  YRec r;
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  const double2 c = __ldg(reinterpret_cast<const double2*>(p) + 2);
-  r.x = a.x;
-  r.y = a.y;
-  r.z = b.x;
-  r.c0 = b.y;
-  r.c1 = c.x;
-  const long long s = __double_as_longlong(c.y);
-  r.s0 = (int32_t)(s & 0xffffffffll);
-  r.s1 = (int32_t)(s >> 32);
-  return r;
-}
+struct AsmSmem {
+  double2 H[kJCap * kUCap];
+  YRec rec[kRCap];
+  double xs_c[kXsCap];
+  int32_t xs_u[kXsCap];
+  int32_t xs_start[kIMax + 1];
+};
 
-__device__ __forceinline__ void acc(double2* h, double c, const c64& g) {
+__device__ __forceinline__ void rmw(char* Hb, int off, double c, double gr, double gi) {
+  double2* h = reinterpret_cast<double2*>(Hb + off);
   double2 v = *h;
-  v.x = fma(c, g.re, v.x);
-  v.y = fma(c, g.im, v.y);
+  v.x = fma(c, gr, v.x);
+  v.y = fma(c, gi, v.y);
   *h = v;
 }
 
 template <bool HELM>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
-  extern __shared__ double2 H[];  // [kJCap][kUCap]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int tile = blockIdx.x;
   const int bi = a.tile_i[tile], bj = a.tile_j[tile];
   const int t = threadIdx.x;
   const int i0 = a.xb_dof_start[bi], nI = a.xb_dof_start[bi + 1] - i0;
   const int j0 = a.yb_dof_start[bj], nJ = a.yb_dof_start[bj + 1] - j0;
   const int l0 = a.xb_loc_start[bi], nu = a.xb_loc_start[bi + 1] - l0;
+  const int r0 = a.yb_rec_start[bj], nrec = a.yb_rec_start[bj + 1] - r0;
+  const int xs0 = a.xsup_start[i0], nxs = a.xsup_start[i0 + nI] - xs0;
 
-  for (int e = t; e < nJ * kUCap; e += kAsmThreads) H[e] = make_double2(0.0, 0.0);
+  // stage: zero H rows, copy records and x support lists
+  for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
+    double2* dst = reinterpret_cast<double2*>(S.rec);
+    for (int e = t; e < nrec * 3; e += kAsmThreads) dst[e] = __ldg(src + e);
+  }
+  for (int e = t; e < nxs; e += kAsmThreads) {
+    S.xs_c[e] = __ldg(a.xsup_c + xs0 + e);
+    S.xs_u[e] = __ldg(a.xsup_u + xs0 + e);
+  }
+  for (int e = t; e <= nI; e += kAsmThreads) S.xs_start[e] = __ldg(a.xsup_start + i0 + e) - xs0;
   double ux = 0.0, uy = 0.0, uz = 0.0;
   if (t < nu) {
-    ux = a.xl_x[l0 + t];
-    uy = a.xl_y[l0 + t];
-    uz = a.xl_z[l0 + t];
+    ux = __ldg(a.xl_x + l0 + t);
+    uy = __ldg(a.xl_y + l0 + t);
+    uz = __ldg(a.xl_z + l0 + t);
+  } else {
+    ux = 1e100;  // idle columns: far away, finite, never gathered
   }
   __syncthreads();
 
   const double eps2 = a.eps2, kappa = a.kappa;
-  const YRec* rec = a.yrec + a.yb_rec_start[bj];
-  const int nrec = a.yb_rec_start[bj + 1] - a.yb_rec_start[bj];
-  double2* Hc = H + t;
+  char* Hb = reinterpret_cast<char*>(S.H) + t * 16;
+  int cur = -1;  // byte offset of the run's slot row
+  double ar = 0.0, ai = 0.0;
   int r = 0;
   for (; r + 1 < nrec; r += 2) {  // two independent pair evaluations in flight
-    const YRec p = load_rec(rec + r);
-    const YRec q = load_rec(rec + r + 1);
+    const YRec& p = S.rec[r];
+    const YRec& q = S.rec[r + 1];
     const c64 gp = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
     const c64 gq = green<HELM>(ux - q.x, uy - q.y, uz - q.z, eps2, kappa);
-    acc(Hc + p.s0 * kUCap, p.c0, gp);
-    if (p.s1 >= 0) acc(Hc + p.s1 * kUCap, p.c1, gp);
-    acc(Hc + q.s0 * kUCap, q.c0, gq);
-    if (q.s1 >= 0) acc(Hc + q.s1 * kUCap, q.c1, gq);
+    if (p.off0 != cur) {
+      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+      cur = p.off0;
+      ar = 0.0;
+      ai = 0.0;
+    }
+    ar = fma(p.c0, gp.re, ar);
+    ai = fma(p.c0, gp.im, ai);
+    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, gp.re, gp.im);
+    if (q.off0 != cur) {
+      rmw(Hb, cur, 1.0, ar, ai);
+      cur = q.off0;
+      ar = 0.0;
+      ai = 0.0;
+    }
+    ar = fma(q.c0, gq.re, ar);
+    ai = fma(q.c0, gq.im, ai);
+    if (q.off1 >= 0) rmw(Hb, q.off1, q.c1, gq.re, gq.im);
   }
   if (r < nrec) {
-    const YRec p = load_rec(rec + r);
+    const YRec& p = S.rec[r];
     const c64 gp = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
-    acc(Hc + p.s0 * kUCap, p.c0, gp);
-    if (p.s1 >= 0) acc(Hc + p.s1 * kUCap, p.c1, gp);
+    if (p.off0 != cur) {
+      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+      cur = p.off0;
+      ar = 0.0;
+      ai = 0.0;
+    }
+    ar = fma(p.c0, gp.re, ar);
+    ai = fma(p.c0, gp.im, ai);
+    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, gp.re, gp.im);
   }
+  if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
   __syncthreads();
 
-  // x-side contraction + write (lanes along rows: coalesced columns)
+  // x-side contraction + write (lanes along rows: coalesced columns for P0)
   double2* A = reinterpret_cast<double2*>(a.A);
   const long long lda = a.lda;
-  for (int e = t; e < nI * nJ; e += kAsmThreads) {
-    const int ii = e % nI, jj = e / nI;
+  const int total = nI * nJ;
+  int ii = t % nI, jj = t / nI;
+  const int di = kAsmThreads % nI, dj = kAsmThreads / nI;
+  for (int e = t; e < total; e += kAsmThreads) {
     const int pi = i0 + ii, pj = j0 + jj;
-    if (a.symmetric && pi > pj) continue;
-    double re = 0.0, im = 0.0;
-    const double2* Hr = H + jj * kUCap;
-    for (int s = a.xsup_start[pi]; s < a.xsup_start[pi + 1]; ++s) {
-      const double2 h = Hr[a.xsup_u[s]];
-      const double c = a.xsup_c[s];
-      re = fma(c, h.x, re);
-      im = fma(c, h.y, im);
+    if (!(a.symmetric && pi > pj)) {
+      double re = 0.0, im = 0.0;
+      const double2* Hr = S.H + jj * kUCap;
+      for (int s = S.xs_start[ii]; s < S.xs_start[ii + 1]; ++s) {
+        const double2 h = Hr[S.xs_u[s]];
+        const double c = S.xs_c[s];
+        re = fma(c, h.x, re);
+        im = fma(c, h.y, im);
+      }
+      const long long oi = __ldg(a.xperm + pi), oj = __ldg(a.yperm + pj);
+      const double2 v = make_double2(re, im);
+      A[oi + oj * lda] = v;
+      if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
     }
-    const long long oi = a.xperm[pi], oj = a.yperm[pj];
-    const double2 v = make_double2(re, im);
-    A[oi + oj * lda] = v;
-    if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
+    ii += di;
+    jj += dj;
+    if (ii >= nI) {
+      ii -= nI;
+      ++jj;
+    }
   }
 }
 
@@ -113,7 +156,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
 
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, void* stream) {
   if (ntiles <= 0) return;
-  const size_t smem = sizeof(double2) * kJCap * kUCap;
+  const size_t smem = sizeof(AsmSmem);
   static bool configured = false;
   if (!configured) {
     cuda_check(cudaFuncSetAttribute(k_assemble<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

@@ -88,6 +88,7 @@ struct Locations {
   std::vector<int32_t> cdof;             // contributing dof (original index)
   std::vector<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
   std::vector<int32_t> perm, iperm;      // locality order: perm[p] = dof
+  bool natural = false;                  // perm is the identity
   std::vector<int64_t> dstart;           // [nfree+1] by permuted dof
   std::vector<int32_t> dloc;             // location id
   std::vector<double> dcoef;
@@ -102,22 +103,28 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 
 // ---- assembly tiling ----------------------------------------------------------------
 constexpr int kUCap = 128;   // x locations per tile (one per thread)
-constexpr int kJCap = 48;    // y dofs per tile (H accumulator rows)
+constexpr int kJCap = 40;    // y dofs per tile (H accumulator rows)
 constexpr int kIMax = 128;   // x dofs per tile
+constexpr int kRCap = 256;   // y records per tile (staged in shared memory)
+constexpr int kXsCap = 1024; // x support entries per tile (staged in shared memory)
 constexpr int kAsmThreads = 128;
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   double x, y, z, c0, c1;
-  int32_t s0, s1;
+  int32_t off0, off1;  // byte offsets slot * kUCap * 16 into H; off1 = -1 if none
 };
 static_assert(sizeof(YRec) == 48, "YRec layout");
+
+// Locality order of the dofs: recursive coordinate bisection of the dof
+// locations (mean of their supporting quadrature locations).
+void rcb_order(Locations& L);
 
 struct TileTables {
   // x blocks
   std::vector<int32_t> xb_dof_start;  // [nIb+1] permuted row ranges
   std::vector<int32_t> xb_loc_start;  // [nIb+1]
   std::vector<double> xl_x, xl_y, xl_z;
-  std::vector<int32_t> xsup_start;    // [nrows+1] by permuted row
+  std::vector<int32_t> xsup_start;    // [nrows+1] by permuted row (global offsets)
   std::vector<int32_t> xsup_u;        // local location index in its block
   std::vector<double> xsup_c;
   // y blocks
@@ -127,6 +134,7 @@ struct TileTables {
   // tiles
   std::vector<int32_t> tile_i, tile_j;
   int64_t pairs_evaluated = 0;
+  double x_halo = 0.0, y_halo = 0.0;
 };
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric);
 

@@ -140,39 +140,107 @@ Locations build_locations(const gk_side& s, const char* who) {
       L.cdof[L.cstart[u] + i] = tdof[cnt[u] + i];
       L.ccoef[L.cstart[u] + i] = tcoef[cnt[u] + i];
     }
-  // dof order by first appearance along the location sequence (element order):
-  // P0 on a hierarchical mesh keeps the natural order; P1 vertices get a
-  // spatially coherent numbering for tiling.
-  L.iperm.assign(s.nfree, -1);
-  L.perm.clear();
-  L.perm.reserve(s.nfree);
-  for (int64_t p = 0; p < L.cstart[U]; ++p) {
-    const int32_t d = L.cdof[p];
-    if (L.iperm[d] < 0) {
-      L.iperm[d] = (int32_t)L.perm.size();
-      L.perm.push_back(d);
-    }
-  }
-  for (int64_t d = 0; d < s.nfree; ++d)
-    if (L.iperm[d] < 0) {
-      L.iperm[d] = (int32_t)L.perm.size();
-      L.perm.push_back((int32_t)d);
-    }
-  // per permuted dof: (location, coef) in location order
-  L.dstart.assign(s.nfree + 1, 0);
+  rcb_order(L);
+  return L;
+}
+
+namespace {
+// per permuted dof: (location, coef) in location order
+void finalize_perm(Locations& L) {
+  const int64_t U = L.size(), n = L.nfree;
+  L.iperm.assign(n, -1);
+  for (int64_t p = 0; p < n; ++p) L.iperm[L.perm[p]] = (int32_t)p;
+  L.dstart.assign(n + 1, 0);
   for (int64_t p = 0; p < L.cstart[U]; ++p) L.dstart[L.iperm[L.cdof[p]] + 1]++;
-  for (int64_t d = 0; d < s.nfree; ++d) L.dstart[d + 1] += L.dstart[d];
+  for (int64_t d = 0; d < n; ++d) L.dstart[d + 1] += L.dstart[d];
   L.dloc.resize(L.cstart[U]);
   L.dcoef.resize(L.cstart[U]);
-  std::vector<int64_t> f2(L.dstart.begin(), L.dstart.end() - 1);
+  std::vector<int64_t> f(L.dstart.begin(), L.dstart.end() - 1);
   for (int64_t u = 0; u < U; ++u)
     for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
       const int32_t pd = L.iperm[L.cdof[p]];
-      L.dloc[f2[pd]] = (int32_t)u;
-      L.dcoef[f2[pd]] = L.ccoef[p];
-      f2[pd]++;
+      L.dloc[f[pd]] = (int32_t)u;
+      L.dcoef[f[pd]] = L.ccoef[p];
+      f[pd]++;
     }
-  return L;
+}
+
+struct RcbPoint {
+  double c[3];
+  int32_t dof;
+};
+
+void rcb(std::vector<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf) {
+  if (hi - lo <= leaf) return;
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = lo; i < hi; ++i)
+    for (int c = 0; c < 3; ++c) {
+      mn[c] = std::min(mn[c], pts[i].c[c]);
+      mx[c] = std::max(mx[c], pts[i].c[c]);
+    }
+  int ax = 0;
+  for (int c = 1; c < 3; ++c)
+    if (mx[c] - mn[c] > mx[ax] - mn[ax]) ax = c;
+  const int64_t mid = lo + (hi - lo) / 2;
+  std::nth_element(pts.begin() + lo, pts.begin() + mid, pts.begin() + hi, [ax](const RcbPoint& a, const RcbPoint& b) {
+    return a.c[ax] < b.c[ax] || (a.c[ax] == b.c[ax] && a.dof < b.dof);
+  });
+  rcb(pts, lo, mid, leaf);
+  rcb(pts, mid, hi, leaf);
+}
+}  // namespace
+
+void rcb_order(Locations& L) {
+  // dof location = mean of its supporting quadrature locations; dofs with no
+  // support (constrained / zero basis) go last in index order.
+  const int64_t n = L.nfree, U = L.size();
+  std::vector<double> sx(n, 0.0), sy(n, 0.0), sz(n, 0.0);
+  std::vector<int64_t> cnt(n, 0);
+  for (int64_t u = 0; u < U; ++u)
+    for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
+      const int32_t d = L.cdof[p];
+      sx[d] += L.x[u];
+      sy[d] += L.y[u];
+      sz[d] += L.z[u];
+      cnt[d]++;
+    }
+  std::vector<RcbPoint> pts;
+  pts.reserve(n);
+  for (int64_t d = 0; d < n; ++d)
+    if (cnt[d]) pts.push_back({{sx[d] / cnt[d], sy[d] / cnt[d], sz[d] / cnt[d]}, (int32_t)d});
+  rcb(pts, 0, (int64_t)pts.size(), 16);
+  std::vector<int32_t> rcb_perm;
+  rcb_perm.reserve(n);
+  for (const auto& p : pts) rcb_perm.push_back(p.dof);
+  for (int64_t d = 0; d < n; ++d)
+    if (!cnt[d]) rcb_perm.push_back((int32_t)d);
+  // Candidate 2: the natural order when it is already local (hierarchical
+  // element order of a subdivided mesh) keeps A's writes coalesced.
+  std::vector<int32_t> natural(n);
+  std::iota(natural.begin(), natural.end(), 0);
+  // halo cost of an order: unique locations touched per block of kJCap dofs
+  std::vector<int64_t> stamp(U, -1);
+  auto cost = [&](const std::vector<int32_t>& perm) {
+    std::vector<int32_t> ip(n);
+    for (int64_t p = 0; p < n; ++p) ip[perm[p]] = (int32_t)p;
+    std::vector<std::vector<int32_t>> dl(n);
+    for (int64_t u = 0; u < U; ++u)
+      for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) dl[L.cdof[p]].push_back((int32_t)u);
+    int64_t total = 0, blk = 0;
+    std::fill(stamp.begin(), stamp.end(), -1);
+    for (int64_t p0 = 0; p0 < n; p0 += kJCap, ++blk)
+      for (int64_t p = p0; p < std::min<int64_t>(n, p0 + kJCap); ++p)
+        for (int32_t u : dl[perm[p]])
+          if (stamp[u] != blk) {
+            stamp[u] = blk;
+            ++total;
+          }
+    return total;
+  };
+  const int64_t c_rcb = cost(rcb_perm), c_nat = cost(natural);
+  L.natural = (double)c_nat <= 1.05 * (double)c_rcb;
+  L.perm = L.natural ? natural : rcb_perm;
+  finalize_perm(L);
 }
 
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
@@ -188,11 +256,13 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   std::vector<int32_t> blk_locs;
   while (p < nrows) {
     const int64_t start = p;
+    const int64_t sup0 = (int64_t)T.xsup_u.size();
     blk_locs.clear();
     while (p < nrows && p - start < kIMax) {
       int fresh = 0;  // a row lists each location once (merged per (location, dof))
       for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) fresh += owner[X.dloc[s]] != blk;
-      if ((int64_t)blk_locs.size() + fresh > kUCap) {
+      const int64_t nsup = X.dstart[p + 1] - X.dstart[p];
+      if ((int64_t)blk_locs.size() + fresh > kUCap || (int64_t)T.xsup_u.size() - sup0 + nsup > kXsCap) {
         if (p == start)
           throw std::invalid_argument("bem_dense: a test dof is supported by more than " +
                                       std::to_string(kUCap) + " quadrature locations");
@@ -220,46 +290,67 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
     T.xb_loc_start.push_back((int32_t)T.xl_x.size());
     ++blk;
   }
-  // ---- y blocks: kJCap consecutive permuted cols; records = incident locations
+  // ---- y blocks: up to kJCap consecutive permuted cols (fewer if their
+  // records would exceed kRCap); records = incident locations, each carrying
+  // <= 2 (slot, coef) pairs, ordered by first slot so that the kernel can keep
+  // a run accumulator for it in registers.
   std::vector<int64_t> ystamp(Y.size(), -1);
+  int64_t stamp_id = 0;
   T.yb_dof_start.push_back(0);
   T.yb_rec_start.push_back(0);
-  for (int64_t q0 = 0; q0 < ncols; q0 += kJCap) {
-    const int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
-    const int64_t bj = (int64_t)T.yb_dof_start.size() - 1;
+  std::vector<YRec> recs;
+  auto make_records = [&](int64_t q0, int64_t q1) {
+    recs.clear();
+    ++stamp_id;
     for (int64_t q = q0; q < q1; ++q)
       for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
         const int32_t v = Y.dloc[s];
-        if (ystamp[v] == bj) continue;
-        ystamp[v] = bj;
-        // slots of v inside [q0, q1)
-        std::vector<std::pair<int32_t, double>> sl;
+        if (ystamp[v] == stamp_id) continue;
+        ystamp[v] = stamp_id;
+        std::vector<std::pair<int32_t, double>> sl;  // slots of v inside [q0, q1)
         for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
           const int32_t pq = Y.iperm[Y.cdof[c]];
           if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
         }
+        std::stable_sort(sl.begin(), sl.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
         for (size_t a = 0; a < sl.size(); a += 2) {
           YRec r;
           r.x = Y.x[v];
           r.y = Y.y[v];
           r.z = Y.z[v];
-          r.s0 = sl[a].first;
+          r.off0 = sl[a].first * kUCap * 16;
           r.c0 = sl[a].second;
           if (a + 1 < sl.size()) {
-            r.s1 = sl[a + 1].first;
+            r.off1 = sl[a + 1].first * kUCap * 16;
             r.c1 = sl[a + 1].second;
           } else {
-            r.s1 = -1;
+            r.off1 = -1;
             r.c1 = 0.0;
           }
-          T.yrec.push_back(r);
+          recs.push_back(r);
         }
       }
+    std::stable_sort(recs.begin(), recs.end(), [](const YRec& a, const YRec& b) { return a.off0 < b.off0; });
+  };
+  for (int64_t q0 = 0; q0 < ncols;) {
+    int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+    make_records(q0, q1);
+    while ((int64_t)recs.size() > kRCap && q1 - q0 > 1) {
+      q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 3 / 4);
+      make_records(q0, q1);
+    }
+    if ((int64_t)recs.size() > kRCap)
+      throw std::invalid_argument("bem_dense: a trial dof is supported by more than " + std::to_string(kRCap) +
+                                  " quadrature locations");
+    T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
     T.yb_dof_start.push_back((int32_t)q1);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
+    q0 = q1;
   }
   // ---- tiles (symmetric: skip tiles strictly below the diagonal)
   const int64_t nIb = (int64_t)T.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
+  T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
+  T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
   for (int64_t bi = 0; bi < nIb; ++bi)
     for (int64_t bj = 0; bj < nJb; ++bj) {
       if (symmetric && T.yb_dof_start[bj + 1] - 1 < T.xb_dof_start[bi]) continue;

@@ -58,6 +58,9 @@ py::dict info_dict(const gk_plan_info& i) {
   d["symmetric"] = (bool)i.symmetric;
   d["eps"] = i.eps;
   d["device_bytes"] = i.device_bytes;
+  d["x_halo"] = i.x_halo;
+  d["y_halo"] = i.y_halo;
+  d["natural_order"] = (bool)i.natural_order;
   return d;
 }
 
@@ -343,6 +346,24 @@ PYBIND11_MODULE(_galerk, m) {
       },
       py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"), py::arg("opts"),
       py::arg("host_ptr"), py::arg("lda"));
+  m.def(
+      "plan_info_dry",
+      [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
+         const BemOptions& o, int symmetric) {
+        const SideTables a = make_side_tables(dx, t), b = make_side_tables(dy, u);
+        const gk_side sa = a.abi(), sb = b.abi();
+        const gk_kernel kk = k.abi();
+        gk_options go;
+        gk_options_default(&go);
+        go.memory_cap_bytes = o.memory_cap_bytes;
+        go.chunk = o.chunk;
+        go.symmetric = symmetric;
+        gk_plan_info info;
+        throw_status(gk_diag_plan_info(&sa, &sb, &kk, &go, &info));
+        return info_dict(info);
+      },
+      py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
+      py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1);
   m.def("diag_fp64_peak", [](int64_t iters, uintptr_t stream) {
     double g = 0;
     throw_status(gk_diag_fp64_peak(iters, &g, as_stream(stream)));
