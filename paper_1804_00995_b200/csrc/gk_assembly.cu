@@ -31,6 +31,8 @@ struct AsmSmem {
   double xs_c[kXsCap];
   int32_t xs_u[kXsCap];
   int32_t xs_start[kIMax + 1];
+  int32_t orow[kIMax];  // original row index of each tile row
+  int32_t ocol[kJCap];  // original column index of each tile column
 };
 
 __device__ __forceinline__ void rmw(char* Hb, int off, double c, double gr, double gi) {
@@ -66,6 +68,8 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     S.xs_u[e] = __ldg(a.xsup_u + xs0 + e);
   }
   for (int e = t; e <= nI; e += kAsmThreads) S.xs_start[e] = __ldg(a.xsup_start + i0 + e) - xs0;
+  for (int e = t; e < nI; e += kAsmThreads) S.orow[e] = __ldg(a.xperm + i0 + e);
+  for (int e = t; e < nJ; e += kAsmThreads) S.ocol[e] = __ldg(a.yperm + j0 + e);
   double ux = 0.0, uy = 0.0, uz = 0.0;
   if (t < nu) {
     ux = __ldg(a.xl_x + l0 + t);
@@ -80,43 +84,33 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   char* Hb = reinterpret_cast<char*>(S.H) + t * 16;
   int cur = -1;  // byte offset of the run's slot row
   double ar = 0.0, ai = 0.0;
+  // fold one evaluated pair into the run accumulator / second slot (uniform branches)
+  auto fold = [&](const YRec& p, const c64& g) {
+    if (p.off0 != cur) {
+      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+      cur = p.off0;
+      ar = 0.0;
+      ai = 0.0;
+    }
+    ar = fma(p.c0, g.re, ar);
+    ai = fma(p.c0, g.im, ai);
+    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, g.re, g.im);
+  };
+  constexpr int kUnroll = 4;  // independent pair evaluations in flight per thread
   int r = 0;
-  for (; r + 1 < nrec; r += 2) {  // two independent pair evaluations in flight
-    const YRec& p = S.rec[r];
-    const YRec& q = S.rec[r + 1];
-    const c64 gp = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
-    const c64 gq = green<HELM>(ux - q.x, uy - q.y, uz - q.z, eps2, kappa);
-    if (p.off0 != cur) {
-      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
-      cur = p.off0;
-      ar = 0.0;
-      ai = 0.0;
+  for (; r + kUnroll <= nrec; r += kUnroll) {
+    c64 g[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const YRec& p = S.rec[r + k];
+      g[k] = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
     }
-    ar = fma(p.c0, gp.re, ar);
-    ai = fma(p.c0, gp.im, ai);
-    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, gp.re, gp.im);
-    if (q.off0 != cur) {
-      rmw(Hb, cur, 1.0, ar, ai);
-      cur = q.off0;
-      ar = 0.0;
-      ai = 0.0;
-    }
-    ar = fma(q.c0, gq.re, ar);
-    ai = fma(q.c0, gq.im, ai);
-    if (q.off1 >= 0) rmw(Hb, q.off1, q.c1, gq.re, gq.im);
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) fold(S.rec[r + k], g[k]);
   }
-  if (r < nrec) {
+  for (; r < nrec; ++r) {
     const YRec& p = S.rec[r];
-    const c64 gp = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
-    if (p.off0 != cur) {
-      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
-      cur = p.off0;
-      ar = 0.0;
-      ai = 0.0;
-    }
-    ar = fma(p.c0, gp.re, ar);
-    ai = fma(p.c0, gp.im, ai);
-    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, gp.re, gp.im);
+    fold(p, green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa));
   }
   if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
   __syncthreads();
@@ -138,7 +132,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
         re = fma(c, h.x, re);
         im = fma(c, h.y, im);
       }
-      const long long oi = __ldg(a.xperm + pi), oj = __ldg(a.yperm + pj);
+      const long long oi = S.orow[ii], oj = S.ocol[jj];
       const double2 v = make_double2(re, im);
       A[oi + oj * lda] = v;
       if (a.symmetric && pi != pj) A[oj + oi * lda] = v;

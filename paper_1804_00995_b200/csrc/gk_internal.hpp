@@ -108,6 +108,7 @@ constexpr int kIMax = 128;   // x dofs per tile
 constexpr int kRCap = 256;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 1024; // x support entries per tile (staged in shared memory)
 constexpr int kAsmThreads = 128;
+constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   double x, y, z, c0, c1;

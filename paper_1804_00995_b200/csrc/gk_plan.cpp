@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "gk_internal.hpp"
@@ -237,8 +238,17 @@ void rcb_order(Locations& L) {
           }
     return total;
   };
+  // Natural order keeps the rows of every tile contiguous in A: full-sector,
+  // coalesced writes (a scattered 16-byte write costs a DRAM read-modify-write
+  // of its sector).  RCB wins only when the input numbering is not local.
   const int64_t c_rcb = cost(rcb_perm), c_nat = cost(natural);
-  L.natural = (double)c_nat <= 1.05 * (double)c_rcb;
+  const char* force = std::getenv("GK_ORDER");
+  if (force && std::string(force) == "natural")
+    L.natural = true;
+  else if (force && std::string(force) == "rcb")
+    L.natural = false;
+  else
+    L.natural = (double)c_nat <= 1.25 * (double)c_rcb;
   L.perm = L.natural ? natural : rcb_perm;
   finalize_perm(L);
 }
@@ -252,22 +262,41 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   T.xb_dof_start.push_back(0);
   T.xb_loc_start.push_back(0);
   T.xsup_start.assign(nrows + 1, 0);
-  int64_t p = 0, blk = 0;
+  // With the natural (hierarchical) order, block ends are aligned to multiples
+  // of kAlign dofs so blocks are unions of whole subdivision subtrees.
+  const int64_t align = X.natural ? kAlign : 1;
+  int64_t p = 0, blk = 0, trial_id = -2;
   std::vector<int32_t> blk_locs;
   while (p < nrows) {
     const int64_t start = p;
-    const int64_t sup0 = (int64_t)T.xsup_u.size();
-    blk_locs.clear();
-    while (p < nrows && p - start < kIMax) {
+    // pass 1: the largest end that fits kUCap locations / kXsCap supports
+    int64_t end = start, nl = 0, ns = 0;
+    --trial_id;
+    while (end < nrows && end - start < kIMax) {
       int fresh = 0;  // a row lists each location once (merged per (location, dof))
-      for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) fresh += owner[X.dloc[s]] != blk;
-      const int64_t nsup = X.dstart[p + 1] - X.dstart[p];
-      if ((int64_t)blk_locs.size() + fresh > kUCap || (int64_t)T.xsup_u.size() - sup0 + nsup > kXsCap) {
-        if (p == start)
-          throw std::invalid_argument("bem_dense: a test dof is supported by more than " +
-                                      std::to_string(kUCap) + " quadrature locations");
-        break;
+      for (int64_t s = X.dstart[end]; s < X.dstart[end + 1]; ++s) fresh += owner[X.dloc[s]] != trial_id;
+      const int64_t nsup = X.dstart[end + 1] - X.dstart[end];
+      if (nl + fresh > kUCap || ns + nsup > kXsCap) break;
+      for (int64_t s = X.dstart[end]; s < X.dstart[end + 1]; ++s) owner[X.dloc[s]] = trial_id;
+      nl += fresh;
+      ns += nsup;
+      ++end;
+    }
+    if (end == start)
+      throw std::invalid_argument("bem_dense: a test dof is supported by more than " + std::to_string(kUCap) +
+                                  " quadrature locations");
+    if (end < nrows && align > 1) {
+      // largest subtree alignment that keeps >= 90% of the rows that fit
+      for (int64_t a = 64; a >= 4; a /= 4) {
+        const int64_t e = (end / a) * a;
+        if (e > start && (double)(e - start) >= 0.9 * (double)(end - start)) {
+          end = e;
+          break;
+        }
       }
+    }
+    blk_locs.clear();
+    while (p < end) {
       for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
         const int32_t u = X.dloc[s];
         if (owner[u] != blk) {
@@ -332,8 +361,17 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
       }
     std::stable_sort(recs.begin(), recs.end(), [](const YRec& a, const YRec& b) { return a.off0 < b.off0; });
   };
+  const int64_t yalign = Y.natural ? kAlign : 1;
   for (int64_t q0 = 0; q0 < ncols;) {
     int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+    if (q1 < ncols && yalign > 1)
+      for (int64_t a = 64; a >= 4; a /= 4) {
+        const int64_t e = (q1 / a) * a;
+        if (e > q0 && (double)(e - q0) >= 0.9 * (double)(q1 - q0)) {
+          q1 = e;
+          break;
+        }
+      }
     make_records(q0, q1);
     while ((int64_t)recs.size() > kRCap && q1 - q0 > 1) {
       q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 3 / 4);
