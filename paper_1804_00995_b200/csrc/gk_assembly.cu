@@ -99,12 +99,17 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   constexpr int kUnroll = 4;  // independent pair evaluations in flight per thread
   int r = 0;
   for (; r + kUnroll <= nrec; r += kUnroll) {
-    c64 g[kUnroll];
+    double dx[kUnroll], dy[kUnroll], dz[kUnroll];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
-      const YRec& p = S.rec[r + k];
-      g[k] = green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa);
+      const double2 a0 = *reinterpret_cast<const double2*>(&S.rec[r + k].x);
+      const double2 a1 = *reinterpret_cast<const double2*>(&S.rec[r + k].z);
+      dx[k] = ux - a0.x;
+      dy[k] = uy - a0.y;
+      dz[k] = uz - a1.x;
     }
+    c64 g[kUnroll];
+    green_n<HELM, kUnroll>(dx, dy, dz, eps2, kappa, g);
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) fold(S.rec[r + k], g[k]);
   }
