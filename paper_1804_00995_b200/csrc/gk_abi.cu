@@ -130,8 +130,8 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   } else {
     Y = build_locations(*trial, "bem_dense(trial)");
   }
+  TileTables T = choose_order_and_tile(X, P->symmetric ? nullptr : &Y, P->symmetric);
   const Locations& Yr = P->symmetric ? X : Y;
-  TileTables T = build_tiles(X, Yr, P->symmetric);
   P->xloc = X.size();
   P->yloc = Yr.size();
   P->pairs_ref = test->npts * trial->npts;

@@ -89,6 +89,7 @@ struct Locations {
   std::vector<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
   std::vector<int32_t> perm, iperm;      // locality order: perm[p] = dof
   bool natural = false;                  // perm is the identity
+  std::vector<int8_t> strength;          // [nfree+1] boundary strength of each cut position
   std::vector<int64_t> dstart;           // [nfree+1] by permuted dof
   std::vector<int32_t> dloc;             // location id
   std::vector<double> dcoef;
@@ -102,12 +103,16 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
                         int64_t nb, const double* bx, const double* by, const double* bz);
 
 // ---- assembly tiling ----------------------------------------------------------------
-constexpr int kUCap = 128;   // x locations per tile (one per thread)
-constexpr int kJCap = 40;    // y dofs per tile (H accumulator rows)
-constexpr int kIMax = 128;   // x dofs per tile
-constexpr int kRCap = 256;   // y records per tile (staged in shared memory)
-constexpr int kXsCap = 1024; // x support entries per tile (staged in shared memory)
-constexpr int kAsmThreads = 128;
+// Tile shape (measured on B200: DFMA dependent latency ~9 cycles; the FP64 pipe
+// needs ~16 warps/SM at 2-3 independent chains per warp).  Two 256-thread CTAs
+// per SM: shared memory per CTA = H (kJCap x kUCap x 16 B = 96 KB) + staged
+// records and x supports (~15 KB).
+constexpr int kUCap = 256;   // x locations per tile (one per thread)
+constexpr int kJCap = 24;    // y dofs per tile (H accumulator rows)
+constexpr int kIMax = 256;   // x dofs per tile
+constexpr int kRCap = 128;   // y records per tile (staged in shared memory)
+constexpr int kXsCap = 640;  // x support entries per tile (staged in shared memory)
+constexpr int kAsmThreads = 256;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
@@ -116,9 +121,10 @@ struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
 };
 static_assert(sizeof(YRec) == 48, "YRec layout");
 
-// Locality order of the dofs: recursive coordinate bisection of the dof
-// locations (mean of their supporting quadrature locations).
-void rcb_order(Locations& L);
+// Dof order used for tiling: natural (input numbering; blocks cut at 4^k
+// boundaries of subdivided meshes, rows of A stay contiguous) or recursive
+// coordinate bisection of the dof locations (blocks cut at bisection splits).
+void set_order(Locations& L, bool natural);
 
 struct TileTables {
   // x blocks
@@ -138,6 +144,10 @@ struct TileTables {
   double x_halo = 0.0, y_halo = 0.0;
 };
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric);
+// Picks natural vs RCB order by the evaluated pair count of the resulting
+// tiles (natural preferred within 10%: coalesced writes); GK_ORDER=natural|rcb
+// overrides.  Y may be null (symmetric: Y = X).
+TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric);
 
 struct AsmArgs {
   const int32_t* tile_i;

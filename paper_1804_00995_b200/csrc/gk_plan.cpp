@@ -141,7 +141,7 @@ Locations build_locations(const gk_side& s, const char* who) {
       L.cdof[L.cstart[u] + i] = tdof[cnt[u] + i];
       L.ccoef[L.cstart[u] + i] = tcoef[cnt[u] + i];
     }
-  rcb_order(L);
+  set_order(L, true);
   return L;
 }
 
@@ -171,7 +171,7 @@ struct RcbPoint {
   int32_t dof;
 };
 
-void rcb(std::vector<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf) {
+void rcb(std::vector<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf, int depth, std::vector<int8_t>& strength) {
   if (hi - lo <= leaf) return;
   double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
   for (int64_t i = lo; i < hi; ++i)
@@ -186,72 +186,65 @@ void rcb(std::vector<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf) {
   std::nth_element(pts.begin() + lo, pts.begin() + mid, pts.begin() + hi, [ax](const RcbPoint& a, const RcbPoint& b) {
     return a.c[ax] < b.c[ax] || (a.c[ax] == b.c[ax] && a.dof < b.dof);
   });
-  rcb(pts, lo, mid, leaf);
-  rcb(pts, mid, hi, leaf);
+  strength[mid] = (int8_t)std::max<int>(strength[mid], 60 - depth);
+  rcb(pts, lo, mid, leaf, depth + 1, strength);
+  rcb(pts, mid, hi, leaf, depth + 1, strength);
 }
 }  // namespace
 
-void rcb_order(Locations& L) {
-  // dof location = mean of its supporting quadrature locations; dofs with no
-  // support (constrained / zero basis) go last in index order.
+void set_order(Locations& L, bool natural) {
   const int64_t n = L.nfree, U = L.size();
-  std::vector<double> sx(n, 0.0), sy(n, 0.0), sz(n, 0.0);
-  std::vector<int64_t> cnt(n, 0);
-  for (int64_t u = 0; u < U; ++u)
-    for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
-      const int32_t d = L.cdof[p];
-      sx[d] += L.x[u];
-      sy[d] += L.y[u];
-      sz[d] += L.z[u];
-      cnt[d]++;
+  L.natural = natural;
+  L.strength.assign(n + 1, 0);
+  if (natural) {
+    // subdivided meshes number children 4-by-4: boundaries at multiples of 4^k
+    L.perm.resize(n);
+    std::iota(L.perm.begin(), L.perm.end(), 0);
+    for (int64_t p = 0; p <= n; ++p) {
+      int s = 0;
+      for (int64_t q = p; q > 0 && q % 4 == 0 && s < 30; q /= 4) ++s;
+      L.strength[p] = (int8_t)s;
     }
-  std::vector<RcbPoint> pts;
-  pts.reserve(n);
-  for (int64_t d = 0; d < n; ++d)
-    if (cnt[d]) pts.push_back({{sx[d] / cnt[d], sy[d] / cnt[d], sz[d] / cnt[d]}, (int32_t)d});
-  rcb(pts, 0, (int64_t)pts.size(), 16);
-  std::vector<int32_t> rcb_perm;
-  rcb_perm.reserve(n);
-  for (const auto& p : pts) rcb_perm.push_back(p.dof);
-  for (int64_t d = 0; d < n; ++d)
-    if (!cnt[d]) rcb_perm.push_back((int32_t)d);
-  // Candidate 2: the natural order when it is already local (hierarchical
-  // element order of a subdivided mesh) keeps A's writes coalesced.
-  std::vector<int32_t> natural(n);
-  std::iota(natural.begin(), natural.end(), 0);
-  // halo cost of an order: unique locations touched per block of kJCap dofs
-  std::vector<int64_t> stamp(U, -1);
-  auto cost = [&](const std::vector<int32_t>& perm) {
-    std::vector<int32_t> ip(n);
-    for (int64_t p = 0; p < n; ++p) ip[perm[p]] = (int32_t)p;
-    std::vector<std::vector<int32_t>> dl(n);
+  } else {
+    // recursive coordinate bisection of the dof locations (mean of their
+    // supporting quadrature locations); unsupported dofs go last.
+    std::vector<double> sx(n, 0.0), sy(n, 0.0), sz(n, 0.0);
+    std::vector<int64_t> cnt(n, 0);
     for (int64_t u = 0; u < U; ++u)
-      for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) dl[L.cdof[p]].push_back((int32_t)u);
-    int64_t total = 0, blk = 0;
-    std::fill(stamp.begin(), stamp.end(), -1);
-    for (int64_t p0 = 0; p0 < n; p0 += kJCap, ++blk)
-      for (int64_t p = p0; p < std::min<int64_t>(n, p0 + kJCap); ++p)
-        for (int32_t u : dl[perm[p]])
-          if (stamp[u] != blk) {
-            stamp[u] = blk;
-            ++total;
-          }
-    return total;
-  };
-  // Natural order keeps the rows of every tile contiguous in A: full-sector,
-  // coalesced writes (a scattered 16-byte write costs a DRAM read-modify-write
-  // of its sector).  RCB wins only when the input numbering is not local.
-  const int64_t c_rcb = cost(rcb_perm), c_nat = cost(natural);
-  const char* force = std::getenv("GK_ORDER");
-  if (force && std::string(force) == "natural")
-    L.natural = true;
-  else if (force && std::string(force) == "rcb")
-    L.natural = false;
-  else
-    L.natural = (double)c_nat <= 1.25 * (double)c_rcb;
-  L.perm = L.natural ? natural : rcb_perm;
+      for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
+        const int32_t d = L.cdof[p];
+        sx[d] += L.x[u];
+        sy[d] += L.y[u];
+        sz[d] += L.z[u];
+        cnt[d]++;
+      }
+    std::vector<RcbPoint> pts;
+    pts.reserve(n);
+    for (int64_t d = 0; d < n; ++d)
+      if (cnt[d]) pts.push_back({{sx[d] / cnt[d], sy[d] / cnt[d], sz[d] / cnt[d]}, (int32_t)d});
+    rcb(pts, 0, (int64_t)pts.size(), 4, 0, L.strength);
+    L.perm.clear();
+    L.perm.reserve(n);
+    for (const auto& p : pts) L.perm.push_back(p.dof);
+    for (int64_t d = 0; d < n; ++d)
+      if (!cnt[d]) L.perm.push_back((int32_t)d);
+  }
+  L.strength[0] = L.strength[n] = 127;
   finalize_perm(L);
 }
+
+namespace {
+// Cut a greedy block [start, end_max) back to the strongest order boundary in
+// its last 20% so blocks are unions of whole spatial clusters.
+int64_t cut(const Locations& L, int64_t start, int64_t end_max) {
+  if (end_max >= L.nfree) return end_max;
+  const int64_t lo = start + std::max<int64_t>(1, (int64_t)std::ceil(0.8 * (double)(end_max - start)));
+  int64_t best = end_max;
+  for (int64_t e = end_max; e >= lo; --e)
+    if (L.strength[e] > L.strength[best]) best = e;
+  return best;
+}
+}  // namespace
 
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   TileTables T;
@@ -262,9 +255,6 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   T.xb_dof_start.push_back(0);
   T.xb_loc_start.push_back(0);
   T.xsup_start.assign(nrows + 1, 0);
-  // With the natural (hierarchical) order, block ends are aligned to multiples
-  // of kAlign dofs so blocks are unions of whole subdivision subtrees.
-  const int64_t align = X.natural ? kAlign : 1;
   int64_t p = 0, blk = 0, trial_id = -2;
   std::vector<int32_t> blk_locs;
   while (p < nrows) {
@@ -285,16 +275,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
     if (end == start)
       throw std::invalid_argument("bem_dense: a test dof is supported by more than " + std::to_string(kUCap) +
                                   " quadrature locations");
-    if (end < nrows && align > 1) {
-      // largest subtree alignment that keeps >= 90% of the rows that fit
-      for (int64_t a = 64; a >= 4; a /= 4) {
-        const int64_t e = (end / a) * a;
-        if (e > start && (double)(e - start) >= 0.9 * (double)(end - start)) {
-          end = e;
-          break;
-        }
-      }
-    }
+    end = cut(X, start, end);
     blk_locs.clear();
     while (p < end) {
       for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
@@ -361,20 +342,16 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
       }
     std::stable_sort(recs.begin(), recs.end(), [](const YRec& a, const YRec& b) { return a.off0 < b.off0; });
   };
-  const int64_t yalign = Y.natural ? kAlign : 1;
   for (int64_t q0 = 0; q0 < ncols;) {
     int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
-    if (q1 < ncols && yalign > 1)
-      for (int64_t a = 64; a >= 4; a /= 4) {
-        const int64_t e = (q1 / a) * a;
-        if (e > q0 && (double)(e - q0) >= 0.9 * (double)(q1 - q0)) {
-          q1 = e;
-          break;
-        }
-      }
     make_records(q0, q1);
     while ((int64_t)recs.size() > kRCap && q1 - q0 > 1) {
-      q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 3 / 4);
+      q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 7 / 8);
+      make_records(q0, q1);
+    }
+    const int64_t qc = cut(Y, q0, q1);
+    if (qc != q1) {
+      q1 = qc;
       make_records(q0, q1);
     }
     if ((int64_t)recs.size() > kRCap)
@@ -398,6 +375,25 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
                            (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
     }
   return T;
+}
+
+TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric) {
+  const char* force = std::getenv("GK_ORDER");
+  const std::string f = force ? force : "";
+  auto tile = [&](bool natural) {
+    set_order(X, natural);
+    if (Y) set_order(*Y, natural);
+    return build_tiles(X, Y ? *Y : X, symmetric);
+  };
+  if (f == "natural") return tile(true);
+  if (f == "rcb") return tile(false);
+  // Natural order keeps the rows of every tile contiguous in A (full-sector,
+  // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
+  // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
+  const int64_t rcb_pairs = tile(false).pairs_evaluated;
+  TileTables nat = tile(true);
+  if ((double)nat.pairs_evaluated <= 1.10 * (double)rcb_pairs) return nat;
+  return tile(false);
 }
 
 }  // namespace gk
