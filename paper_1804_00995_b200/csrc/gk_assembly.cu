@@ -56,8 +56,10 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int r0 = a.yb_rec_start[bj], nrec = a.yb_rec_start[bj + 1] - r0;
   const int xs0 = a.xsup_start[i0], nxs = a.xsup_start[i0 + nI] - xs0;
 
-  // stage: zero H rows, copy records and x support lists
-  for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
+  // stage: copy records and x support lists; H rows are initialised by their
+  // first-touch store (host-flagged) unless some row gets no record at all
+  if (a.yb_zero[bj])
+    for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
   {
     const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
     double2* dst = reinterpret_cast<double2*>(S.rec);
@@ -83,18 +85,32 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const double eps2 = a.eps2, kappa = a.kappa;
   char* Hb = reinterpret_cast<char*>(S.H) + t * 16;
   int cur = -1;  // byte offset of the run's slot row
+  bool cur_first = false;
   double ar = 0.0, ai = 0.0;
+  auto flush = [&]() {
+    if (cur_first)
+      *reinterpret_cast<double2*>(Hb + cur) = make_double2(ar, ai);
+    else
+      rmw(Hb, cur, 1.0, ar, ai);
+  };
   // fold one evaluated pair into the run accumulator / second slot (uniform branches)
   auto fold = [&](const YRec& p, const c64& g) {
-    if (p.off0 != cur) {
-      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
-      cur = p.off0;
+    const int o0 = p.off0 & kOffMask;
+    if (o0 != cur) {
+      if (cur >= 0) flush();
+      cur = o0;
+      cur_first = (p.off0 & kFirstTouch) != 0;
       ar = 0.0;
       ai = 0.0;
     }
     ar = fma(p.c0, g.re, ar);
     ai = fma(p.c0, g.im, ai);
-    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, g.re, g.im);
+    if (p.off1 >= 0) {
+      if (p.off1 & kFirstTouch)
+        *reinterpret_cast<double2*>(Hb + (p.off1 & kOffMask)) = make_double2(p.c1 * g.re, p.c1 * g.im);
+      else
+        rmw(Hb, p.off1, p.c1, g.re, g.im);
+    }
   };
   constexpr int kUnroll = 4;  // independent pair evaluations in flight per thread
   int r = 0;
@@ -117,7 +133,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     const YRec& p = S.rec[r];
     fold(p, green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa));
   }
-  if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+  if (cur >= 0) flush();
   __syncthreads();
 
   // x-side contraction + write (lanes along rows: coalesced columns for P0)
@@ -126,28 +142,55 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int total = nI * nJ;
   int ii = t % nI, jj = t / nI;
   const int di = kAsmThreads % nI, dj = kAsmThreads / nI;
-  for (int e = t; e < total; e += kAsmThreads) {
-    const int pi = i0 + ii, pj = j0 + jj;
-    if (!(a.symmetric && pi > pj)) {
-      double re = 0.0, im = 0.0;
-      const double2* Hr = S.H + jj * kUCap;
-      for (int s = S.xs_start[ii]; s < S.xs_start[ii + 1]; ++s) {
-        const double2 h = Hr[S.xs_u[s]];
-        const double c = S.xs_c[s];
-        re = fma(c, h.x, re);
-        im = fma(c, h.y, im);
+  auto step = [&](int& i_, int& j_) {
+    i_ += di;
+    j_ += dj;
+    if (i_ >= nI) {
+      i_ -= nI;
+      ++j_;
+    }
+  };
+  for (int e = t; e < total; e += 2 * kAsmThreads) {  // two entries per iteration (ILP)
+    int ii2 = ii, jj2 = jj;
+    step(ii2, jj2);
+    const bool live1 = !(a.symmetric && i0 + ii > j0 + jj);
+    const bool live2 = e + kAsmThreads < total && !(a.symmetric && i0 + ii2 > j0 + jj2);
+    double re1 = 0.0, im1 = 0.0, re2 = 0.0, im2 = 0.0;
+    int s1 = live1 ? S.xs_start[ii] : 0, e1 = live1 ? S.xs_start[ii + 1] : 0;
+    int s2 = live2 ? S.xs_start[ii2] : 0, e2 = live2 ? S.xs_start[ii2 + 1] : 0;
+    const double2* H1 = S.H + jj * kUCap;
+    const double2* H2 = S.H + jj2 * kUCap;
+    while (s1 < e1 || s2 < e2) {
+      if (s1 < e1) {
+        const double2 h = H1[S.xs_u[s1]];
+        const double c = S.xs_c[s1];
+        re1 = fma(c, h.x, re1);
+        im1 = fma(c, h.y, im1);
+        ++s1;
       }
+      if (s2 < e2) {
+        const double2 h = H2[S.xs_u[s2]];
+        const double c = S.xs_c[s2];
+        re2 = fma(c, h.x, re2);
+        im2 = fma(c, h.y, im2);
+        ++s2;
+      }
+    }
+    if (live1) {
       const long long oi = S.orow[ii], oj = S.ocol[jj];
-      const double2 v = make_double2(re, im);
+      const double2 v = make_double2(re1, im1);
       A[oi + oj * lda] = v;
-      if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
+      if (a.symmetric && i0 + ii != j0 + jj) A[oj + oi * lda] = v;
     }
-    ii += di;
-    jj += dj;
-    if (ii >= nI) {
-      ii -= nI;
-      ++jj;
+    if (live2) {
+      const long long oi = S.orow[ii2], oj = S.ocol[jj2];
+      const double2 v = make_double2(re2, im2);
+      A[oi + oj * lda] = v;
+      if (a.symmetric && i0 + ii2 != j0 + jj2) A[oj + oi * lda] = v;
     }
+    ii = ii2;
+    jj = jj2;
+    step(ii, jj);
   }
 }
 
