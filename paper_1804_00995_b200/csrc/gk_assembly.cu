@@ -150,46 +150,22 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
       ++j_;
     }
   };
-  for (int e = t; e < total; e += 2 * kAsmThreads) {  // two entries per iteration (ILP)
-    int ii2 = ii, jj2 = jj;
-    step(ii2, jj2);
-    const bool live1 = !(a.symmetric && i0 + ii > j0 + jj);
-    const bool live2 = e + kAsmThreads < total && !(a.symmetric && i0 + ii2 > j0 + jj2);
-    double re1 = 0.0, im1 = 0.0, re2 = 0.0, im2 = 0.0;
-    int s1 = live1 ? S.xs_start[ii] : 0, e1 = live1 ? S.xs_start[ii + 1] : 0;
-    int s2 = live2 ? S.xs_start[ii2] : 0, e2 = live2 ? S.xs_start[ii2 + 1] : 0;
-    const double2* H1 = S.H + jj * kUCap;
-    const double2* H2 = S.H + jj2 * kUCap;
-    while (s1 < e1 || s2 < e2) {
-      if (s1 < e1) {
-        const double2 h = H1[S.xs_u[s1]];
-        const double c = S.xs_c[s1];
-        re1 = fma(c, h.x, re1);
-        im1 = fma(c, h.y, im1);
-        ++s1;
+  for (int e = t; e < total; e += kAsmThreads) {
+    const int pi = i0 + ii, pj = j0 + jj;
+    if (!(a.symmetric && pi > pj)) {
+      double re = 0.0, im = 0.0;
+      const double2* Hr = S.H + jj * kUCap;
+      for (int s = S.xs_start[ii]; s < S.xs_start[ii + 1]; ++s) {
+        const double2 h = Hr[S.xs_u[s]];
+        const double c = S.xs_c[s];
+        re = fma(c, h.x, re);
+        im = fma(c, h.y, im);
       }
-      if (s2 < e2) {
-        const double2 h = H2[S.xs_u[s2]];
-        const double c = S.xs_c[s2];
-        re2 = fma(c, h.x, re2);
-        im2 = fma(c, h.y, im2);
-        ++s2;
-      }
-    }
-    if (live1) {
       const long long oi = S.orow[ii], oj = S.ocol[jj];
-      const double2 v = make_double2(re1, im1);
+      const double2 v = make_double2(re, im);
       A[oi + oj * lda] = v;
-      if (a.symmetric && i0 + ii != j0 + jj) A[oj + oi * lda] = v;
+      if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
     }
-    if (live2) {
-      const long long oi = S.orow[ii2], oj = S.ocol[jj2];
-      const double2 v = make_double2(re2, im2);
-      A[oi + oj * lda] = v;
-      if (a.symmetric && i0 + ii2 != j0 + jj2) A[oj + oi * lda] = v;
-    }
-    ii = ii2;
-    jj = jj2;
     step(ii, jj);
   }
 }
