@@ -56,10 +56,8 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int r0 = a.yb_rec_start[bj], nrec = a.yb_rec_start[bj + 1] - r0;
   const int xs0 = a.xsup_start[i0], nxs = a.xsup_start[i0 + nI] - xs0;
 
-  // stage: copy records and x support lists; H rows are initialised by their
-  // first-touch store (host-flagged) unless some row gets no record at all
-  if (a.yb_zero[bj])
-    for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
+  // stage: zero H rows, copy records and x support lists
+  for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
   {
     const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
     double2* dst = reinterpret_cast<double2*>(S.rec);
@@ -85,32 +83,18 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const double eps2 = a.eps2, kappa = a.kappa;
   char* Hb = reinterpret_cast<char*>(S.H) + t * 16;
   int cur = -1;  // byte offset of the run's slot row
-  bool cur_first = false;
   double ar = 0.0, ai = 0.0;
-  auto flush = [&]() {
-    if (cur_first)
-      *reinterpret_cast<double2*>(Hb + cur) = make_double2(ar, ai);
-    else
-      rmw(Hb, cur, 1.0, ar, ai);
-  };
   // fold one evaluated pair into the run accumulator / second slot (uniform branches)
   auto fold = [&](const YRec& p, const c64& g) {
-    const int o0 = p.off0 & kOffMask;
-    if (o0 != cur) {
-      if (cur >= 0) flush();
-      cur = o0;
-      cur_first = (p.off0 & kFirstTouch) != 0;
+    if (p.off0 != cur) {
+      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+      cur = p.off0;
       ar = 0.0;
       ai = 0.0;
     }
     ar = fma(p.c0, g.re, ar);
     ai = fma(p.c0, g.im, ai);
-    if (p.off1 >= 0) {
-      if (p.off1 & kFirstTouch)
-        *reinterpret_cast<double2*>(Hb + (p.off1 & kOffMask)) = make_double2(p.c1 * g.re, p.c1 * g.im);
-      else
-        rmw(Hb, p.off1, p.c1, g.re, g.im);
-    }
+    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, g.re, g.im);
   };
   constexpr int kUnroll = 4;  // independent pair evaluations in flight per thread
   int r = 0;
@@ -133,7 +117,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     const YRec& p = S.rec[r];
     fold(p, green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa));
   }
-  if (cur >= 0) flush();
+  if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
   __syncthreads();
 
   // x-side contraction + write (lanes along rows: coalesced columns for P0)
@@ -142,14 +126,6 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int total = nI * nJ;
   int ii = t % nI, jj = t / nI;
   const int di = kAsmThreads % nI, dj = kAsmThreads / nI;
-  auto step = [&](int& i_, int& j_) {
-    i_ += di;
-    j_ += dj;
-    if (i_ >= nI) {
-      i_ -= nI;
-      ++j_;
-    }
-  };
   for (int e = t; e < total; e += kAsmThreads) {
     const int pi = i0 + ii, pj = j0 + jj;
     if (!(a.symmetric && pi > pj)) {
@@ -166,7 +142,12 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
       A[oi + oj * lda] = v;
       if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
     }
-    step(ii, jj);
+    ii += di;
+    jj += dj;
+    if (ii >= nI) {
+      ii -= nI;
+      ++jj;
+    }
   }
 }
 

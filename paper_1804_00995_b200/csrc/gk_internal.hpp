@@ -118,9 +118,7 @@ constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision s
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   double x, y, z, c0, c1;
   int32_t off0, off1;  // byte offsets slot * kUCap * 16 into H; off1 = -1 if none
-};                     // bit 30 (kFirstTouch): first operation on that H row
-constexpr int32_t kFirstTouch = 1 << 30;
-constexpr int32_t kOffMask = kFirstTouch - 1;
+};
 static_assert(sizeof(YRec) == 48, "YRec layout");
 
 // Dof order used for tiling: natural (input numbering; blocks cut at 4^k
@@ -140,7 +138,6 @@ struct TileTables {
   std::vector<int32_t> yb_dof_start;  // [nJb+1]
   std::vector<int32_t> yb_rec_start;  // [nJb+1]
   std::vector<YRec> yrec;
-  std::vector<int32_t> yb_zero;       // [nJb] 1: some H row gets no record -> zero-fill
   // tiles
   std::vector<int32_t> tile_i, tile_j;
   int64_t pairs_evaluated = 0;
@@ -166,7 +163,6 @@ struct AsmArgs {
   const int32_t* yb_dof_start;
   const int32_t* yb_rec_start;
   const YRec* yrec;
-  const int32_t* yb_zero;
   const int32_t* xperm;
   const int32_t* yperm;
   void* A;

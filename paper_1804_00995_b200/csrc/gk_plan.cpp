@@ -309,7 +309,6 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   T.yb_dof_start.push_back(0);
   T.yb_rec_start.push_back(0);
   std::vector<YRec> recs;
-  bool needs_zero = false;
   auto make_records = [&](int64_t q0, int64_t q1) {
     recs.clear();
     ++stamp_id;
@@ -342,26 +341,6 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
         }
       }
     std::stable_sort(recs.begin(), recs.end(), [](const YRec& a, const YRec& b) { return a.off0 < b.off0; });
-    // First-touch flags: replay the kernel's H operations (run flushes keyed
-    // by off0, second-slot updates by off1) and mark the first operation on
-    // each H row, which then stores instead of read-modify-writing, so H is
-    // never zero-filled.  Rows left untouched force a zero fill of the tile.
-    std::vector<char> touched(q1 - q0, 0);
-    int32_t cur = -1;
-    for (auto& r : recs) {
-      const int32_t s0 = r.off0 / (kUCap * 16);
-      if (s0 != cur) {
-        cur = s0;
-        if (!touched[s0]) r.off0 |= kFirstTouch;
-        touched[s0] = 1;
-      }
-      if (r.off1 >= 0) {
-        const int32_t s1 = r.off1 / (kUCap * 16);
-        if (!touched[s1]) r.off1 |= kFirstTouch;
-        touched[s1] = 1;
-      }
-    }
-    needs_zero = std::find(touched.begin(), touched.end(), 0) != touched.end();
   };
   for (int64_t q0 = 0; q0 < ncols;) {
     int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
@@ -381,7 +360,6 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
     T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
     T.yb_dof_start.push_back((int32_t)q1);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
-    T.yb_zero.push_back(needs_zero ? 1 : 0);
     q0 = q1;
   }
   // ---- tiles (symmetric: skip tiles strictly below the diagonal)
