@@ -205,12 +205,19 @@ def main():
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     nmv = 10 if args.config == 4 else 1
-    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n)
+    # cfg 3: "including the near-field singular correction" -> K3 inside the step
+    nf = g.NearField(dom, dom, space, "[1/r]", space) if args.config == 3 else None
+    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n) + (3 if nf else 0)
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         plan.assemble(A.data_ptr(), n, sp)
+        if nf:
+            if ev:
+                ev[3].record(stream)
+            nf.compute(sp)
+            nf.apply(A.data_ptr(), n, sp)
         if ev:
             ev[1].record(stream)
         for _ in range(nmv):
@@ -222,7 +229,7 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -236,7 +243,12 @@ def main():
     if dist:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
-    asm_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    if nf:
+        nf_ms = float(np.mean([e[3].elapsed_time(e[1]) for e in evs]))
+        asm_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in evs]))
+    else:
+        nf_ms = None
+        asm_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
     if dist:
         tt = torch.tensor([total_ms], device=dev)
@@ -275,6 +287,8 @@ def main():
                              % (16 * n * n / 1e9, info["device_bytes"] / 1e6)},
             "entries_per_s": world * n * n / (ms_step * 1e-3),
             "assembly_ms": asm_ms,
+            "nearfield_ms": nf_ms,
+            "nearfield": (dict(zip(("pairs", "entries"), nf.info())) | {"analytic_calls": nf.stats()[0]}) if nf else None,
             "matvec_ms": mv_ms,
             "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
             "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
