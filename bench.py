@@ -30,17 +30,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
-# Algorithmic FP64 work per unique location pair: the
-# production pair formula (gk_math.cuh green<>: 33 FP64 instructions = 51
-# flops with DFMA = 2) plus one complex x real accumulate (2 DFMA = 4 flops).
-F_PAIR_FLOPS = {True: 55.0, False: 23.0}  # Helmholtz / Laplace ("[1/r]": 11 instr = 19 flops + 4)
+# FP64 work per unique location pair (DESIGN.md §4 "F_pair"), frozen from ncu
+# counters (profiles/r01_fpair_probe.txt):
+#  - canonical probe: the reference formula kernels.cpp:94-114 with
+#    libdevice sqrt/sin/cos/division + one complex x real accumulate:
+#    43 DFMA + 13 DMUL + 7 DADD = 106 flops/pair (DFMA = 2 flops);
+#  - production formula (gk_math.cuh green_n + accumulate):
+#    20 DFMA + 8 DMUL + 6 DADD = 54 flops/pair.
+# Laplace ("[1/r]", cfg 1): 11 FP64 instructions + accumulate = 23 flops.
+F_PAIR_PROBE_FLOPS = {True: 106.0, False: 23.0}
+F_PAIR_PROD_FLOPS = {True: 54.0, False: 23.0}
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,28 +88,46 @@ def workload_name(cfg, spec, mesh):
 
 # ---------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region (NVML, 5 ms
+    period; falls back to nvidia-smi at 200 ms)."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, power_w, reasons_mask)
         self._stop = threading.Event()
         self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nv = None
+
+    def _sample(self):
+        if self._nv is not None:
+            nv, h = self._nv, self._h
+            return (float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                    float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                    nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                    int(nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        c = [x.strip() for x in out.stdout.strip().split(",")]
+        return float(c[0]), float(c[1]), float(c[2]), int(c[3], 16)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+                self.rows.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.005 if self._nv is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -113,17 +137,18 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        try:  # one sample at the end of the region as well
+            self.rows.append(self._sample())
+        except Exception:
+            pass
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        reasons = sorted({n for r in self.rows for n, bit in self.REASONS.items() if r[3] & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(r[2] for r in self.rows),
+                "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -263,8 +288,10 @@ def main():
         peaks = measured_peaks()
         hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
         helm = k != 0.0
-        alg_flops = info["pairs_unique"] * F_PAIR_FLOPS[helm]
+        alg_flops = info["pairs_unique"] * F_PAIR_PROBE_FLOPS[helm]
         achieved = alg_flops / (asm_ms * 1e-3) / 1e12
+        achieved_prod = info["pairs_unique"] * F_PAIR_PROD_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
+        exec_prod = info["pairs_evaluated"] * F_PAIR_PROD_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
         peak = fp64_peak_gflops / 1e3
         mv_bytes = 16.0 * n * n + 32.0 * n
         clocks = clk.summary()
@@ -296,7 +323,10 @@ def main():
             "roofline": {"bound": "fp64", "kernel": "k_assemble (K1+K2)", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": profile_traffic(args.config),
                          "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no FP64)",
-                         "work": "pairs_unique x %.0f FP64 flops/pair (DESIGN.md F_pair)" % F_PAIR_FLOPS[helm]},
+                         "work": "pairs_unique (twins merged, symmetric half) x %.0f flops/pair = canonical "
+                                 "libdevice probe F_pair (SURVEY 8d)" % F_PAIR_PROBE_FLOPS[helm],
+                         "frac_production_formula": achieved_prod / peak,
+                         "frac_executed_pairs_production_formula": exec_prod / peak},
             "roofline_matvec": {"bound": "hbm", "achieved": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak": hbm,
                                 "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
