@@ -151,6 +151,22 @@ class ClockSampler:
                 "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
+def max_over_ranks(ms, dist, device):
+    """Device-timed milliseconds -> max over all ranks (replicas finish when the slowest does)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(ms)
+    import torch
+
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(units_per_rank, world, ms_step):
+    """Whole-job throughput: units of all ranks / the max-over-ranks step time."""
+    return world * units_per_rank / (ms_step * 1e-3)
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -275,13 +291,10 @@ def main():
         nf_ms = None
         asm_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
-    if dist:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    total_ms = max_over_ranks(total_ms, dist, dev)
     ms_step = total_ms / args.steps
     pairs_ref = info["pairs_reference"]
-    value = world * pairs_ref / (ms_step * 1e-3)
+    value = aggregate_value(pairs_ref, world, ms_step)
 
     out = None
     if rank == 0:
