@@ -111,6 +111,7 @@ typedef struct gk_plan_info {
   int64_t pairs_unique;         /* unique location pairs (symmetry-halved if on) */
   int64_t pairs_evaluated;      /* location pairs the kernel evaluates (halo)    */
   int64_t tiles;                /* CTA tiles launched (after symmetric skip)     */
+  int64_t masked_tiles;         /* of which apply the r^2 <= eps^2 mask          */
   int32_t symmetric;
   double eps;                   /* singular_guard_radius (kernels.cpp:14-19)     */
   uint64_t device_bytes;        /* plan tables resident on the device            */

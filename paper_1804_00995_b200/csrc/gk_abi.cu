@@ -62,14 +62,15 @@ struct gk_plan {
   int64_t rows = 0, cols = 0;
   bool symmetric = false, helmholtz = false;
   double eps = 0.0, k = 0.0;
-  int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0;
+  int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0, nmtiles = 0;
   double x_halo = 0.0, y_halo = 0.0;
-  bool natural = false;
-  DevBuf tile_i, tile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c,
-      yb_dof_start, yb_rec_start, yrec, xperm, yperm;
+  bool natural = false, second_slot = true;
+  DevBuf tile_i, tile_j, mtile_i, mtile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u,
+      xsup_c, yb_dof_start, yb_rec_start, yrec, xperm, yperm;
   uint64_t device_bytes() const {
-    const DevBuf* b[] = {&tile_i, &tile_j, &xb_dof_start, &xb_loc_start, &xl_x, &xl_y, &xl_z, &xsup_start,
-                         &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &xperm, &yperm};
+    const DevBuf* b[] = {&tile_i, &tile_j, &mtile_i, &mtile_j, &xb_dof_start, &xb_loc_start, &xl_x, &xl_y,
+                         &xl_z, &xsup_start, &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &xperm,
+                         &yperm};
     uint64_t s = 0;
     for (auto* p : b) s += p->bytes;
     return s;
@@ -130,7 +131,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   } else {
     Y = build_locations(*trial, "bem_dense(trial)");
   }
-  TileTables T = choose_order_and_tile(X, P->symmetric ? nullptr : &Y, P->symmetric);
+  TileTables T = choose_order_and_tile(X, P->symmetric ? nullptr : &Y, P->symmetric, P->eps);
   const Locations& Yr = P->symmetric ? X : Y;
   P->xloc = X.size();
   P->yloc = Yr.size();
@@ -141,9 +142,13 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->y_halo = T.y_halo;
   P->natural = X.natural;
   P->ntiles = (int64_t)T.tile_i.size();
+  P->nmtiles = (int64_t)T.mtile_i.size();
+  P->second_slot = T.has_second_slot;
   if (dry_run) return P;
   P->tile_i.upload(T.tile_i);
   P->tile_j.upload(T.tile_j);
+  P->mtile_i.upload(T.mtile_i);
+  P->mtile_j.upload(T.mtile_j);
   P->xb_dof_start.upload(T.xb_dof_start);
   P->xb_loc_start.upload(T.xb_loc_start);
   P->xl_x.upload(T.xl_x);
@@ -186,7 +191,11 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.eps2 = P->eps * P->eps;
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
-  launch_assemble(a, P->ntiles, P->helmholtz, stream);
+  // tiles that can hold a coincident pair apply the distance mask; the rest skip it
+  launch_assemble(a, P->ntiles, P->helmholtz, /*mask=*/false, P->second_slot, stream);
+  a.tile_i = P->mtile_i.as<int32_t>();
+  a.tile_j = P->mtile_j.as<int32_t>();
+  launch_assemble(a, P->nmtiles, P->helmholtz, /*mask=*/true, P->second_slot, stream);
 }
 
 }  // namespace
@@ -229,7 +238,8 @@ gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
     info->pairs_reference = P->pairs_ref;
     info->pairs_unique = P->pairs_unique;
     info->pairs_evaluated = P->pairs_eval;
-    info->tiles = P->ntiles;
+    info->tiles = P->ntiles + P->nmtiles;
+    info->masked_tiles = P->nmtiles;
     info->symmetric = P->symmetric ? 1 : 0;
     info->eps = P->eps;
     info->device_bytes = P->device_bytes();
@@ -243,7 +253,9 @@ gk_status gk_plan_assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream
   return guard([&] { assemble(P, A, lda, stream); });
 }
 
-int32_t gk_plan_launches(const gk_plan* P) { return (P && P->ntiles > 0) ? 1 : 0; }
+int32_t gk_plan_launches(const gk_plan* P) {
+  return P ? (P->ntiles > 0 ? 1 : 0) + (P->nmtiles > 0 ? 1 : 0) : 0;
+}
 
 gk_status gk_plan_destroy(gk_plan* P) {
   return guard([&] { delete P; });

@@ -5,17 +5,23 @@
 // y-side product kr = G (W_y Psi) (assembly.cpp:217) and the x-side update
 // A += (W_x Phi)^T kr (assembly.cpp:218).
 //
-// Tile = (x block I, y block J).  Thread t owns x location u_t of the block
-// (twins merged, <= 128 per block).  The block's y records (unique y
-// locations with their <= 2 (slot, coef) pairs, sorted by first slot) and the
-// x support lists are staged in shared memory.  All threads walk the same
-// record list (broadcast reads), evaluate G(u_t, v) once per unique location
-// pair, keep a run accumulator for the current first slot in registers and
-// add the second slot into H[slot][u_t] — the y-side contraction,
-// owner-computes per thread column, no atomics.  After a barrier each thread
-// gathers whole entries A_ij = sum_u c_ui H[j][u] (x-side contraction, fixed
-// order) and writes them; with identical sides only tiles on or above the
-// diagonal are computed and mirrored (G is symmetric).
+// Tile = (x block I, y block J).  Thread t owns x locations t and t+128 of
+// the block (twins merged, <= 256 per block).  The block's y records (unique
+// y locations with their <= 2 (slot, coef) pairs, sorted by first slot) and
+// the x support lists are staged in shared memory.  All threads walk the same
+// record list (broadcast reads) and evaluate G(u, v) once per unique location
+// pair — two x locations per record, so record loads and the uniform run /
+// slot branches are shared by two pair evaluations and every thread carries
+// 2 x kRecUnroll independent FP64 chains.  c0*G goes to a register run
+// accumulator for the record's first slot (flushed when the slot changes),
+// c1*G is added into H[slot][u] in shared memory: the y-side contraction,
+// owner-computes per column, no atomics.  After a barrier each thread gathers
+// whole entries A_ij = sum_u c_ui H[j][u] (x-side contraction, fixed order)
+// and writes them; with identical sides only tiles on or above the diagonal
+// are computed and mirrored (G is symmetric).
+//
+// Specialisations: MASK (tile may hold a coincident pair -> r^2 <= eps^2
+// mask), S1 (some record has a second slot; P0 with twin-free rules has none).
 #include <cuda_runtime.h>
 
 #include "gk_internal.hpp"
@@ -24,6 +30,8 @@
 namespace gk {
 
 namespace {
+
+constexpr int kRecUnroll = 2;  // records per group (x kUPT locations = independent evaluations)
 
 struct AsmSmem {
   double2 H[kJCap * kUCap];
@@ -43,8 +51,9 @@ __device__ __forceinline__ void rmw(char* Hb, int off, double c, double gr, doub
   *h = v;
 }
 
-template <bool HELM>
+template <bool HELM, bool MASK, bool S1>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
+  static_assert(kUPT == 2, "two x locations per thread");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int tile = blockIdx.x;
@@ -70,57 +79,81 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   for (int e = t; e <= nI; e += kAsmThreads) S.xs_start[e] = __ldg(a.xsup_start + i0 + e) - xs0;
   for (int e = t; e < nI; e += kAsmThreads) S.orow[e] = __ldg(a.xperm + i0 + e);
   for (int e = t; e < nJ; e += kAsmThreads) S.ocol[e] = __ldg(a.yperm + j0 + e);
-  double ux = 0.0, uy = 0.0, uz = 0.0;
-  if (t < nu) {
-    ux = __ldg(a.xl_x + l0 + t);
-    uy = __ldg(a.xl_y + l0 + t);
-    uz = __ldg(a.xl_z + l0 + t);
-  } else {
-    ux = 1e100;  // idle columns: far away, finite, never gathered
+  // my two x locations; idle columns are far away (finite, never gathered)
+  double ux[kUPT], uy[kUPT], uz[kUPT];
+#pragma unroll
+  for (int h = 0; h < kUPT; ++h) {
+    const int c = t + h * kAsmThreads;
+    ux[h] = c < nu ? __ldg(a.xl_x + l0 + c) : 1e100;
+    uy[h] = c < nu ? __ldg(a.xl_y + l0 + c) : 0.0;
+    uz[h] = c < nu ? __ldg(a.xl_z + l0 + c) : 0.0;
   }
   __syncthreads();
 
   const double eps2 = a.eps2, kappa = a.kappa;
-  char* Hb = reinterpret_cast<char*>(S.H) + t * 16;
+  char* Hb0 = reinterpret_cast<char*>(S.H) + t * 16;
+  char* Hb1 = Hb0 + kAsmThreads * 16;
   int cur = -1;  // byte offset of the run's slot row
-  double ar = 0.0, ai = 0.0;
-  // fold one evaluated pair into the run accumulator / second slot (uniform branches)
-  auto fold = [&](const YRec& p, const c64& g) {
+  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+  // fold one record's two evaluated pairs (uniform branches)
+  auto fold = [&](const YRec& p, const c64& g0, const c64& g1) {
     if (p.off0 != cur) {
-      if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+      if (cur >= 0) {
+        rmw(Hb0, cur, 1.0, ar0, ai0);
+        rmw(Hb1, cur, 1.0, ar1, ai1);
+      }
       cur = p.off0;
-      ar = 0.0;
-      ai = 0.0;
+      ar0 = ai0 = ar1 = ai1 = 0.0;
     }
-    ar = fma(p.c0, g.re, ar);
-    ai = fma(p.c0, g.im, ai);
-    if (p.off1 >= 0) rmw(Hb, p.off1, p.c1, g.re, g.im);
+    ar0 = fma(p.c0, g0.re, ar0);
+    ai0 = fma(p.c0, g0.im, ai0);
+    ar1 = fma(p.c0, g1.re, ar1);
+    ai1 = fma(p.c0, g1.im, ai1);
+    if (S1 && p.off1 >= 0) {
+      rmw(Hb0, p.off1, p.c1, g0.re, g0.im);
+      rmw(Hb1, p.off1, p.c1, g1.re, g1.im);
+    }
   };
-  constexpr int kUnroll = 4;  // independent pair evaluations in flight per thread
+  constexpr int N = kRecUnroll * kUPT;
   int r = 0;
-  for (; r + kUnroll <= nrec; r += kUnroll) {
-    double dx[kUnroll], dy[kUnroll], dz[kUnroll];
+  for (; r + kRecUnroll <= nrec; r += kRecUnroll) {
+    double dx[N], dy[N], dz[N];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < kRecUnroll; ++k) {
       const double2 a0 = *reinterpret_cast<const double2*>(&S.rec[r + k].x);
       const double2 a1 = *reinterpret_cast<const double2*>(&S.rec[r + k].z);
-      dx[k] = ux - a0.x;
-      dy[k] = uy - a0.y;
-      dz[k] = uz - a1.x;
-    }
-    c64 g[kUnroll];
-    green_n<HELM, kUnroll>(dx, dy, dz, eps2, kappa, g);
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) fold(S.rec[r + k], g[k]);
+      for (int h = 0; h < kUPT; ++h) {
+        dx[k * kUPT + h] = ux[h] - a0.x;
+        dy[k * kUPT + h] = uy[h] - a0.y;
+        dz[k * kUPT + h] = uz[h] - a1.x;
+      }
+    }
+    c64 g[N];
+    green_n<HELM, N, MASK>(dx, dy, dz, eps2, kappa, g);
+#pragma unroll
+    for (int k = 0; k < kRecUnroll; ++k) fold(S.rec[r + k], g[k * kUPT], g[k * kUPT + 1]);
   }
   for (; r < nrec; ++r) {
     const YRec& p = S.rec[r];
-    fold(p, green<HELM>(ux - p.x, uy - p.y, uz - p.z, eps2, kappa));
+    double dx[kUPT], dy[kUPT], dz[kUPT];
+#pragma unroll
+    for (int h = 0; h < kUPT; ++h) {
+      dx[h] = ux[h] - p.x;
+      dy[h] = uy[h] - p.y;
+      dz[h] = uz[h] - p.z;
+    }
+    c64 g[kUPT];
+    green_n<HELM, kUPT, MASK>(dx, dy, dz, eps2, kappa, g);
+    fold(p, g[0], g[1]);
   }
-  if (cur >= 0) rmw(Hb, cur, 1.0, ar, ai);
+  if (cur >= 0) {
+    rmw(Hb0, cur, 1.0, ar0, ai0);
+    rmw(Hb1, cur, 1.0, ar1, ai1);
+  }
   __syncthreads();
 
-  // x-side contraction + write (lanes along rows: coalesced columns for P0)
+  // x-side contraction + write (lanes along rows: coalesced columns for the natural order)
   double2* A = reinterpret_cast<double2*>(a.A);
   const long long lda = a.lda;
   const int total = nI * nJ;
@@ -151,25 +184,37 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   }
 }
 
-}  // namespace
-
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, void* stream) {
-  if (ntiles <= 0) return;
+template <bool HELM, bool MASK, bool S1>
+void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
   const size_t smem = sizeof(AsmSmem);
-  static bool configured = false;
+  static bool configured = false;  // one flag per instantiation
   if (!configured) {
-    cuda_check(cudaFuncSetAttribute(k_assemble<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "cudaFuncSetAttribute");
-    cuda_check(cudaFuncSetAttribute(k_assemble<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, MASK, S1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
+  k_assemble<HELM, MASK, S1><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+}
+
+}  // namespace
+
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, bool second_slot,
+                     void* stream) {
+  if (ntiles <= 0) return;
   if (ntiles > INT32_MAX) throw std::invalid_argument("bem_dense: too many tiles");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (helmholtz)
-    k_assemble<true><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
-  else
-    k_assemble<false><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+  const int sel = (helmholtz ? 4 : 0) | (mask ? 2 : 0) | (second_slot ? 1 : 0);
+  switch (sel) {
+    case 0: launch_one<false, false, false>(a, ntiles, s); break;
+    case 1: launch_one<false, false, true>(a, ntiles, s); break;
+    case 2: launch_one<false, true, false>(a, ntiles, s); break;
+    case 3: launch_one<false, true, true>(a, ntiles, s); break;
+    case 4: launch_one<true, false, false>(a, ntiles, s); break;
+    case 5: launch_one<true, false, true>(a, ntiles, s); break;
+    case 6: launch_one<true, true, false>(a, ntiles, s); break;
+    default: launch_one<true, true, true>(a, ntiles, s); break;
+  }
   cuda_check(cudaGetLastError(), "k_assemble launch");
 }
 

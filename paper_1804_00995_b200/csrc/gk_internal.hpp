@@ -107,12 +107,13 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // needs ~16 warps/SM at 2-3 independent chains per warp).  Two 256-thread CTAs
 // per SM: shared memory per CTA = H (kJCap x kUCap x 16 B = 96 KB) + staged
 // records and x supports (~15 KB).
-constexpr int kUCap = 256;   // x locations per tile (one per thread)
+constexpr int kUCap = 256;   // x locations per tile (kUPT per thread)
+constexpr int kUPT = 2;      // x locations per thread: records and branches shared by 2 pairs
 constexpr int kJCap = 24;    // y dofs per tile (H accumulator rows)
 constexpr int kIMax = 256;   // x dofs per tile
 constexpr int kRCap = 128;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 640;  // x support entries per tile (staged in shared memory)
-constexpr int kAsmThreads = 256;
+constexpr int kAsmThreads = kUCap / kUPT;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
@@ -138,16 +139,20 @@ struct TileTables {
   std::vector<int32_t> yb_dof_start;  // [nJb+1]
   std::vector<int32_t> yb_rec_start;  // [nJb+1]
   std::vector<YRec> yrec;
-  // tiles
-  std::vector<int32_t> tile_i, tile_j;
+  // tiles: `masked` tiles may contain coincident location pairs and apply the
+  // r^2 <= eps^2 mask; the others provably cannot (exact coincidences only,
+  // checked on the host) and skip it.
+  std::vector<int32_t> tile_i, tile_j;          // unmasked tiles
+  std::vector<int32_t> mtile_i, mtile_j;        // masked tiles
+  bool has_second_slot = false;                 // any record with off1 >= 0
   int64_t pairs_evaluated = 0;
   double x_halo = 0.0, y_halo = 0.0;
 };
-TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric);
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, double eps);
 // Picks natural vs RCB order by the evaluated pair count of the resulting
 // tiles (natural preferred within 10%: coalesced writes); GK_ORDER=natural|rcb
 // overrides.  Y may be null (symmetric: Y = X).
-TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric);
+TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps);
 
 struct AsmArgs {
   const int32_t* tile_i;
@@ -171,7 +176,8 @@ struct AsmArgs {
   double kappa;  // 2k/pi
   int32_t symmetric;
 };
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, void* stream);
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, bool second_slot,
+                     void* stream);
 
 // ---- matvec ---------------------------------------------------------------------------
 void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,

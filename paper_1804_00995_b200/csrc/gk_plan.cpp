@@ -246,9 +246,10 @@ int64_t cut(const Locations& L, int64_t start, int64_t end_max) {
 }
 }  // namespace
 
-TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, double eps) {
   TileTables T;
   const int64_t nrows = X.nfree, ncols = Y.nfree;
+  std::vector<int32_t> xl_id;  // global x location id of every block entry (parallel to xl_x)
   // ---- x blocks: consecutive permuted rows while their locations fit kUCap
   std::vector<int64_t> owner(X.size(), -1);
   std::vector<int32_t> local(X.size(), 0);
@@ -295,6 +296,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
       T.xl_x.push_back(X.x[u]);
       T.xl_y.push_back(X.y[u]);
       T.xl_z.push_back(X.z[u]);
+      xl_id.push_back(u);
     }
     T.xb_dof_start.push_back((int32_t)p);
     T.xb_loc_start.push_back((int32_t)T.xl_x.size());
@@ -309,8 +311,13 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
   T.yb_dof_start.push_back(0);
   T.yb_rec_start.push_back(0);
   std::vector<YRec> recs;
+  std::vector<int32_t> rec_loc;                  // y location id of each record of the block
+  std::vector<std::vector<int32_t>> yblocks_of;  // y location -> y blocks holding it
+  if (!symmetric || &X != &Y) yblocks_of.resize(Y.size());
+  else yblocks_of.resize(X.size());
   auto make_records = [&](int64_t q0, int64_t q1) {
     recs.clear();
+    rec_loc.clear();
     ++stamp_id;
     for (int64_t q = q0; q < q1; ++q)
       for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
@@ -338,9 +345,20 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
             r.c1 = 0.0;
           }
           recs.push_back(r);
+          rec_loc.push_back(v);
         }
       }
-    std::stable_sort(recs.begin(), recs.end(), [](const YRec& a, const YRec& b) { return a.off0 < b.off0; });
+    std::vector<int32_t> order(recs.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return recs[a].off0 < recs[b].off0; });
+    std::vector<YRec> r2(recs.size());
+    std::vector<int32_t> l2(recs.size());
+    for (size_t i = 0; i < order.size(); ++i) {
+      r2[i] = recs[order[i]];
+      l2[i] = rec_loc[order[i]];
+    }
+    recs.swap(r2);
+    rec_loc.swap(l2);
   };
   for (int64_t q0 = 0; q0 < ncols;) {
     int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
@@ -357,33 +375,83 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric) {
     if ((int64_t)recs.size() > kRCap)
       throw std::invalid_argument("bem_dense: a trial dof is supported by more than " + std::to_string(kRCap) +
                                   " quadrature locations");
+    const int32_t bj = (int32_t)T.yb_dof_start.size() - 1;
+    for (int32_t v : rec_loc)
+      if (yblocks_of[v].empty() || yblocks_of[v].back() != bj) yblocks_of[v].push_back(bj);
+    for (const YRec& r : recs) T.has_second_slot |= r.off1 >= 0;
     T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
     T.yb_dof_start.push_back((int32_t)q1);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
     q0 = q1;
   }
-  // ---- tiles (symmetric: skip tiles strictly below the diagonal)
   const int64_t nIb = (int64_t)T.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
+
+  // ---- which tiles can hold a coincident (masked) pair?  Masking matters only
+  // for r^2 <= eps^2.  If every such pair is an exact coincidence (checked with
+  // a grid of cell 16 eps), masked pairs are x/y locations with identical
+  // coordinates, and only tiles containing one need the mask.
+  const bool same = &X == &Y;
+  std::vector<int32_t> y_of_x(X.size(), -1);
+  bool unsafe = !(eps > 0.0);
+  if (!unsafe) {
+    const double cell = 16.0 * eps, near2 = (8.0 * eps) * (8.0 * eps);
+    auto key = [cell](double a, double b, double c) {
+      return Key{(uint64_t)(int64_t)std::floor(a / cell), (uint64_t)(int64_t)std::floor(b / cell),
+                 (uint64_t)(int64_t)std::floor(c / cell)};
+    };
+    std::unordered_map<Key, std::vector<int32_t>, KeyHash> grid;
+    grid.reserve((size_t)Y.size());
+    for (int64_t v = 0; v < Y.size(); ++v) grid[key(Y.x[v], Y.y[v], Y.z[v])].push_back((int32_t)v);
+    for (int64_t u = 0; u < X.size() && !unsafe; ++u) {
+      const Key k = key(X.x[u], X.y[u], X.z[u]);
+      for (int dx = -1; dx <= 1 && !unsafe; ++dx)
+        for (int dy = -1; dy <= 1 && !unsafe; ++dy)
+          for (int dz = -1; dz <= 1 && !unsafe; ++dz) {
+            auto it = grid.find(Key{k.a + (uint64_t)(int64_t)dx, k.b + (uint64_t)(int64_t)dy, k.c + (uint64_t)(int64_t)dz});
+            if (it == grid.end()) continue;
+            for (int32_t v : it->second) {
+              const double ex = X.x[u] - Y.x[v], ey = X.y[u] - Y.y[v], ez = X.z[u] - Y.z[v];
+              if (ex * ex + ey * ey + ez * ez > near2) continue;
+              if (bits(X.x[u]) == bits(Y.x[v]) && bits(X.y[u]) == bits(Y.y[v]) && bits(X.z[u]) == bits(Y.z[v]))
+                y_of_x[u] = v;
+              else
+                unsafe = true;  // a near-coincidence that is not exact: keep the mask everywhere
+            }
+          }
+    }
+    if (same)
+      for (int64_t u = 0; u < X.size(); ++u) y_of_x[u] = (int32_t)u;
+  }
+  std::unordered_map<int64_t, char> masked;
+  if (!unsafe)
+    for (int64_t bi = 0; bi < nIb; ++bi)
+      for (int32_t e = T.xb_loc_start[bi]; e < T.xb_loc_start[bi + 1]; ++e) {
+        const int32_t v = y_of_x[xl_id[e]];
+        if (v < 0) continue;
+        for (int32_t bj : yblocks_of[v]) masked[bi * nJb + bj] = 1;
+      }
+  // ---- tiles (symmetric: skip tiles strictly below the diagonal)
   for (int64_t bi = 0; bi < nIb; ++bi)
     for (int64_t bj = 0; bj < nJb; ++bj) {
       if (symmetric && T.yb_dof_start[bj + 1] - 1 < T.xb_dof_start[bi]) continue;
-      T.tile_i.push_back((int32_t)bi);
-      T.tile_j.push_back((int32_t)bj);
+      const bool m = unsafe || masked.count(bi * nJb + bj);
+      (m ? T.mtile_i : T.tile_i).push_back((int32_t)bi);
+      (m ? T.mtile_j : T.tile_j).push_back((int32_t)bj);
       T.pairs_evaluated += (int64_t)(T.xb_loc_start[bi + 1] - T.xb_loc_start[bi]) *
                            (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
     }
   return T;
 }
 
-TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric) {
+TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps) {
   const char* force = std::getenv("GK_ORDER");
   const std::string f = force ? force : "";
   auto tile = [&](bool natural) {
     set_order(X, natural);
     if (Y) set_order(*Y, natural);
-    return build_tiles(X, Y ? *Y : X, symmetric);
+    return build_tiles(X, Y ? *Y : X, symmetric, eps);
   };
   if (f == "natural") return tile(true);
   if (f == "rcb") return tile(false);

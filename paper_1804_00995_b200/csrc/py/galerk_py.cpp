@@ -55,6 +55,7 @@ py::dict info_dict(const gk_plan_info& i) {
   d["pairs_unique"] = i.pairs_unique;
   d["pairs_evaluated"] = i.pairs_evaluated;
   d["tiles"] = i.tiles;
+  d["masked_tiles"] = i.masked_tiles;
   d["symmetric"] = (bool)i.symmetric;
   d["eps"] = i.eps;
   d["device_bytes"] = i.device_bytes;
