@@ -31,7 +31,7 @@ namespace gk {
 
 namespace {
 
-constexpr int kRecUnroll = 2;  // records per group (x kUPT locations = independent evaluations)
+constexpr int kRecUnroll = 4 / kUPT;  // records per group (x kUPT locations = 4 independent evaluations)
 
 struct AsmSmem {
   double2 H[kJCap * kUCap];
@@ -53,7 +53,6 @@ __device__ __forceinline__ void rmw(char* Hb, int off, double c, double gr, doub
 
 template <bool HELM, bool MASK, bool S1>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
-  static_assert(kUPT == 2, "two x locations per thread");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int tile = blockIdx.x;
@@ -91,28 +90,31 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   __syncthreads();
 
   const double eps2 = a.eps2, kappa = a.kappa;
-  char* Hb0 = reinterpret_cast<char*>(S.H) + t * 16;
-  char* Hb1 = Hb0 + kAsmThreads * 16;
+  char* Hb[kUPT];
+#pragma unroll
+  for (int h = 0; h < kUPT; ++h) Hb[h] = reinterpret_cast<char*>(S.H) + (t + h * kAsmThreads) * 16;
   int cur = -1;  // byte offset of the run's slot row
-  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
-  // fold one record's two evaluated pairs (uniform branches)
-  auto fold = [&](const YRec& p, const c64& g0, const c64& g1) {
+  double ar[kUPT], ai[kUPT];
+#pragma unroll
+  for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
+  // fold one record's kUPT evaluated pairs (uniform branches)
+  auto fold = [&](const YRec& p, const c64* g) {
     if (p.off0 != cur) {
-      if (cur >= 0) {
-        rmw(Hb0, cur, 1.0, ar0, ai0);
-        rmw(Hb1, cur, 1.0, ar1, ai1);
-      }
+      if (cur >= 0)
+#pragma unroll
+        for (int h = 0; h < kUPT; ++h) rmw(Hb[h], cur, 1.0, ar[h], ai[h]);
       cur = p.off0;
-      ar0 = ai0 = ar1 = ai1 = 0.0;
+#pragma unroll
+      for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
     }
-    ar0 = fma(p.c0, g0.re, ar0);
-    ai0 = fma(p.c0, g0.im, ai0);
-    ar1 = fma(p.c0, g1.re, ar1);
-    ai1 = fma(p.c0, g1.im, ai1);
-    if (S1 && p.off1 >= 0) {
-      rmw(Hb0, p.off1, p.c1, g0.re, g0.im);
-      rmw(Hb1, p.off1, p.c1, g1.re, g1.im);
+#pragma unroll
+    for (int h = 0; h < kUPT; ++h) {
+      ar[h] = fma(p.c0, g[h].re, ar[h]);
+      ai[h] = fma(p.c0, g[h].im, ai[h]);
     }
+    if (S1 && p.off1 >= 0)
+#pragma unroll
+      for (int h = 0; h < kUPT; ++h) rmw(Hb[h], p.off1, p.c1, g[h].re, g[h].im);
   };
   constexpr int N = kRecUnroll * kUPT;
   int r = 0;
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     c64 g[N];
     green_n<HELM, N, MASK>(dx, dy, dz, eps2, kappa, g);
 #pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) fold(S.rec[r + k], g[k * kUPT], g[k * kUPT + 1]);
+    for (int k = 0; k < kRecUnroll; ++k) fold(S.rec[r + k], g + k * kUPT);
   }
   for (; r < nrec; ++r) {
     const YRec& p = S.rec[r];
@@ -145,12 +147,11 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     }
     c64 g[kUPT];
     green_n<HELM, kUPT, MASK>(dx, dy, dz, eps2, kappa, g);
-    fold(p, g[0], g[1]);
+    fold(p, g);
   }
-  if (cur >= 0) {
-    rmw(Hb0, cur, 1.0, ar0, ai0);
-    rmw(Hb1, cur, 1.0, ar1, ai1);
-  }
+  if (cur >= 0)
+#pragma unroll
+    for (int h = 0; h < kUPT; ++h) rmw(Hb[h], cur, 1.0, ar[h], ai[h]);
   __syncthreads();
 
   // x-side contraction + write (lanes along rows: coalesced columns for the natural order)

@@ -108,7 +108,7 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // per SM: shared memory per CTA = H (kJCap x kUCap x 16 B = 96 KB) + staged
 // records and x supports (~15 KB).
 constexpr int kUCap = 256;   // x locations per tile (kUPT per thread)
-constexpr int kUPT = 2;      // x locations per thread: records and branches shared by 2 pairs
+constexpr int kUPT = 1;      // x locations per thread (2 measured slower: 8 warps/SM)
 constexpr int kJCap = 24;    // y dofs per tile (H accumulator rows)
 constexpr int kIMax = 256;   // x dofs per tile
 constexpr int kRCap = 128;   // y records per tile (staged in shared memory)
