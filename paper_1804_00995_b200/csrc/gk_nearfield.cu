@@ -90,39 +90,49 @@ struct WarpSmem {
   YTri tri;
 };
 
-__device__ void analytic(const YTri& T, V3 x, double& newton, V3& moment, V3& rho) {
-  // kernels.cpp:151-207 with the y-triangle frame precomputed
+// kernels.cpp:151-207 with the y-triangle frame precomputed, written for ILP:
+// the three edges are independent chains (unrolled, branch-free selects for
+// the cancellation-safe log argument), and
+//   beta = atan(t sp / A_p) - atan(t sm / A_m),   A_p, A_m > 0,
+// is evaluated as one atan2 of the complex product (A_p + i t sp)(A_m - i t sm):
+// both angles lie in (-pi/2, pi/2), so their difference is the product's
+// argument exactly (no branch wrap), with one transcendental and no division.
+template <bool MOMENT>
+__device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3& moment, V3& rho) {
   const double w0 = dot(x - T.v[0], T.n), aw0 = fabs(w0);
   rho = x - w0 * T.n;
-  double nw = 0.0;
-  V3 mom = mk(0, 0, 0);
   double rv[3];
+#pragma unroll
   for (int i = 0; i < 3; ++i) rv[i] = nrm(x - T.v[i]);  // rp of edge i == rm of edge i+1
+  double f[3], beta[3], t[3], mo[3];
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int ip = i == 2 ? 0 : i + 1;
-    if (T.len[i] <= 1e-300) continue;
-    const V3 pm = T.v[i], pp = T.v[ip];
-    const double t = dot(pm - rho, T.m_hat[i]);
-    const double sm = dot(pm - rho, T.s_hat[i]);
-    const double sp = dot(pp - rho, T.s_hat[i]);
+    const V3 dm = T.v[i] - rho, dp = T.v[ip] - rho;
+    const double ti = dot(dm, T.m_hat[i]);
+    const double sm = dot(dm, T.s_hat[i]);
+    const double sp = dot(dp, T.s_hat[i]);
     const double rm = rv[i], rp = rv[ip];
-    const double r0sq = t * t + w0 * w0;
-    double f = 0.0;
-    if (r0sq > 1e-28 * T.len[i] * T.len[i]) {
-      if (sm >= 0.0)
-        f = log((rp + sp) / (rm + sm));
-      else if (sp <= 0.0)
-        f = log((rm - sm) / (rp - sp));
-      else
-        f = log((rp + sp) * (rm - sm) / r0sq);
-    }
-    const double beta = atan(t * sp / (r0sq + aw0 * rp)) - atan(t * sm / (r0sq + aw0 * rm));
-    nw += t * f - aw0 * beta;
-    const double mo = r0sq * f + sp * rp - sm * rm;
-    mom = mom + mo * (0.5 * T.m_hat[i]);
+    const double r0sq = ti * ti + w0 * w0;
+    const bool a = sm >= 0.0, b = sp <= 0.0;
+    const double num = a ? rp + sp : (b ? rm - sm : (rp + sp) * (rm - sm));
+    const double den = a ? rm + sm : (b ? rp - sp : r0sq);
+    const bool ok = r0sq > 1e-28 * T.len[i] * T.len[i] && T.len[i] > 1e-300;
+    f[i] = ok ? log(num / den) : 0.0;
+    const double Ap = fma(aw0, rp, r0sq), Am = fma(aw0, rm, r0sq);
+    const double Bp = ti * sp, Bm = ti * sm;
+    beta[i] = T.len[i] > 1e-300 ? atan2(Bp * Am - Ap * Bm, Ap * Am + Bp * Bm) : 0.0;
+    t[i] = T.len[i] > 1e-300 ? ti : 0.0;
+    if (MOMENT) mo[i] = r0sq * f[i] + sp * rp - sm * rm;
   }
-  newton = nw;
-  moment = mom;
+  newton = (t[0] * f[0] - aw0 * beta[0]) + (t[1] * f[1] - aw0 * beta[1]) + (t[2] * f[2] - aw0 * beta[2]);
+  if (MOMENT) {
+    V3 mom = mk(0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (T.len[i] > 1e-300) mom = mom + mo[i] * (0.5 * T.m_hat[i]);
+    moment = mom;
+  }
 }
 
 // barycentric corners of sub-cell s (assembly.cpp:587-594):
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
         const double w = c_r7_w[lane] * (measure_x * 1.0);
         double nw;
         V3 mo, rho;
-        analytic(T, x, nw, mo, rho);
+        analytic<NTR == 3>(T, x, nw, mo, rho);
         double d[NTR];
         exact_values<NT, NTR>(T, nw, mo, rho, d);
 #pragma unroll
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
         const double w = c_r7_w[q] * (measure_x * frac);
         double nw;
         V3 mo, rho;
-        analytic(T, x, nw, mo, rho);
+        analytic<NTR == 3>(T, x, nw, mo, rho);
         double d[NTR];
         exact_values<NT, NTR>(T, nw, mo, rho, d);
 #pragma unroll
