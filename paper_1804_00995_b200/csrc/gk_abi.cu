@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <unordered_map>
 
@@ -123,7 +126,18 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;  // "[1/r]" forces k = 0 (kernels.cpp:47-49)
   P->eps = guard_radius(*test, *trial);
   P->symmetric = o.symmetric == 1 || (o.symmetric < 0 && sides_identical(*test, *trial));
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = now();
+    std::fprintf(stderr, "[gk_plan] %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   Locations X = build_locations(*test, "bem_dense(test)");
+  lap("locations(test)");
   Locations Y;
   if (P->symmetric) {
     if (!sides_identical(*test, *trial))
@@ -131,7 +145,9 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   } else {
     Y = build_locations(*trial, "bem_dense(trial)");
   }
+  lap("locations(trial)");
   TileTables T = choose_order_and_tile(X, P->symmetric ? nullptr : &Y, P->symmetric, P->eps);
+  lap("order+tiles");
   const Locations& Yr = P->symmetric ? X : Y;
   P->xloc = X.size();
   P->yloc = Yr.size();
@@ -162,6 +178,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->yrec.upload(T.yrec);
   P->xperm.upload(X.perm);
   P->yperm.upload(Yr.perm);
+  lap("upload");
   return P;
 }
 

@@ -148,7 +148,23 @@ struct TileTables {
   int64_t pairs_evaluated = 0;
   double x_halo = 0.0, y_halo = 0.0;
 };
-TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, double eps);
+// Exact x/y location coincidences (the only pairs the r^2 <= eps^2 mask can
+// hit when `unsafe` is false: no two points closer than 8 eps are distinct).
+struct Coincidence {
+  std::vector<int32_t> y_of_x;  // y location with the same coordinates, or -1
+  bool unsafe = false;          // some near-coincidence is not exact: mask every tile
+};
+Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same, double eps);
+// Block boundaries for the current dof orders and the pairs they evaluate
+// (count-only: cheap enough to compare orders).
+struct BlockLayout {
+  std::vector<int32_t> xb, xloc;  // x block dof starts [nIb+1], locations per block
+  std::vector<int32_t> yb, yrec;  // y block dof starts [nJb+1], records per block
+  int64_t pairs = 0;
+};
+BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric);
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
+                       const BlockLayout& B);
 // Picks natural vs RCB order by the evaluated pair count of the resulting
 // tiles (natural preferred within 10%: coalesced writes); GK_ORDER=natural|rcb
 // overrides.  Y may be null (symmetric: Y = X).

@@ -4,7 +4,9 @@
 // matrices (W B)^T and per-dof std::map lists; here the same information is
 // laid out for the device as unique locations + per-tile tables.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <numeric>
 #include <cstdlib>
 #include <unordered_map>
@@ -246,23 +248,18 @@ int64_t cut(const Locations& L, int64_t start, int64_t end_max) {
 }
 }  // namespace
 
-TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, double eps) {
-  TileTables T;
+BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric) {
+  BlockLayout B;
   const int64_t nrows = X.nfree, ncols = Y.nfree;
-  std::vector<int32_t> xl_id;  // global x location id of every block entry (parallel to xl_x)
-  // ---- x blocks: consecutive permuted rows while their locations fit kUCap
+  // ---- x blocks: consecutive permuted rows while their locations fit kUCap,
+  // cut back to the strongest order boundary
   std::vector<int64_t> owner(X.size(), -1);
-  std::vector<int32_t> local(X.size(), 0);
-  T.xb_dof_start.push_back(0);
-  T.xb_loc_start.push_back(0);
-  T.xsup_start.assign(nrows + 1, 0);
-  int64_t p = 0, blk = 0, trial_id = -2;
-  std::vector<int32_t> blk_locs;
+  int64_t p = 0, trial_id = 0;
+  B.xb.push_back(0);
   while (p < nrows) {
     const int64_t start = p;
-    // pass 1: the largest end that fits kUCap locations / kXsCap supports
     int64_t end = start, nl = 0, ns = 0;
-    --trial_id;
+    ++trial_id;
     while (end < nrows && end - start < kIMax) {
       int fresh = 0;  // a row lists each location once (merged per (location, dof))
       for (int64_t s = X.dstart[end]; s < X.dstart[end + 1]; ++s) fresh += owner[X.dloc[s]] != trial_id;
@@ -277,6 +274,87 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, d
       throw std::invalid_argument("bem_dense: a test dof is supported by more than " + std::to_string(kUCap) +
                                   " quadrature locations");
     end = cut(X, start, end);
+    ++trial_id;  // count the locations of the final block
+    int64_t nloc = 0;
+    for (int64_t q = start; q < end; ++q)
+      for (int64_t s = X.dstart[q]; s < X.dstart[q + 1]; ++s)
+        if (owner[X.dloc[s]] != trial_id) {
+          owner[X.dloc[s]] = trial_id;
+          ++nloc;
+        }
+    B.xb.push_back((int32_t)end);
+    B.xloc.push_back((int32_t)nloc);
+    p = end;
+  }
+  // ---- y blocks: up to kJCap consecutive permuted cols (fewer if their
+  // records would exceed kRCap), cut back to the strongest order boundary
+  std::vector<int64_t> ystamp(Y.size(), -1);
+  int64_t sid = 0;
+  auto count_records = [&](int64_t q0, int64_t q1) {
+    ++sid;
+    int64_t n = 0;
+    for (int64_t q = q0; q < q1; ++q)
+      for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
+        const int32_t v = Y.dloc[s];
+        if (ystamp[v] == sid) continue;
+        ystamp[v] = sid;
+        int slots = 0;
+        for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
+          const int32_t pq = Y.iperm[Y.cdof[c]];
+          slots += pq >= q0 && pq < q1;
+        }
+        n += (slots + 1) / 2;
+      }
+    return n;
+  };
+  B.yb.push_back(0);
+  for (int64_t q0 = 0; q0 < ncols;) {
+    int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+    int64_t nrec = count_records(q0, q1);
+    while (nrec > kRCap && q1 - q0 > 1) {
+      q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 7 / 8);
+      nrec = count_records(q0, q1);
+    }
+    const int64_t qc = cut(Y, q0, q1);
+    if (qc != q1) {
+      q1 = qc;
+      nrec = count_records(q0, q1);
+    }
+    if (nrec > kRCap)
+      throw std::invalid_argument("bem_dense: a trial dof is supported by more than " + std::to_string(kRCap) +
+                                  " quadrature locations");
+    B.yb.push_back((int32_t)q1);
+    B.yrec.push_back((int32_t)nrec);
+    q0 = q1;
+  }
+  // ---- evaluated pairs: symmetric plans keep tiles whose last column >= first row
+  const int64_t nJb = (int64_t)B.yrec.size();
+  std::vector<int64_t> suffix(nJb + 1, 0);
+  for (int64_t bj = nJb - 1; bj >= 0; --bj) suffix[bj] = suffix[bj + 1] + B.yrec[bj];
+  for (size_t bi = 0; bi < B.xloc.size(); ++bi) {
+    int64_t first = 0;
+    if (symmetric)  // first y block with yb[bj+1] - 1 >= xb[bi]
+      first = std::upper_bound(B.yb.begin() + 1, B.yb.end(), B.xb[bi]) - (B.yb.begin() + 1);
+    B.pairs += (int64_t)B.xloc[bi] * suffix[first];
+  }
+  return B;
+}
+
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
+                       const BlockLayout& B) {
+  TileTables T;
+  const int64_t nrows = X.nfree;
+  std::vector<int32_t> xl_id;  // global x location id of every block entry (parallel to xl_x)
+  // ---- x blocks (boundaries from the layout)
+  std::vector<int64_t> owner(X.size(), -1);
+  std::vector<int32_t> local(X.size(), 0);
+  T.xb_dof_start.push_back(0);
+  T.xb_loc_start.push_back(0);
+  T.xsup_start.assign(nrows + 1, 0);
+  int64_t p = 0;
+  std::vector<int32_t> blk_locs;
+  for (size_t blk = 0; blk + 1 < B.xb.size(); ++blk) {
+    const int64_t end = B.xb[blk + 1];
     blk_locs.clear();
     while (p < end) {
       for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
@@ -300,21 +378,18 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, d
     }
     T.xb_dof_start.push_back((int32_t)p);
     T.xb_loc_start.push_back((int32_t)T.xl_x.size());
-    ++blk;
   }
-  // ---- y blocks: up to kJCap consecutive permuted cols (fewer if their
-  // records would exceed kRCap); records = incident locations, each carrying
-  // <= 2 (slot, coef) pairs, ordered by first slot so that the kernel can keep
-  // a run accumulator for it in registers.
+  // ---- y blocks (boundaries from the layout): records = incident locations,
+  // each carrying <= 2 (slot, coef) pairs, ordered by first slot so that the
+  // kernel can keep a run accumulator for it in registers.
   std::vector<int64_t> ystamp(Y.size(), -1);
   int64_t stamp_id = 0;
   T.yb_dof_start.push_back(0);
   T.yb_rec_start.push_back(0);
   std::vector<YRec> recs;
   std::vector<int32_t> rec_loc;                  // y location id of each record of the block
-  std::vector<std::vector<int32_t>> yblocks_of;  // y location -> y blocks holding it
-  if (!symmetric || &X != &Y) yblocks_of.resize(Y.size());
-  else yblocks_of.resize(X.size());
+  std::vector<std::vector<int32_t>> yblocks_of(Y.size());  // y location -> y blocks holding it
+  std::vector<std::pair<int32_t, double>> sl;    // slots of one location inside the block
   auto make_records = [&](int64_t q0, int64_t q1) {
     recs.clear();
     rec_loc.clear();
@@ -324,7 +399,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, d
         const int32_t v = Y.dloc[s];
         if (ystamp[v] == stamp_id) continue;
         ystamp[v] = stamp_id;
-        std::vector<std::pair<int32_t, double>> sl;  // slots of v inside [q0, q1)
+        sl.clear();
         for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
           const int32_t pq = Y.iperm[Y.cdof[c]];
           if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
@@ -360,21 +435,9 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, d
     recs.swap(r2);
     rec_loc.swap(l2);
   };
-  for (int64_t q0 = 0; q0 < ncols;) {
-    int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+  for (size_t b = 0; b + 1 < B.yb.size(); ++b) {
+    const int64_t q0 = B.yb[b], q1 = B.yb[b + 1];
     make_records(q0, q1);
-    while ((int64_t)recs.size() > kRCap && q1 - q0 > 1) {
-      q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 7 / 8);
-      make_records(q0, q1);
-    }
-    const int64_t qc = cut(Y, q0, q1);
-    if (qc != q1) {
-      q1 = qc;
-      make_records(q0, q1);
-    }
-    if ((int64_t)recs.size() > kRCap)
-      throw std::invalid_argument("bem_dense: a trial dof is supported by more than " + std::to_string(kRCap) +
-                                  " quadrature locations");
     const int32_t bj = (int32_t)T.yb_dof_start.size() - 1;
     for (int32_t v : rec_loc)
       if (yblocks_of[v].empty() || yblocks_of[v].back() != bj) yblocks_of[v].push_back(bj);
@@ -382,86 +445,134 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, d
     T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
     T.yb_dof_start.push_back((int32_t)q1);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
-    q0 = q1;
   }
   const int64_t nIb = (int64_t)T.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
 
-  // ---- which tiles can hold a coincident (masked) pair?  Masking matters only
-  // for r^2 <= eps^2.  If every such pair is an exact coincidence (checked with
-  // a grid of cell 16 eps), masked pairs are x/y locations with identical
-  // coordinates, and only tiles containing one need the mask.
-  const bool same = &X == &Y;
-  std::vector<int32_t> y_of_x(X.size(), -1);
-  bool unsafe = !(eps > 0.0);
-  if (!unsafe) {
-    const double cell = 16.0 * eps, near2 = (8.0 * eps) * (8.0 * eps);
-    auto key = [cell](double a, double b, double c) {
-      return Key{(uint64_t)(int64_t)std::floor(a / cell), (uint64_t)(int64_t)std::floor(b / cell),
-                 (uint64_t)(int64_t)std::floor(c / cell)};
-    };
-    std::unordered_map<Key, std::vector<int32_t>, KeyHash> grid;
-    grid.reserve((size_t)Y.size());
-    for (int64_t v = 0; v < Y.size(); ++v) grid[key(Y.x[v], Y.y[v], Y.z[v])].push_back((int32_t)v);
-    for (int64_t u = 0; u < X.size() && !unsafe; ++u) {
-      const Key k = key(X.x[u], X.y[u], X.z[u]);
-      for (int dx = -1; dx <= 1 && !unsafe; ++dx)
-        for (int dy = -1; dy <= 1 && !unsafe; ++dy)
-          for (int dz = -1; dz <= 1 && !unsafe; ++dz) {
-            auto it = grid.find(Key{k.a + (uint64_t)(int64_t)dx, k.b + (uint64_t)(int64_t)dy, k.c + (uint64_t)(int64_t)dz});
-            if (it == grid.end()) continue;
-            for (int32_t v : it->second) {
-              const double ex = X.x[u] - Y.x[v], ey = X.y[u] - Y.y[v], ez = X.z[u] - Y.z[v];
-              if (ex * ex + ey * ey + ez * ez > near2) continue;
-              if (bits(X.x[u]) == bits(Y.x[v]) && bits(X.y[u]) == bits(Y.y[v]) && bits(X.z[u]) == bits(Y.z[v]))
-                y_of_x[u] = v;
-              else
-                unsafe = true;  // a near-coincidence that is not exact: keep the mask everywhere
-            }
-          }
-    }
-    if (same)
-      for (int64_t u = 0; u < X.size(); ++u) y_of_x[u] = (int32_t)u;
-  }
-  std::unordered_map<int64_t, char> masked;
+  // ---- which tiles can hold a coincident (masked) pair?  With only exact
+  // coincidences (find_coincidences), a tile needs the mask iff one of its x
+  // locations coincides with one of its y records' locations.
+  const bool unsafe = C.unsafe;
+  std::vector<std::vector<int32_t>> masked_j(nIb);
   if (!unsafe)
-    for (int64_t bi = 0; bi < nIb; ++bi)
+    for (int64_t bi = 0; bi < nIb; ++bi) {
       for (int32_t e = T.xb_loc_start[bi]; e < T.xb_loc_start[bi + 1]; ++e) {
-        const int32_t v = y_of_x[xl_id[e]];
-        if (v < 0) continue;
-        for (int32_t bj : yblocks_of[v]) masked[bi * nJb + bj] = 1;
+        const int32_t v = C.y_of_x[xl_id[e]];
+        if (v >= 0) masked_j[bi].insert(masked_j[bi].end(), yblocks_of[v].begin(), yblocks_of[v].end());
       }
+      std::sort(masked_j[bi].begin(), masked_j[bi].end());
+    }
   // ---- tiles (symmetric: skip tiles strictly below the diagonal)
-  for (int64_t bi = 0; bi < nIb; ++bi)
-    for (int64_t bj = 0; bj < nJb; ++bj) {
-      if (symmetric && T.yb_dof_start[bj + 1] - 1 < T.xb_dof_start[bi]) continue;
-      const bool m = unsafe || masked.count(bi * nJb + bj);
+  for (int64_t bi = 0; bi < nIb; ++bi) {
+    int64_t first = 0;
+    if (symmetric)
+      first = std::upper_bound(T.yb_dof_start.begin() + 1, T.yb_dof_start.end(), T.xb_dof_start[bi]) -
+              (T.yb_dof_start.begin() + 1);
+    for (int64_t bj = first; bj < nJb; ++bj) {
+      const bool m = unsafe || std::binary_search(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)bj);
       (m ? T.mtile_i : T.tile_i).push_back((int32_t)bi);
       (m ? T.mtile_j : T.tile_j).push_back((int32_t)bj);
       T.pairs_evaluated += (int64_t)(T.xb_loc_start[bi + 1] - T.xb_loc_start[bi]) *
                            (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
     }
+  }
   return T;
+}
+
+Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same, double eps) {
+  // Sweep over x-coordinate-sorted points of both sides with a window of
+  // 8 eps: every pair closer than that must be an exact coincidence, or the
+  // plan keeps the distance mask everywhere.
+  Coincidence C;
+  C.y_of_x.assign(X.size(), -1);
+  if (!(eps > 0.0)) {
+    C.unsafe = true;
+    return C;
+  }
+  const double win = 8.0 * eps, win2 = win * win;
+  struct P {
+    double x;
+    int32_t id;
+    int8_t side;
+  };
+  std::vector<P> pts;
+  pts.reserve(X.size() + (same ? 0 : Y.size()));
+  for (int64_t u = 0; u < X.size(); ++u) pts.push_back({X.x[u], (int32_t)u, 0});
+  if (!same)
+    for (int64_t v = 0; v < Y.size(); ++v) pts.push_back({Y.x[v], (int32_t)v, 1});
+  std::sort(pts.begin(), pts.end(), [](const P& a, const P& b) { return a.x < b.x || (a.x == b.x && a.side < b.side); });
+  auto coord = [&](const P& p, double& x, double& y, double& z) {
+    const Locations& L = p.side ? Y : X;
+    x = L.x[p.id];
+    y = L.y[p.id];
+    z = L.z[p.id];
+  };
+  for (size_t i = 0; i < pts.size() && !C.unsafe; ++i)
+    for (size_t j = i + 1; j < pts.size() && pts[j].x - pts[i].x <= win; ++j) {
+      double ax, ay, az, bx, by, bz;
+      coord(pts[i], ax, ay, az);
+      coord(pts[j], bx, by, bz);
+      const double dx = ax - bx, dy = ay - by, dz = az - bz;
+      if (dx * dx + dy * dy + dz * dz > win2) continue;
+      // within 8 eps: allowed only as an exact x/y coincidence
+      const bool exact = bits(ax) == bits(bx) && bits(ay) == bits(by) && bits(az) == bits(bz);
+      if (same || pts[i].side == pts[j].side || !exact) {
+        C.unsafe = true;  // distinct locations of one side within 8 eps, or a near miss
+        break;
+      }
+      const P& px = pts[i].side == 0 ? pts[i] : pts[j];
+      const P& py = pts[i].side == 0 ? pts[j] : pts[i];
+      C.y_of_x[px.id] = py.id;
+    }
+  if (same && !C.unsafe)
+    for (int64_t u = 0; u < X.size(); ++u) C.y_of_x[u] = (int32_t)u;
+  return C;
 }
 
 TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps) {
   const char* force = std::getenv("GK_ORDER");
   const std::string f = force ? force : "";
-  auto tile = [&](bool natural) {
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gk_plan]   %-20s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  const Coincidence C = find_coincidences(X, Y ? *Y : X, Y == nullptr, eps);
+  lap("coincidences");
+  auto order = [&](bool natural) {
     set_order(X, natural);
     if (Y) set_order(*Y, natural);
-    return build_tiles(X, Y ? *Y : X, symmetric, eps);
+    lap(natural ? "order natural" : "order rcb");
+    BlockLayout B = layout_blocks(X, Y ? *Y : X, symmetric);
+    lap("layout");
+    return B;
   };
-  if (f == "natural") return tile(true);
-  if (f == "rcb") return tile(false);
-  // Natural order keeps the rows of every tile contiguous in A (full-sector,
-  // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
-  // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
-  const int64_t rcb_pairs = tile(false).pairs_evaluated;
-  TileTables nat = tile(true);
-  if ((double)nat.pairs_evaluated <= 1.10 * (double)rcb_pairs) return nat;
-  return tile(false);
+  bool natural;
+  BlockLayout B;
+  if (f == "natural" || f == "rcb") {
+    natural = f == "natural";
+    B = order(natural);
+  } else {
+    // Natural order keeps the rows of every tile contiguous in A (full-sector,
+    // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
+    // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
+    BlockLayout rcb = order(false);
+    B = order(true);
+    natural = (double)B.pairs <= 1.10 * (double)rcb.pairs;
+    if (!natural) {
+      set_order(X, false);  // restore the RCB numbering the layout refers to
+      if (Y) set_order(*Y, false);
+      B = std::move(rcb);
+    }
+  }
+  TileTables T = build_tiles(X, Y ? *Y : X, symmetric, C, B);
+  lap("tiles");
+  return T;
 }
 
 }  // namespace gk
