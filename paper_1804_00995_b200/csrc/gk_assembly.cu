@@ -119,22 +119,35 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   constexpr int N = kRecUnroll * kUPT;
   int r = 0;
   for (; r + kRecUnroll <= nrec; r += kRecUnroll) {
-    double dx[N], dy[N], dz[N];
+    // the whole group's records into registers first (3 LDS.128 each): the H
+    // stores in fold() would otherwise force re-loads of every field
+    YRec rr[kRecUnroll];
 #pragma unroll
     for (int k = 0; k < kRecUnroll; ++k) {
-      const double2 a0 = *reinterpret_cast<const double2*>(&S.rec[r + k].x);
-      const double2 a1 = *reinterpret_cast<const double2*>(&S.rec[r + k].z);
+      const double2* src = reinterpret_cast<const double2*>(&S.rec[r + k]);
+      const double2 a0 = src[0], a1 = src[1], a2 = src[2];
+      rr[k].x = a0.x;
+      rr[k].y = a0.y;
+      rr[k].z = a1.x;
+      rr[k].c0 = a1.y;
+      rr[k].c1 = a2.x;
+      const long long s = __double_as_longlong(a2.y);
+      rr[k].off0 = (int32_t)(s & 0xffffffffll);
+      rr[k].off1 = (int32_t)(s >> 32);
+    }
+    double dx[N], dy[N], dz[N];
+#pragma unroll
+    for (int k = 0; k < kRecUnroll; ++k)
 #pragma unroll
       for (int h = 0; h < kUPT; ++h) {
-        dx[k * kUPT + h] = ux[h] - a0.x;
-        dy[k * kUPT + h] = uy[h] - a0.y;
-        dz[k * kUPT + h] = uz[h] - a1.x;
+        dx[k * kUPT + h] = ux[h] - rr[k].x;
+        dy[k * kUPT + h] = uy[h] - rr[k].y;
+        dz[k * kUPT + h] = uz[h] - rr[k].z;
       }
-    }
     c64 g[N];
     green_n<HELM, N, MASK>(dx, dy, dz, eps2, kappa, g);
 #pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) fold(S.rec[r + k], g + k * kUPT);
+    for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], g + k * kUPT);
   }
   for (; r < nrec; ++r) {
     const YRec& p = S.rec[r];
