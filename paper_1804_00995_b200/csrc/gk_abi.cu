@@ -69,10 +69,11 @@ struct gk_plan {
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false, second_slot = true;
   DevBuf tile_i, tile_j, mtile_i, mtile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u,
-      xsup_c, yb_dof_start, yb_rec_start, yrec, xperm, yperm;
+      xsup_c, yb_dof_start, yb_rec_start, yrec, yb_zero, xperm, yperm;
   uint64_t device_bytes() const {
     const DevBuf* b[] = {&tile_i, &tile_j, &mtile_i, &mtile_j, &xb_dof_start, &xb_loc_start, &xl_x, &xl_y,
-                         &xl_z, &xsup_start, &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &xperm,
+                         &xl_z, &xsup_start, &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &yb_zero,
+                         &xperm,
                          &yperm};
     uint64_t s = 0;
     for (auto* p : b) s += p->bytes;
@@ -176,6 +177,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->yb_dof_start.upload(T.yb_dof_start);
   P->yb_rec_start.upload(T.yb_rec_start);
   P->yrec.upload(T.yrec);
+  P->yb_zero.upload(T.yb_zero);
   P->xperm.upload(X.perm);
   P->yperm.upload(Yr.perm);
   lap("upload");
@@ -201,6 +203,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.yb_dof_start = P->yb_dof_start.as<int32_t>();
   a.yb_rec_start = P->yb_rec_start.as<int32_t>();
   a.yrec = P->yrec.as<YRec>();
+  a.yb_zero = P->yb_zero.as<uint32_t>();
   a.xperm = P->xperm.as<int32_t>();
   a.yperm = P->yperm.as<int32_t>();
   a.A = A;

@@ -64,8 +64,13 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int r0 = a.yb_rec_start[bj], nrec = a.yb_rec_start[bj + 1] - r0;
   const int xs0 = a.xsup_start[i0], nxs = a.xsup_start[i0 + nI] - xs0;
 
-  // stage: zero H rows, copy records and x support lists
-  for (int e = t; e < nJ * kUCap; e += kAsmThreads) S.H[e] = make_double2(0.0, 0.0);
+  // stage: records and x support lists.  Records run in descending first-slot
+  // order, so each H row is first written by its own run flush (a plain store);
+  // only rows without a run (host bitmask) are zero-filled.
+  const uint32_t zero_rows = a.yb_zero[bj];
+  if (zero_rows)
+    for (int e = t; e < nJ * kUCap; e += kAsmThreads)
+      if ((zero_rows >> (e / kUCap)) & 1u) S.H[e] = make_double2(0.0, 0.0);
   {
     const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
     double2* dst = reinterpret_cast<double2*>(S.rec);
@@ -98,11 +103,13 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
 #pragma unroll
   for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
   // fold one record's kUPT evaluated pairs (uniform branches)
+  auto flush = [&]() {
+#pragma unroll
+    for (int h = 0; h < kUPT; ++h) *reinterpret_cast<double2*>(Hb[h] + cur) = make_double2(ar[h], ai[h]);
+  };
   auto fold = [&](const YRec& p, const c64* g) {
     if (p.off0 != cur) {
-      if (cur >= 0)
-#pragma unroll
-        for (int h = 0; h < kUPT; ++h) rmw(Hb[h], cur, 1.0, ar[h], ai[h]);
+      if (cur >= 0) flush();
       cur = p.off0;
 #pragma unroll
       for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
@@ -162,9 +169,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     green_n<HELM, kUPT, MASK>(dx, dy, dz, eps2, kappa, g);
     fold(p, g);
   }
-  if (cur >= 0)
-#pragma unroll
-    for (int h = 0; h < kUPT; ++h) rmw(Hb[h], cur, 1.0, ar[h], ai[h]);
+  if (cur >= 0) flush();
   __syncthreads();
 
   // x-side contraction + write (lanes along rows: coalesced columns for the natural order)

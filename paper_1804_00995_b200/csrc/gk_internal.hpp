@@ -121,6 +121,7 @@ struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   int32_t off0, off1;  // byte offsets slot * kUCap * 16 into H; off1 = -1 if none
 };
 static_assert(sizeof(YRec) == 48, "YRec layout");
+static_assert(kJCap <= 32, "per-block zero-fill mask is 32 bits");
 
 // Dof order used for tiling: natural (input numbering; blocks cut at 4^k
 // boundaries of subdivided meshes, rows of A stay contiguous) or recursive
@@ -139,6 +140,7 @@ struct TileTables {
   std::vector<int32_t> yb_dof_start;  // [nJb+1]
   std::vector<int32_t> yb_rec_start;  // [nJb+1]
   std::vector<YRec> yrec;
+  std::vector<uint32_t> yb_zero;      // [nJb] bitmask of H rows with no run (need zero fill)
   // tiles: `masked` tiles may contain coincident location pairs and apply the
   // r^2 <= eps^2 mask; the others provably cannot (exact coincidences only,
   // checked on the host) and skip it.
@@ -184,6 +186,7 @@ struct AsmArgs {
   const int32_t* yb_dof_start;
   const int32_t* yb_rec_start;
   const YRec* yrec;
+  const uint32_t* yb_zero;
   const int32_t* xperm;
   const int32_t* yperm;
   void* A;

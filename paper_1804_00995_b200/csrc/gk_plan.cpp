@@ -425,7 +425,10 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
       }
     std::vector<int32_t> order(recs.size());
     std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return recs[a].off0 < recs[b].off0; });
+    // Descending first slot: second slots are larger than first slots, so every
+    // second-slot update of a row comes after that row's own run has been
+    // flushed — the run flush is the row's first touch and can be a plain store.
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return recs[a].off0 > recs[b].off0; });
     std::vector<YRec> r2(recs.size());
     std::vector<int32_t> l2(recs.size());
     for (size_t i = 0; i < order.size(); ++i) {
@@ -441,7 +444,14 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
     const int32_t bj = (int32_t)T.yb_dof_start.size() - 1;
     for (int32_t v : rec_loc)
       if (yblocks_of[v].empty() || yblocks_of[v].back() != bj) yblocks_of[v].push_back(bj);
-    for (const YRec& r : recs) T.has_second_slot |= r.off1 >= 0;
+    // rows without a run of their own are only ever read-modify-written: zero them
+    uint32_t has_run = 0;
+    for (const YRec& r : recs) {
+      T.has_second_slot |= r.off1 >= 0;
+      has_run |= 1u << (r.off0 / (kUCap * 16));
+    }
+    const uint32_t all = (q1 - q0) >= 32 ? 0xffffffffu : ((1u << (q1 - q0)) - 1u);
+    T.yb_zero.push_back(all & ~has_run);
     T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
     T.yb_dof_start.push_back((int32_t)q1);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
