@@ -178,6 +178,11 @@ typedef struct gk_mesh_side {
 gk_status gk_nearfield_create(const gk_mesh_side* test, const gk_mesh_side* trial,
                               const char* singular_name, int32_t near_rule, double hbar,
                               gk_nearfield** out);
+/* Collocation form, replacing regularize_radiation (assembly.cpp:699-750):
+ * rows are the given points (host [npts*3] xyz), pairs are (point, element)
+ * with |c_y - x| <= 3 R_y.  Same compute/apply/triplets calls. */
+gk_status gk_nearfield_create_points(int64_t npts, const double* points, const gk_mesh_side* trial,
+                                     const char* singular_name, gk_nearfield** out);
 /* Number of near element pairs and of summed (row, col) entries. */
 gk_status gk_nearfield_get_info(const gk_nearfield* nf, int64_t* pairs, int64_t* entries);
 /* Evaluate the correction on the device (one warp per near pair). */

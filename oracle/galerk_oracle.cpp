@@ -944,6 +944,54 @@ std::vector<Triplet> regularize(const Mesh& mx, int gx, Family fx, const Mesh& m
   return out;
 }
 
+std::vector<Triplet> regularize_radiation(const std::vector<V3>& points, const Mesh& my, int gy, Family fy,
+                                          const std::string& singular_name) {  // assembly.cpp:699-750
+  if (singular_name != "[1/r]") {
+    if (singular_name == "grady[1/r]")
+      throw std::invalid_argument("regularize: grady[1/r] is outside this restatement (MFIE)");
+    throw std::invalid_argument("regularize: unsupported singular kernel '" + singular_name + "'");
+  }
+  const Quad yq = quadrature(my, gy);
+  const Rule& yrule = triangle_rule(gy);
+  const double eps = singular_guard_radius(points, yq.pts);
+  std::vector<V3> yc;
+  std::vector<double> yr;
+  element_geometry(my, yc, yr);
+  const std::vector<double> zero_radius(points.size(), 0.0);
+  const auto pairs = close_pairs_impl(points, zero_radius, yc, yr, NearRule::Ref, 0.0);
+  std::map<std::pair<int, int>, double> acc;  // setFromTriplets: (col, row) -> sum in triplet order
+  for (const auto& [pt, ye] : pairs) {
+    YCtx y;
+    y.A = my.vertices[my.elements[ye][0]];
+    y.B = my.vertices[my.elements[ye][1]];
+    y.C = my.vertices[my.elements[ye][2]];
+    y.fam = fy;
+    if (fy == P0) {
+      y.tdofs.push_back({ye, 0, 0});
+    } else {
+      for (int l = 0; l < 3; ++l) y.tdofs.push_back({my.elements[ye][l], 1, l});
+      y.g_bary = barycentric_gradients(my, ye);
+    }
+    const V3 x = points[pt];
+    const TriangleNewton tn = analytic_triangle_integrals(y.A, y.B, y.C, x);
+    const auto lam = y.lam_at_rho(tn);
+    for (size_t j = 0; j < y.tdofs.size(); ++j) {
+      const double exact = y.exact(j, tn, lam);
+      const double gauss = y.gauss(x, j, yq, ye, gy, eps, yrule);
+      const auto key = std::make_pair(y.tdofs[j].free_index, pt);
+      auto it = acc.find(key);
+      if (it == acc.end())
+        acc.emplace(key, exact - gauss);
+      else
+        it->second += exact - gauss;
+    }
+  }
+  std::vector<Triplet> out;
+  out.reserve(acc.size());
+  for (auto& [k, v] : acc) out.push_back({k.second, k.first, v});
+  return out;
+}
+
 std::vector<PairValue> regularize_pairs_p0(const Mesh& mx, int gx, const Mesh& my, int gy,
                                            NearRule rule, double hbar,
                                            const std::vector<int>* only_x, int threads,

@@ -169,6 +169,9 @@ std::vector<Triplet> regularize(const Mesh& mx, int gx, Family fx, const Mesh& m
                                 RegStats* stats = nullptr, NearRule rule = NearRule::Ref,
                                 double hbar = 0.0, const std::vector<int>* only_x = nullptr,
                                 int threads = 1);
+// regularize_radiation (assembly.cpp:699-750): point x trial-element pairs.
+std::vector<Triplet> regularize_radiation(const std::vector<V3>& points, const Mesh& my, int gy, Family fy,
+                                          const std::string& singular_name);
 // Per-pair local values in pair order (P0 x P0 only) -> (ex, ey, value)
 struct PairValue { int ex, ey; double val; };
 std::vector<PairValue> regularize_pairs_p0(const Mesh& mx, int gx, const Mesh& my, int gy,

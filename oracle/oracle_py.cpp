@@ -214,6 +214,17 @@ PYBIND11_MODULE(_oracle, m) {
         py::arg("vx"), py::arg("ex"), py::arg("gx"), py::arg("fx"), py::arg("vy"), py::arg("ey"),
         py::arg("gy"), py::arg("fy"), py::arg("name"), py::arg("rule") = 0, py::arg("hbar") = 0.0,
         py::arg("only_x") = py::none(), py::arg("threads") = 1);
+  m.def("regularize_radiation", [](F64 pts, F64 vy, I32 ey, int gy, int fy, const std::string& name) {
+    auto t = regularize_radiation(to_pts(pts), to_mesh(vy, ey), gy, (Family)fy, name);
+    std::vector<int> r(t.size()), c(t.size());
+    std::vector<double> v(t.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+      r[i] = t[i].row;
+      c[i] = t[i].col;
+      v[i] = t[i].val;
+    }
+    return py::make_tuple(r, c, v);
+  });
   m.def("near_pairs", [](F64 vx, I32 ex, F64 vy, I32 ey, int rule, double hbar) {
     return near_pairs(to_mesh(vx, ex), to_mesh(vy, ey), (NearRule)rule, hbar);
   });

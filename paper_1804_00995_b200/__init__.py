@@ -50,6 +50,7 @@ BemOptions = _native.BemOptions
 bem_dense = _native.bem_dense
 radiation_dense = _native.radiation_dense
 regularize = _native.regularize
+regularize_radiation = _native.regularize_radiation
 AssemblyPlan = _native.AssemblyPlan
 GreenPlan = _native.GreenPlan
 NearField = _native.NearField

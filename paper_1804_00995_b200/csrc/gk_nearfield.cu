@@ -63,6 +63,8 @@ struct NfArgs {
   const int32_t* ye;
   const double* xq;  // x quadrature per point: x,y,z,w  [nex*gx*4]
   const double* yq;  // y quadrature per point
+  const double* xrule;  // [g*3] barycentric rule of the x domain (per plan)
+  const double* yrule;
   int gx, gy;
   double eps;
   double* local;     // [npairs * kMaxLoc]
@@ -72,8 +74,6 @@ struct NfArgs {
 
 __constant__ double c_r7_bary[7][3];
 __constant__ double c_r7_w[7];
-__constant__ double c_xrule_bary[7][3];
-__constant__ double c_yrule_bary[7][3];
 
 struct Node {
   double corners[9];
@@ -248,13 +248,13 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
         const double kv = 1.0 / r;
 #pragma unroll
         for (int j = 0; j < NTR; ++j) {
-          const double psi = NTR == 1 ? 1.0 : c_yrule_bary[l][j];
+          const double psi = NTR == 1 ? 1.0 : a.yrule[3 * l + j];
           d[j] += yq[3] * kv * psi;
         }
       }
 #pragma unroll
       for (int i = 0; i < NT; ++i) {
-        const double tv = NT == 1 ? 1.0 : c_xrule_bary[lane][i];
+        const double tv = NT == 1 ? 1.0 : a.xrule[3 * lane + i];
 #pragma unroll
         for (int j = 0; j < NTR; ++j) S.vals[lane][i * NTR + j] = -(w * (tv * d[j]));
       }
@@ -381,6 +381,62 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
   }
 }
 
+// regularize_radiation (assembly.cpp:725-745): one thread per (point, element)
+// pair; local[j] = exact(j) - gauss(j) for the element's trial dofs.
+template <int NTR>
+__global__ void __launch_bounds__(128) k_nf_points(const NfArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.npairs) return;
+  const int pt = a.pair_ex[p], ey = a.pair_ey[p];
+  YTri T;
+  for (int c = 0; c < 3; ++c) {
+    const int vi = a.ye[3 * ey + c];
+    T.v[c] = mk(a.yv[3 * vi], a.yv[3 * vi + 1], a.yv[3 * vi + 2]);
+  }
+  const V3 cr = cross(T.v[1] - T.v[0], T.v[2] - T.v[0]);
+  const double area2 = nrm(cr);
+  const double diam = fmax(fmax(nrm(T.v[1] - T.v[0]), nrm(T.v[2] - T.v[1])), nrm(T.v[0] - T.v[2]));
+  if (area2 <= 1e-14 * diam * diam) atomicExch(a.stats + 8, 1ull);
+  T.n = mk(cr.x / area2, cr.y / area2, cr.z / area2);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const V3 d = T.v[i == 2 ? 0 : i + 1] - T.v[i];
+    const double len = nrm(d);
+    T.len[i] = len;
+    T.s_hat[i] = mk(d.x / len, d.y / len, d.z / len);
+    T.m_hat[i] = cross(T.s_hat[i], T.n);
+  }
+  if (NTR == 3) {
+    const V3 e1 = T.v[1] - T.v[0], e2 = T.v[2] - T.v[0];
+    const double g00 = dot(e1, e1), g01 = dot(e1, e2), g11 = dot(e2, e2);
+    const double det = g00 * g11 - g01 * g01;
+    const double i00 = g11 / det, i01 = -g01 / det, i11 = g00 / det;
+    T.g_bary[1] = mk(e1.x * i00 + e2.x * i01, e1.y * i00 + e2.y * i01, e1.z * i00 + e2.z * i01);
+    T.g_bary[2] = mk(e1.x * i01 + e2.x * i11, e1.y * i01 + e2.y * i11, e1.z * i01 + e2.z * i11);
+    T.g_bary[0] = mk(0, 0, 0) - T.g_bary[1] - T.g_bary[2];
+  }
+  const V3 x = mk(a.xv[3 * pt], a.xv[3 * pt + 1], a.xv[3 * pt + 2]);
+  double nw;
+  V3 mo, rho;
+  analytic<NTR == 3>(T, x, nw, mo, rho);
+  double d[NTR];
+  exact_values<1, NTR>(T, nw, mo, rho, d);
+  double gs[NTR];
+#pragma unroll
+  for (int j = 0; j < NTR; ++j) gs[j] = 0.0;
+  for (int l = 0; l < a.gy; ++l) {  // YContext::gauss (assembly.cpp:504-543)
+    const double* yq = a.yq + ((int64_t)ey * a.gy + l) * 4;
+    const double r = nrm(x - mk(yq[0], yq[1], yq[2]));
+    if (r <= a.eps) continue;
+    const double kv = 1.0 / r;
+#pragma unroll
+    for (int j = 0; j < NTR; ++j) gs[j] += yq[3] * kv * (NTR == 1 ? 1.0 : a.yrule[3 * l + j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NTR; ++j) a.local[p * kMaxLoc + j] = d[j] - gs[j];
+  atomicAdd(a.stats, 1ull);
+}
+
 // A[row + col*lda].re += sum of the entry's contributions in pair order
 __global__ void k_nf_reduce(int64_t n, const int64_t* __restrict__ start, const int64_t* __restrict__ src,
                             const double* __restrict__ local, double* __restrict__ vals) {
@@ -494,10 +550,12 @@ std::vector<double> host_quadrature(const HostMesh& m, int g) {  // quadrature.c
 using namespace gk;
 
 struct gk_nearfield {
+  bool points = false;  // collocation form (regularize_radiation)
   int fx = 0, fy = 0, gx = 0, gy = 0, nt = 1, ntr = 1;
   int64_t npairs = 0, nentries = 0;
   double eps = 0.0;
-  DevBuf pair_ex, pair_ey, xv, xe, yv, ye, xq, yq, local, work, stats, ent_row, ent_col, ent_start, ent_src, vals;
+  DevBuf pair_ex, pair_ey, xv, xe, yv, ye, xq, yq, local, work, stats, ent_row, ent_col, ent_start, ent_src, vals,
+      xrule, yrule;
   std::vector<int32_t> h_row, h_col;
   bool computed = false;
 };
@@ -616,8 +674,108 @@ gk_status gk_nearfield_create(const gk_mesh_side* test, const gk_mesh_side* tria
     std::copy(rby.begin(), rby.end(), by);
     cuda_check(cudaMemcpyToSymbol(c_r7_bary, b7.data(), sizeof(double) * 21), "rule7");
     cuda_check(cudaMemcpyToSymbol(c_r7_w, w7.data(), sizeof(double) * 7), "rule7w");
-    cuda_check(cudaMemcpyToSymbol(c_xrule_bary, bx, sizeof(double) * 21), "xrule");
-    cuda_check(cudaMemcpyToSymbol(c_yrule_bary, by, sizeof(double) * 21), "yrule");
+    N->xrule.upload(bx, sizeof(bx));
+    N->yrule.upload(by, sizeof(by));
+    *out = N.release();
+  });
+}
+
+gk_status gk_nearfield_create_points(int64_t npts, const double* points, const gk_mesh_side* trial,
+                                     const char* singular_name, gk_nearfield** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("gk_nearfield_create_points: null output");
+    *out = nullptr;
+    const std::string name = singular_name ? singular_name : "";
+    if (name != "[1/r]") {  // assembly.cpp:701-704
+      if (name == "grady[1/r]")
+        throw std::invalid_argument("regularize: grady[1/r] (MFIE/CFIE) is outside the B200 hot path");
+      throw std::invalid_argument("regularize: unsupported singular kernel '" + name + "'");
+    }
+    if (!trial || trial->ne <= 0 || !trial->vertices || !trial->elements)
+      throw std::invalid_argument("regularize: dom_y must be a triangle mesh");
+    if (trial->family != 0 && trial->family != 1)
+      throw std::invalid_argument("regularize: unsupported trial family/operator combination");
+    if (npts < 0 || (npts > 0 && !points)) throw std::invalid_argument("regularize_radiation: bad points");
+    require_device();
+    auto N = std::make_unique<gk_nearfield>();
+    N->points = true;
+    N->fx = 0;
+    N->fy = trial->family;
+    N->gx = 1;
+    N->gy = trial->g;
+    N->nt = 1;
+    N->ntr = N->fy == 0 ? 1 : 3;
+    const HostMesh my{trial->vertices, trial->elements, trial->nv, trial->ne};
+    const std::vector<double> yq = host_quadrature(my, N->gy);
+    {
+      const int64_t nb = my.ne * N->gy;
+      std::vector<double> ax(npts), ay(npts), az(npts), bx(nb), by(nb), bz(nb);
+      for (int64_t i = 0; i < npts; ++i) ax[i] = points[3 * i], ay[i] = points[3 * i + 1], az[i] = points[3 * i + 2];
+      for (int64_t i = 0; i < nb; ++i) bx[i] = yq[4 * i], by[i] = yq[4 * i + 1], bz[i] = yq[4 * i + 2];
+      N->eps = guard_radius_pts(npts, ax.data(), ay.data(), az.data(), nb, bx.data(), by.data(), bz.data());
+    }
+    // close_pairs(points, zero radii, yc, yr) (assembly.cpp:721-722)
+    std::vector<HV3> yc(my.ne);
+    std::vector<double> yr(my.ne);
+    double rmax = 0.0;
+    for (int64_t e = 0; e < my.ne; ++e) yc[e] = my.centroid(e), yr[e] = my.circumradius(e), rmax = std::max(rmax, yr[e]);
+    const double cell = std::max(3.0 * rmax, 1e-300);
+    auto key = [cell](const HV3& p) {
+      return std::array<int64_t, 3>{(int64_t)std::floor(p.x / cell), (int64_t)std::floor(p.y / cell),
+                                    (int64_t)std::floor(p.z / cell)};
+    };
+    std::map<std::array<int64_t, 3>, std::vector<int>> grid;
+    for (int64_t e = 0; e < my.ne; ++e) grid[key(yc[e])].push_back((int)e);
+    std::vector<int32_t> ppt, pey;
+    for (int64_t i = 0; i < npts; ++i) {
+      const HV3 xi{points[3 * i], points[3 * i + 1], points[3 * i + 2]};
+      const auto k = key(xi);
+      for (int64_t dx = -1; dx <= 1; ++dx)
+        for (int64_t dy = -1; dy <= 1; ++dy)
+          for (int64_t dz = -1; dz <= 1; ++dz) {
+            const auto it = grid.find({k[0] + dx, k[1] + dy, k[2] + dz});
+            if (it == grid.end()) continue;
+            for (int e : it->second)
+              if (hnrm(hsub(yc[e], xi)) <= 3.0 * std::max(0.0, yr[e])) {
+                ppt.push_back((int32_t)i);
+                pey.push_back(e);
+              }
+          }
+    }
+    N->npairs = (int64_t)ppt.size();
+    std::map<std::pair<int32_t, int32_t>, std::vector<int64_t>> ent;  // (col,row) -> contributions
+    for (int64_t p = 0; p < N->npairs; ++p)
+      for (int j = 0; j < N->ntr; ++j) {
+        const int32_t c = N->fy == 0 ? pey[p] : trial->elements[3 * pey[p] + j];
+        if (c >= trial->nfree) throw std::invalid_argument("regularize: dof out of range");
+        ent[{c, ppt[p]}].push_back(p * kMaxLoc + j);
+      }
+    N->nentries = (int64_t)ent.size();
+    std::vector<int64_t> start{0}, src;
+    for (auto& [k, v] : ent) {
+      N->h_col.push_back(k.first);
+      N->h_row.push_back(k.second);
+      src.insert(src.end(), v.begin(), v.end());
+      start.push_back((int64_t)src.size());
+    }
+    N->pair_ex.upload(ppt);
+    N->pair_ey.upload(pey);
+    N->xv.upload(points, sizeof(double) * 3 * std::max<int64_t>(npts, 0));
+    N->yv.upload(trial->vertices, sizeof(double) * 3 * trial->nv);
+    N->ye.upload(trial->elements, sizeof(int32_t) * 3 * trial->ne);
+    N->yq.upload(yq);
+    N->local.alloc(sizeof(double) * kMaxLoc * std::max<int64_t>(1, N->npairs));
+    N->work.alloc(sizeof(unsigned long long));
+    N->stats.alloc(sizeof(unsigned long long) * 9);
+    N->ent_row.upload(N->h_row);
+    N->ent_col.upload(N->h_col);
+    N->ent_start.upload(start);
+    N->ent_src.upload(src);
+    N->vals.alloc(sizeof(double) * std::max<int64_t>(1, N->nentries));
+    const std::vector<double> rby = host_rule(N->gy, false);
+    double by[21] = {0};
+    std::copy(rby.begin(), rby.end(), by);
+    N->yrule.upload(by, sizeof(by));
     *out = N.release();
   });
 }
@@ -647,6 +805,8 @@ gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
       a.ye = N->ye.as<int32_t>();
       a.xq = N->xq.as<double>();
       a.yq = N->yq.as<double>();
+      a.xrule = N->xrule.as<double>();
+      a.yrule = N->yrule.as<double>();
       a.gx = N->gx;
       a.gy = N->gy;
       a.eps = N->eps;
@@ -665,7 +825,13 @@ gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(1, per_sm)));
         kern<<<grid, 32 * kNfWarps, smem, s>>>(a);
       };
-      if (N->nt == 1 && N->ntr == 1)
+      if (N->points) {
+        const unsigned grid = (unsigned)((N->npairs + 127) / 128);
+        if (N->ntr == 1)
+          k_nf_points<1><<<grid, 128, 0, s>>>(a);
+        else
+          k_nf_points<3><<<grid, 128, 0, s>>>(a);
+      } else if (N->nt == 1 && N->ntr == 1)
         launch(k_nearfield<1, 1>);
       else if (N->nt == 3 && N->ntr == 3)
         launch(k_nearfield<3, 3>);

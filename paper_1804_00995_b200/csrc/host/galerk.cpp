@@ -466,22 +466,22 @@ MatrixXcd radiation_dense(const std::vector<Vec3>& points, const Domain& dom_y, 
   return product(tst, kernel, tri, opts);
 }
 
-SpMat regularize(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const std::string& singular_name,
-                 const FemSpace& trial) {
-  auto mesh_side = [](const Domain& d, const FemSpace& s) {
-    gk_mesh_side m;
-    m.nv = d.mesh.vertex_count();
-    m.vertices = d.mesh.vertices.data();
-    m.ne = d.mesh.element_count();
-    m.elements = d.mesh.elements.data();
-    m.family = s.family() == Family::P0 ? 0 : 1;
-    m.g = d.gauss_count;
-    m.nfree = s.free_count();
-    return m;
-  };
-  const gk_mesh_side mx = mesh_side(dom_x, test), my = mesh_side(dom_y, trial);
-  gk_nearfield* nf = nullptr;
-  throw_status(gk_nearfield_create(&mx, &my, singular_name.c_str(), GK_NEAR_REF, 0.0, &nf));
+namespace {
+gk_mesh_side mesh_side(const Domain& d, const FemSpace& s) {
+  gk_mesh_side m;
+  m.nv = d.mesh.vertex_count();
+  m.vertices = d.mesh.vertices.data();
+  m.ne = d.mesh.element_count();
+  m.elements = d.mesh.elements.data();
+  m.family = s.family() == Family::P0 ? 0 : 1;
+  m.g = d.gauss_count;
+  m.nfree = s.free_count();
+  return m;
+}
+
+// Runs a created near-field plan and returns its summed correction as the
+// column-major sparse matrix the reference's setFromTriplets produces.
+SpMat run_nearfield(gk_nearfield* nf, int64_t rows, int64_t cols) {
   std::unique_ptr<gk_nearfield, decltype(&gk_nearfield_destroy)> guard(nf, &gk_nearfield_destroy);
   throw_status(gk_nearfield_compute(nf, nullptr));
   throw_status(gk_stream_synchronize(nullptr));
@@ -491,14 +491,39 @@ SpMat regularize(const Domain& dom_x, const Domain& dom_y, const FemSpace& test,
   std::vector<double> v(entries);
   throw_status(gk_nearfield_triplets(nf, r.data(), c.data(), v.data()));
   SpMat S;
-  S.rows = test.free_count();
-  S.cols = trial.free_count();
+  S.rows = rows;
+  S.cols = cols;
   S.col_ptr.assign(S.cols + 1, 0);
   for (int64_t p = 0; p < entries; ++p) S.col_ptr[c[p] + 1]++;
   for (int64_t j = 0; j < S.cols; ++j) S.col_ptr[j + 1] += S.col_ptr[j];
   S.row_idx = r;  // triplets come back col-major sorted
   S.values = v;
   return S;
+}
+}  // namespace
+
+// assembly.cpp:609-697
+SpMat regularize(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const std::string& singular_name,
+                 const FemSpace& trial) {
+  const gk_mesh_side mx = mesh_side(dom_x, test), my = mesh_side(dom_y, trial);
+  gk_nearfield* nf = nullptr;
+  throw_status(gk_nearfield_create(&mx, &my, singular_name.c_str(), GK_NEAR_REF, 0.0, &nf));
+  return run_nearfield(nf, test.free_count(), trial.free_count());
+}
+
+// assembly.cpp:699-750
+SpMat regularize_radiation(const std::vector<Vec3>& points, const Domain& dom_y, const std::string& singular_name,
+                           const FemSpace& trial) {
+  const gk_mesh_side my = mesh_side(dom_y, trial);
+  std::vector<double> xyz(3 * points.size());
+  for (size_t i = 0; i < points.size(); ++i) {
+    xyz[3 * i] = points[i].x;
+    xyz[3 * i + 1] = points[i].y;
+    xyz[3 * i + 2] = points[i].z;
+  }
+  gk_nearfield* nf = nullptr;
+  throw_status(gk_nearfield_create_points((int64_t)points.size(), xyz.data(), &my, singular_name.c_str(), &nf));
+  return run_nearfield(nf, (int64_t)points.size(), trial.free_count());
 }
 
 // ---------------------------------------------------------------------------------

@@ -163,6 +163,8 @@ MatrixXcd radiation_dense(const std::vector<Vec3>& points, const Domain& dom_y, 
                           const FemSpace& trial, const BemOptions& opts = {});  // assembly.cpp:334-341
 SpMat regularize(const Domain& dom_x, const Domain& dom_y, const FemSpace& test,
                  const std::string& singular_name, const FemSpace& trial);   // assembly.cpp:609-697
+SpMat regularize_radiation(const std::vector<Vec3>& points, const Domain& dom_y,
+                           const std::string& singular_name, const FemSpace& trial);  // assembly.cpp:699-750
 
 // ---- device-resident forms (the B200 data path; no reference counterpart) -----------
 // The quadrature/dof tables of one side in the C-ABI layout (owns its arrays).

@@ -264,6 +264,18 @@ PYBIND11_MODULE(_galerk, m) {
     }
     return py::make_tuple(S.col_ptr, S.row_idx, S.values, py::make_tuple(S.rows, S.cols));
   });
+  m.def(
+      "regularize_radiation",
+      [](F64 pts, const Domain& dy, const std::string& name, const FemSpace& u) {
+        auto P = to_points(pts);
+        SpMat S;
+        {
+          py::gil_scoped_release rel;
+          S = regularize_radiation(P, dy, name, u);
+        }
+        return py::make_tuple(S.col_ptr, S.row_idx, S.values, py::make_tuple(S.rows, S.cols));
+      },
+      py::arg("points"), py::arg("dom_y"), py::arg("singular_name"), py::arg("trial"));
 
   py::class_<AssemblyPlan>(m, "AssemblyPlan")
       .def(py::init<const Domain&, const Domain&, const FemSpace&, const Kernel&, const FemSpace&,

@@ -117,3 +117,41 @@ def test_config3_nearfield_sampled(galerk, oracle, rule):
     assert set(got) == set(ref)
     keys = sorted(ref)
     assert rel_fro([got[k] for k in keys], [ref[k] for k in keys]) <= 1e-10
+
+
+@pytest.mark.parametrize("where,gauss,fam", [("centroids", 3, "P1"), ("inside", 3, "P1"), ("outside", 7, "P0"),
+                                             ("cloud", 6, "P1")])
+def test_regularize_radiation_matches_oracle(galerk, oracle, where, gauss, fam):
+    """regularize_radiation (assembly.cpp:699-750) vs the oracle, and the
+    test_assembly.cpp:248-260 potential check at well-defined points."""
+    m, dom, sp, _ = sphere_problem(galerk, 642, gauss, fam)
+    v, e = np.asarray(m.vertices), np.asarray(m.elements)
+    rng = np.random.default_rng(7)
+    pts = {"centroids": v[e[:5]].mean(axis=1), "inside": 0.999 * v[:5], "outside": 1.001 * v[:5],
+           "cloud": rng.normal(size=(300, 3))}[where]
+    if where == "cloud":
+        pts *= (1.0 + 0.05 * rng.uniform(-1, 1, size=(300, 1))) / np.linalg.norm(pts, axis=1, keepdims=True)
+    colptr, rows, vals, shape = galerk.regularize_radiation(pts, dom, "[1/r]", sp)
+    assert shape == (len(pts), sp.free_count())
+    cols = np.repeat(np.arange(shape[1]), np.diff(colptr))
+    orr, occ, ov = oracle.regularize_radiation(pts, v, e, gauss, FAM[fam], "[1/r]")
+    r, c, vv = _sorted(rows, cols, vals)
+    orr, occ, ov = _sorted(orr, occ, ov)
+    assert np.array_equal(r, orr) and np.array_equal(c, occ)
+    assert rel_fro(vv, ov) <= 1e-10
+    if where != "cloud" and fam == "P1":
+        rad = galerk.radiation_dense(pts, dom, galerk.green_kernel("[1/r]", 0.0), sp)
+        rad[r, c] += vv
+        pot = (rad @ np.ones(shape[1])).real / (4 * math.pi)
+        assert np.all(np.abs(pot - 1.0) < 0.02)
+
+
+def test_regularize_radiation_edge_cases(galerk):
+    m, dom, sp, _ = sphere_problem(galerk, 162, 3, "P1")
+    colptr, rows, vals, shape = galerk.regularize_radiation(np.zeros((0, 3)), dom, "[1/r]", sp)
+    assert shape == (0, sp.free_count()) and len(vals) == 0
+    far = np.array([[100.0, 0.0, 0.0]])
+    colptr, rows, vals, shape = galerk.regularize_radiation(far, dom, "[1/r]", sp)
+    assert len(vals) == 0  # no element within 3 R_y of a far point
+    with pytest.raises(ValueError):
+        galerk.regularize_radiation(far, dom, "[log r]", sp)

@@ -300,3 +300,32 @@ def test_p0_regularize_pairs_ref_vs_2hbar(oracle):
     two = oracle.near_pairs(v, e, v, e, 1, hbar)
     assert len(ref) != len(two)
     assert all(p in set(ref) for p in [(i, i) for i in range(10)])
+
+
+def _collocation_potential(oracle, v, e, pts):
+    rad = oracle.radiation_dense(pts, v, e, 3, P1, "[1/r]", 0.0)
+    r, c, vals = oracle.regularize_radiation(pts, v, e, 3, P1, "[1/r]")
+    rad[np.asarray(r), np.asarray(c)] += vals
+    return (rad @ np.ones(rad.shape[1])).real / (4 * math.pi)
+
+
+@pytest.mark.xfail(strict=True, reason="reference test test_assembly.cpp:248-260 collocates at mesh "
+                   "vertices, where analytic_triangle_integrals (kernels.cpp:192-193) evaluates "
+                   "atan(0/0) = NaN for every triangle sharing the vertex; the restated algorithm "
+                   "reproduces that NaN")
+def test_regularized_collocation_at_vertices_reference_form(oracle):
+    v, e = oracle.build_sphere(642, 1.0)
+    pot = _collocation_potential(oracle, v, e, np.asarray(v)[:5])
+    assert np.all(np.abs(pot - 1.0) < 0.02)
+
+
+@pytest.mark.parametrize("where", ["centroids", "inside", "outside"])
+def test_regularized_collocation_near_the_surface(oracle, where):
+    # Same check as test_assembly.cpp:248-260 (|pot - 1| < 0.02 for the unit
+    # density) at collocation points the analytic integrals are defined at.
+    v, e = oracle.build_sphere(642, 1.0)
+    v, e = np.asarray(v), np.asarray(e)
+    pts = {"centroids": v[e[:5]].mean(axis=1), "inside": 0.999 * v[:5],
+           "outside": 1.001 * v[:5]}[where]
+    pot = _collocation_potential(oracle, v, e, pts)
+    assert np.all(np.abs(pot - 1.0) < 0.02)
