@@ -53,8 +53,11 @@ def build(force=False, verbose=False):
             objs.append(o)
             if force or _newer(o, [s] + hdrs):
                 changed = True
-                _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-ccbin", CXX, "-Xcompiler", "-fPIC",
-                      "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", s, "-o", o], log)
+                # per-source register/spill report of the latest compile (+ the running log)
+                with open(o + ".ptxas", "w") as one:
+                    res = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-ccbin", CXX, "-Xcompiler",
+                                "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", s, "-o", o], log)
+                    one.write(res.stdout + res.stderr)
         for src in CXX_SOURCES:
             s = os.path.join(CSRC, src)
             o = os.path.join(OUT, os.path.basename(src) + ".o")

@@ -32,6 +32,8 @@ namespace gk {
 namespace {
 
 constexpr int kRecUnroll = 4 / kUPT;  // records per group (x kUPT locations = 4 independent evaluations)
+constexpr int kGC = 4;                // gather: columns per work item
+static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
 
 struct AsmSmem {
   double2 H[kJCap * kUCap];
@@ -98,26 +100,26 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   char* Hb[kUPT];
 #pragma unroll
   for (int h = 0; h < kUPT; ++h) Hb[h] = reinterpret_cast<char*>(S.H) + (t + h * kAsmThreads) * 16;
-  int cur = -1;  // byte offset of the run's slot row
+  // run accumulator of the current first slot; cur starts at the first
+  // record's slot so that the fold below needs no "first run" case
+  int cur = nrec > 0 ? S.rec[0].off0 : 0;  // byte offset of the run's slot row
   double ar[kUPT], ai[kUPT];
 #pragma unroll
   for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
-  // fold one record's kUPT evaluated pairs (uniform branches)
   auto flush = [&]() {
 #pragma unroll
     for (int h = 0; h < kUPT; ++h) *reinterpret_cast<double2*>(Hb[h] + cur) = make_double2(ar[h], ai[h]);
   };
+  // fold one record's evaluated pairs: a run change stores the finished run
+  // (predicated) and restarts the accumulator with selects — no branches
   auto fold = [&](const YRec& p, const c64* g) {
-    if (p.off0 != cur) {
-      if (cur >= 0) flush();
-      cur = p.off0;
-#pragma unroll
-      for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
-    }
+    const bool fresh = p.off0 != cur;
+    if (fresh) flush();
+    cur = p.off0;
 #pragma unroll
     for (int h = 0; h < kUPT; ++h) {
-      ar[h] = fma(p.c0, g[h].re, ar[h]);
-      ai[h] = fma(p.c0, g[h].im, ai[h]);
+      ar[h] = fma(p.c0, g[h].re, fresh ? 0.0 : ar[h]);
+      ai[h] = fma(p.c0, g[h].im, fresh ? 0.0 : ai[h]);
     }
     if (S1 && p.off1 >= 0)
 #pragma unroll
@@ -169,36 +171,44 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     green_n<HELM, kUPT, MASK>(dx, dy, dz, eps2, kappa, g);
     fold(p, g);
   }
-  if (cur >= 0) flush();
+  if (nrec > 0) flush();
   __syncthreads();
 
-  // x-side contraction + write (lanes along rows: coalesced columns for the natural order)
+  // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
+  // the row's support entries are read once per item and feed kGC independent
+  // H loads; lanes run along rows (coalesced columns for the natural order).
   double2* A = reinterpret_cast<double2*>(a.A);
   const long long lda = a.lda;
-  const int total = nI * nJ;
-  int ii = t % nI, jj = t / nI;
-  const int di = kAsmThreads % nI, dj = kAsmThreads / nI;
-  for (int e = t; e < total; e += kAsmThreads) {
-    const int pi = i0 + ii, pj = j0 + jj;
-    if (!(a.symmetric && pi > pj)) {
-      double re = 0.0, im = 0.0;
-      const double2* Hr = S.H + jj * kUCap;
-      for (int s = S.xs_start[ii]; s < S.xs_start[ii + 1]; ++s) {
-        const double2 h = Hr[S.xs_u[s]];
-        const double c = S.xs_c[s];
-        re = fma(c, h.x, re);
-        im = fma(c, h.y, im);
+  const int items = nI * ((nJ + kGC - 1) / kGC);
+  for (int e = t; e < items; e += kAsmThreads) {
+    const int ii = e % nI, jb = (e / nI) * kGC;
+    const int pi = i0 + ii;
+    if (a.symmetric && pi > j0 + min(jb + kGC, nJ) - 1) continue;  // whole group below the diagonal
+    double re[kGC], im[kGC];
+#pragma unroll
+    for (int q = 0; q < kGC; ++q) re[q] = im[q] = 0.0;
+    const double2* Hr = S.H + jb * kUCap;  // rows past nJ hold stale values that are never stored
+    const int s1 = S.xs_start[ii + 1];
+    for (int s = S.xs_start[ii]; s < s1; ++s) {
+      const double c = S.xs_c[s];
+      const int u = S.xs_u[s];
+#pragma unroll
+      for (int q = 0; q < kGC; ++q) {
+        const double2 h = Hr[q * kUCap + u];
+        re[q] = fma(c, h.x, re[q]);
+        im[q] = fma(c, h.y, im[q]);
       }
-      const long long oi = S.orow[ii], oj = S.ocol[jj];
-      const double2 v = make_double2(re, im);
-      A[oi + oj * lda] = v;
-      if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
     }
-    ii += di;
-    jj += dj;
-    if (ii >= nI) {
-      ii -= nI;
-      ++jj;
+    const long long oi = S.orow[ii];
+#pragma unroll
+    for (int q = 0; q < kGC; ++q) {
+      const int jj = jb + q, pj = j0 + jj;
+      if (jj < nJ && !(a.symmetric && pi > pj)) {
+        const long long oj = S.ocol[jj];
+        const double2 v = make_double2(re[q], im[q]);
+        A[oi + oj * lda] = v;
+        if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
+      }
     }
   }
 }
