@@ -67,7 +67,8 @@ struct gk_plan {
   double eps = 0.0, k = 0.0;
   int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0, nmtiles = 0;
   double x_halo = 0.0, y_halo = 0.0;
-  bool natural = false, second_slot = true;
+  bool natural = false;
+  int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0)
   DevBuf tile_i, tile_j, mtile_i, mtile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u,
       xsup_c, yb_dof_start, yb_rec_start, yrec, yb_zero, xperm, yperm;
   uint64_t device_bytes() const {
@@ -160,7 +161,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->natural = X.natural;
   P->ntiles = (int64_t)T.tile_i.size();
   P->nmtiles = (int64_t)T.mtile_i.size();
-  P->second_slot = T.has_second_slot;
+  P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
   P->tile_i.upload(T.tile_i);
   P->tile_j.upload(T.tile_j);
@@ -212,10 +213,10 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
-  launch_assemble(a, P->ntiles, P->helmholtz, /*mask=*/false, P->second_slot, stream);
+  launch_assemble(a, P->ntiles, P->helmholtz, /*mask=*/false, P->slots, stream);
   a.tile_i = P->mtile_i.as<int32_t>();
   a.tile_j = P->mtile_j.as<int32_t>();
-  launch_assemble(a, P->nmtiles, P->helmholtz, /*mask=*/true, P->second_slot, stream);
+  launch_assemble(a, P->nmtiles, P->helmholtz, /*mask=*/true, P->slots, stream);
 }
 
 }  // namespace

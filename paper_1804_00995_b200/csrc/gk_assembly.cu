@@ -5,23 +5,24 @@
 // y-side product kr = G (W_y Psi) (assembly.cpp:217) and the x-side update
 // A += (W_x Phi)^T kr (assembly.cpp:218).
 //
-// Tile = (x block I, y block J).  Thread t owns x locations t and t+128 of
-// the block (twins merged, <= 256 per block).  The block's y records (unique
-// y locations with their <= 2 (slot, coef) pairs, sorted by first slot) and
-// the x support lists are staged in shared memory.  All threads walk the same
-// record list (broadcast reads) and evaluate G(u, v) once per unique location
-// pair — two x locations per record, so record loads and the uniform run /
-// slot branches are shared by two pair evaluations and every thread carries
-// 2 x kRecUnroll independent FP64 chains.  c0*G goes to a register run
-// accumulator for the record's first slot (flushed when the slot changes),
-// c1*G is added into H[slot][u] in shared memory: the y-side contraction,
-// owner-computes per column, no atomics.  After a barrier each thread gathers
-// whole entries A_ij = sum_u c_ui H[j][u] (x-side contraction, fixed order)
-// and writes them; with identical sides only tiles on or above the diagonal
-// are computed and mirrored (G is symmetric).
+// Tile = (x block I, y block J), one CTA.  Thread t owns x location t of the
+// block (twins merged, <= 256 per block).  The block's y records (unique y
+// locations with their <= 2 (slot, coef) pairs, in descending first-slot
+// order) and the x support lists are staged in shared memory.  All threads
+// walk the same record list (broadcast reads), kRecUnroll records at a time so
+// that every thread carries kRecUnroll independent FP64 chains, and evaluate
+// G(u, v) once per unique location pair.  c0*G goes to a register run
+// accumulator for the record's first slot (stored to H[slot][u] when the slot
+// changes), c1*G is added into H[slot][u] in shared memory: the y-side
+// contraction, owner-computes per column, no atomics.  After a barrier the
+// threads gather whole entries A_ij = sum_u c_ui H[j][u] (x-side contraction,
+// fixed order) and write them; with identical sides only tiles on or above
+// the diagonal are computed and mirrored (G is symmetric).
 //
 // Specialisations: MASK (tile may hold a coincident pair -> r^2 <= eps^2
-// mask), S1 (some record has a second slot; P0 with twin-free rules has none).
+// mask); SLOTS = 0 (no record has a second slot: P0 with twin-free rules),
+// 1 (second slots), 2 (second slots whose coefficient equals the first one in
+// every record — the P1 edge-midpoint rule — so c*rinv is formed once).
 #include <cuda_runtime.h>
 
 #include "gk_internal.hpp"
@@ -31,8 +32,8 @@ namespace gk {
 
 namespace {
 
-constexpr int kRecUnroll = 4 / kUPT;  // records per group (x kUPT locations = 4 independent evaluations)
-constexpr int kGC = 4;                // gather: columns per work item
+constexpr int kRecUnroll = 4;  // records per group = independent evaluations per thread
+constexpr int kGC = 4;         // gather: columns per work item
 static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
 
 struct AsmSmem {
@@ -45,15 +46,22 @@ struct AsmSmem {
   int32_t ocol[kJCap];  // original column index of each tile column
 };
 
-__device__ __forceinline__ void rmw(char* Hb, int off, double c, double gr, double gi) {
-  double2* h = reinterpret_cast<double2*>(Hb + off);
-  double2 v = *h;
-  v.x = fma(c, gr, v.x);
-  v.y = fma(c, gi, v.y);
-  *h = v;
+__device__ __forceinline__ YRec load_rec(const YRec* p) {
+  const double2* src = reinterpret_cast<const double2*>(p);
+  const double2 a0 = src[0], a1 = src[1], a2 = src[2];
+  YRec r;
+  r.x = a0.x;
+  r.y = a0.y;
+  r.z = a1.x;
+  r.c0 = a1.y;
+  r.c1 = a2.x;
+  const long long s = __double_as_longlong(a2.y);
+  r.off0 = (int32_t)(s & 0xffffffffll);
+  r.off1 = (int32_t)(s >> 32);
+  return r;
 }
 
-template <bool HELM, bool MASK, bool S1>
+template <bool HELM, bool MASK, int SLOTS>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
@@ -85,91 +93,72 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   for (int e = t; e <= nI; e += kAsmThreads) S.xs_start[e] = __ldg(a.xsup_start + i0 + e) - xs0;
   for (int e = t; e < nI; e += kAsmThreads) S.orow[e] = __ldg(a.xperm + i0 + e);
   for (int e = t; e < nJ; e += kAsmThreads) S.ocol[e] = __ldg(a.yperm + j0 + e);
-  // my two x locations; idle columns are far away (finite, never gathered)
-  double ux[kUPT], uy[kUPT], uz[kUPT];
-#pragma unroll
-  for (int h = 0; h < kUPT; ++h) {
-    const int c = t + h * kAsmThreads;
-    ux[h] = c < nu ? __ldg(a.xl_x + l0 + c) : 1e100;
-    uy[h] = c < nu ? __ldg(a.xl_y + l0 + c) : 0.0;
-    uz[h] = c < nu ? __ldg(a.xl_z + l0 + c) : 0.0;
-  }
+  // my x location; idle columns are far away (finite, never gathered)
+  const double ux = t < nu ? __ldg(a.xl_x + l0 + t) : 1e100;
+  const double uy = t < nu ? __ldg(a.xl_y + l0 + t) : 0.0;
+  const double uz = t < nu ? __ldg(a.xl_z + l0 + t) : 0.0;
   __syncthreads();
 
   const double eps2 = a.eps2, kappa = a.kappa;
-  char* Hb[kUPT];
-#pragma unroll
-  for (int h = 0; h < kUPT; ++h) Hb[h] = reinterpret_cast<char*>(S.H) + (t + h * kAsmThreads) * 16;
+  char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
   // run accumulator of the current first slot; cur starts at the first
   // record's slot so that the fold below needs no "first run" case
   int cur = nrec > 0 ? S.rec[0].off0 : 0;  // byte offset of the run's slot row
-  double ar[kUPT], ai[kUPT];
-#pragma unroll
-  for (int h = 0; h < kUPT; ++h) ar[h] = ai[h] = 0.0;
-  auto flush = [&]() {
-#pragma unroll
-    for (int h = 0; h < kUPT; ++h) *reinterpret_cast<double2*>(Hb[h] + cur) = make_double2(ar[h], ai[h]);
-  };
-  // fold one record's evaluated pairs: a run change stores the finished run
-  // (predicated) and restarts the accumulator with selects — no branches
-  auto fold = [&](const YRec& p, const c64* g) {
+  double ar = 0.0, ai = 0.0;
+  auto flush = [&]() { *reinterpret_cast<double2*>(Hb + cur) = make_double2(ar, ai); };
+  // fold one record's evaluated pair G = (cs + i sn) rinv: a run change stores
+  // the finished run (predicated) and restarts the accumulator with selects —
+  // no branches.  The basis coefficient is folded into rinv (one DMUL).
+  auto fold = [&](const YRec& p, double cs, double sn, double rinv) {
     const bool fresh = p.off0 != cur;
     if (fresh) flush();
     cur = p.off0;
-#pragma unroll
-    for (int h = 0; h < kUPT; ++h) {
-      ar[h] = fma(p.c0, g[h].re, fresh ? 0.0 : ar[h]);
-      ai[h] = fma(p.c0, g[h].im, fresh ? 0.0 : ai[h]);
+    const double w0 = p.c0 * rinv;
+    if (HELM) {
+      ar = fma(cs, w0, fresh ? 0.0 : ar);
+      ai = fma(sn, w0, fresh ? 0.0 : ai);
+    } else {
+      ar = fresh ? w0 : ar + w0;
+      ai = 0.0;
     }
-    if (S1 && p.off1 >= 0)
-#pragma unroll
-      for (int h = 0; h < kUPT; ++h) rmw(Hb[h], p.off1, p.c1, g[h].re, g[h].im);
+    if (SLOTS > 0 && p.off1 >= 0) {
+      const double w1 = SLOTS == 2 ? w0 : p.c1 * rinv;
+      double2* h = reinterpret_cast<double2*>(Hb + p.off1);
+      double2 v = *h;
+      if (HELM) {
+        v.x = fma(cs, w1, v.x);
+        v.y = fma(sn, w1, v.y);
+      } else {
+        v.x += w1;
+      }
+      *h = v;
+    }
   };
-  constexpr int N = kRecUnroll * kUPT;
   int r = 0;
   for (; r + kRecUnroll <= nrec; r += kRecUnroll) {
     // the whole group's records into registers first (3 LDS.128 each): the H
     // stores in fold() would otherwise force re-loads of every field
     YRec rr[kRecUnroll];
 #pragma unroll
+    for (int k = 0; k < kRecUnroll; ++k) rr[k] = load_rec(&S.rec[r + k]);
+    double dx[kRecUnroll], dy[kRecUnroll], dz[kRecUnroll];
+#pragma unroll
     for (int k = 0; k < kRecUnroll; ++k) {
-      const double2* src = reinterpret_cast<const double2*>(&S.rec[r + k]);
-      const double2 a0 = src[0], a1 = src[1], a2 = src[2];
-      rr[k].x = a0.x;
-      rr[k].y = a0.y;
-      rr[k].z = a1.x;
-      rr[k].c0 = a1.y;
-      rr[k].c1 = a2.x;
-      const long long s = __double_as_longlong(a2.y);
-      rr[k].off0 = (int32_t)(s & 0xffffffffll);
-      rr[k].off1 = (int32_t)(s >> 32);
+      dx[k] = ux - rr[k].x;
+      dy[k] = uy - rr[k].y;
+      dz[k] = uz - rr[k].z;
     }
-    double dx[N], dy[N], dz[N];
+    double cs[kRecUnroll], sn[kRecUnroll], rinv[kRecUnroll];
+    green_parts_n<HELM, kRecUnroll, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
 #pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k)
-#pragma unroll
-      for (int h = 0; h < kUPT; ++h) {
-        dx[k * kUPT + h] = ux[h] - rr[k].x;
-        dy[k * kUPT + h] = uy[h] - rr[k].y;
-        dz[k * kUPT + h] = uz[h] - rr[k].z;
-      }
-    c64 g[N];
-    green_n<HELM, N, MASK>(dx, dy, dz, eps2, kappa, g);
-#pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], g + k * kUPT);
+    for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], cs[k], sn[k], rinv[k]);
   }
   for (; r < nrec; ++r) {
-    const YRec& p = S.rec[r];
-    double dx[kUPT], dy[kUPT], dz[kUPT];
-#pragma unroll
-    for (int h = 0; h < kUPT; ++h) {
-      dx[h] = ux[h] - p.x;
-      dy[h] = uy[h] - p.y;
-      dz[h] = uz[h] - p.z;
-    }
-    c64 g[kUPT];
-    green_n<HELM, kUPT, MASK>(dx, dy, dz, eps2, kappa, g);
-    fold(p, g);
+    const YRec p = load_rec(&S.rec[r]);
+    double dx[1] = {ux - p.x}, dy[1] = {uy - p.y}, dz[1] = {uz - p.z};
+    double cs[1], sn[1], rinv[1];
+    green_parts_n<HELM, 1, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+    fold(p, cs[0], sn[0], rinv[0]);
   }
   if (nrec > 0) flush();
   __syncthreads();
@@ -213,37 +202,39 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   }
 }
 
-template <bool HELM, bool MASK, bool S1>
+template <bool HELM, bool MASK, int SLOTS>
 void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
   const size_t smem = sizeof(AsmSmem);
   static bool configured = false;  // one flag per instantiation
   if (!configured) {
-    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, MASK, S1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, MASK, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
-  k_assemble<HELM, MASK, S1><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+  k_assemble<HELM, MASK, SLOTS><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+}
+
+template <bool HELM, bool MASK>
+void launch_slots(const AsmArgs& a, int64_t ntiles, int slots, cudaStream_t s) {
+  if (slots == 0)
+    launch_one<HELM, MASK, 0>(a, ntiles, s);
+  else if (slots == 1)
+    launch_one<HELM, MASK, 1>(a, ntiles, s);
+  else
+    launch_one<HELM, MASK, 2>(a, ntiles, s);
 }
 
 }  // namespace
 
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, bool second_slot,
-                     void* stream) {
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, int slots, void* stream) {
   if (ntiles <= 0) return;
   if (ntiles > INT32_MAX) throw std::invalid_argument("bem_dense: too many tiles");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int sel = (helmholtz ? 4 : 0) | (mask ? 2 : 0) | (second_slot ? 1 : 0);
-  switch (sel) {
-    case 0: launch_one<false, false, false>(a, ntiles, s); break;
-    case 1: launch_one<false, false, true>(a, ntiles, s); break;
-    case 2: launch_one<false, true, false>(a, ntiles, s); break;
-    case 3: launch_one<false, true, true>(a, ntiles, s); break;
-    case 4: launch_one<true, false, false>(a, ntiles, s); break;
-    case 5: launch_one<true, false, true>(a, ntiles, s); break;
-    case 6: launch_one<true, true, false>(a, ntiles, s); break;
-    default: launch_one<true, true, true>(a, ntiles, s); break;
-  }
+  if (helmholtz)
+    mask ? launch_slots<true, true>(a, ntiles, slots, s) : launch_slots<true, false>(a, ntiles, slots, s);
+  else
+    mask ? launch_slots<false, true>(a, ntiles, slots, s) : launch_slots<false, false>(a, ntiles, slots, s);
   cuda_check(cudaGetLastError(), "k_assemble launch");
 }
 

@@ -107,13 +107,12 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // needs ~16 warps/SM at 2-3 independent chains per warp).  Two 256-thread CTAs
 // per SM: shared memory per CTA = H (kJCap x kUCap x 16 B = 96 KB) + staged
 // records and x supports (~15 KB).
-constexpr int kUCap = 256;   // x locations per tile (kUPT per thread)
-constexpr int kUPT = 1;      // x locations per thread (2 measured slower: 8 warps/SM)
+constexpr int kUCap = 256;   // x locations per tile, one per thread (two per thread measured slower: 8 warps/SM)
 constexpr int kJCap = 24;    // y dofs per tile (H accumulator rows)
 constexpr int kIMax = 256;   // x dofs per tile
 constexpr int kRCap = 128;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 640;  // x support entries per tile (staged in shared memory)
-constexpr int kAsmThreads = kUCap / kUPT;
+constexpr int kAsmThreads = kUCap;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
@@ -147,6 +146,7 @@ struct TileTables {
   std::vector<int32_t> tile_i, tile_j;          // unmasked tiles
   std::vector<int32_t> mtile_i, mtile_j;        // masked tiles
   bool has_second_slot = false;                 // any record with off1 >= 0
+  bool equal_coefs = true;                      // every such record has c1 == c0 (bitwise)
   int64_t pairs_evaluated = 0;
   double x_halo = 0.0, y_halo = 0.0;
 };
@@ -195,8 +195,8 @@ struct AsmArgs {
   double kappa;  // 2k/pi
   int32_t symmetric;
 };
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, bool second_slot,
-                     void* stream);
+// slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, int slots, void* stream);
 
 // ---- matvec ---------------------------------------------------------------------------
 void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,

@@ -448,6 +448,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
     uint32_t has_run = 0;
     for (const YRec& r : recs) {
       T.has_second_slot |= r.off1 >= 0;
+      if (r.off1 >= 0 && __builtin_memcmp(&r.c0, &r.c1, sizeof(double)) != 0) T.equal_coefs = false;
       has_run |= 1u << (r.off0 / (kUCap * 16));
     }
     const uint32_t all = (q1 - q0) >= 32 ? 0xffffffffu : ((1u << (q1 - q0)) - 1u);
