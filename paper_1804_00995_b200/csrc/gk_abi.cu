@@ -69,13 +69,10 @@ struct gk_plan {
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false;
   int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0)
-  DevBuf tile_i, tile_j, mtile_i, mtile_j, xb_dof_start, xb_loc_start, xl_x, xl_y, xl_z, xsup_start, xsup_u,
-      xsup_c, yb_dof_start, yb_rec_start, yrec, yb_zero, xperm, yperm;
+  DevBuf tiles, mtiles;  // TileDesc per unmasked / masked tile
+  DevBuf xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c, yrec, xperm, yperm;
   uint64_t device_bytes() const {
-    const DevBuf* b[] = {&tile_i, &tile_j, &mtile_i, &mtile_j, &xb_dof_start, &xb_loc_start, &xl_x, &xl_y,
-                         &xl_z, &xsup_start, &xsup_u, &xsup_c, &yb_dof_start, &yb_rec_start, &yrec, &yb_zero,
-                         &xperm,
-                         &yperm};
+    const DevBuf* b[] = {&tiles, &mtiles, &xl_x, &xl_y, &xl_z, &xsup_start, &xsup_u, &xsup_c, &yrec, &xperm, &yperm};
     uint64_t s = 0;
     for (auto* p : b) s += p->bytes;
     return s;
@@ -110,6 +107,30 @@ void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) 
     throw std::runtime_error("bem_dense: estimated memory " + std::to_string(need / 1000000) +
                              " MB exceeds the cap of " + std::to_string(o.memory_cap_bytes / 1000000) +
                              " MB; use the tol (H-matrix) variant");
+}
+
+// One self-contained descriptor per tile: the kernel's staging loads then
+// depend on a single descriptor load instead of a chain of table lookups.
+std::vector<TileDesc> make_tile_descs(const TileTables& T, const std::vector<int32_t>& ti,
+                                      const std::vector<int32_t>& tj) {
+  std::vector<TileDesc> d(ti.size());
+  for (size_t k = 0; k < ti.size(); ++k) {
+    const int32_t bi = ti[k], bj = tj[k];
+    TileDesc& D = d[k];
+    D.i0 = T.xb_dof_start[bi];
+    D.nI = T.xb_dof_start[bi + 1] - D.i0;
+    D.j0 = T.yb_dof_start[bj];
+    D.nJ = T.yb_dof_start[bj + 1] - D.j0;
+    D.l0 = T.xb_loc_start[bi];
+    D.nu = T.xb_loc_start[bi + 1] - D.l0;
+    D.r0 = T.yb_rec_start[bj];
+    D.nrec = T.yb_rec_start[bj + 1] - D.r0;
+    D.xs0 = T.xsup_start[D.i0];
+    D.nxs = T.xsup_start[D.i0 + D.nI] - D.xs0;
+    D.zero_rows = T.yb_zero[bj];
+    D.pad = 0;
+  }
+  return d;
 }
 
 std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
@@ -163,22 +184,15 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->nmtiles = (int64_t)T.mtile_i.size();
   P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
-  P->tile_i.upload(T.tile_i);
-  P->tile_j.upload(T.tile_j);
-  P->mtile_i.upload(T.mtile_i);
-  P->mtile_j.upload(T.mtile_j);
-  P->xb_dof_start.upload(T.xb_dof_start);
-  P->xb_loc_start.upload(T.xb_loc_start);
+  P->tiles.upload(make_tile_descs(T, T.tile_i, T.tile_j));
+  P->mtiles.upload(make_tile_descs(T, T.mtile_i, T.mtile_j));
   P->xl_x.upload(T.xl_x);
   P->xl_y.upload(T.xl_y);
   P->xl_z.upload(T.xl_z);
   P->xsup_start.upload(T.xsup_start);
   P->xsup_u.upload(T.xsup_u);
   P->xsup_c.upload(T.xsup_c);
-  P->yb_dof_start.upload(T.yb_dof_start);
-  P->yb_rec_start.upload(T.yb_rec_start);
   P->yrec.upload(T.yrec);
-  P->yb_zero.upload(T.yb_zero);
   P->xperm.upload(X.perm);
   P->yperm.upload(Yr.perm);
   lap("upload");
@@ -191,20 +205,14 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   if (!A) throw std::invalid_argument("gk_plan_assemble: null matrix");
   if (lda < P->rows) throw std::invalid_argument("gk_plan_assemble: lda < rows");
   AsmArgs a;
-  a.tile_i = P->tile_i.as<int32_t>();
-  a.tile_j = P->tile_j.as<int32_t>();
-  a.xb_dof_start = P->xb_dof_start.as<int32_t>();
-  a.xb_loc_start = P->xb_loc_start.as<int32_t>();
+  a.tiles = P->tiles.as<TileDesc>();
   a.xl_x = P->xl_x.as<double>();
   a.xl_y = P->xl_y.as<double>();
   a.xl_z = P->xl_z.as<double>();
   a.xsup_start = P->xsup_start.as<int32_t>();
   a.xsup_u = P->xsup_u.as<int32_t>();
   a.xsup_c = P->xsup_c.as<double>();
-  a.yb_dof_start = P->yb_dof_start.as<int32_t>();
-  a.yb_rec_start = P->yb_rec_start.as<int32_t>();
   a.yrec = P->yrec.as<YRec>();
-  a.yb_zero = P->yb_zero.as<uint32_t>();
   a.xperm = P->xperm.as<int32_t>();
   a.yperm = P->yperm.as<int32_t>();
   a.A = A;
@@ -214,8 +222,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.symmetric = P->symmetric ? 1 : 0;
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
   launch_assemble(a, P->ntiles, P->helmholtz, /*mask=*/false, P->slots, stream);
-  a.tile_i = P->mtile_i.as<int32_t>();
-  a.tile_j = P->mtile_j.as<int32_t>();
+  a.tiles = P->mtiles.as<TileDesc>();
   launch_assemble(a, P->nmtiles, P->helmholtz, /*mask=*/true, P->slots, stream);
 }
 

@@ -65,19 +65,17 @@ template <bool HELM, bool MASK, int SLOTS>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
-  const int tile = blockIdx.x;
-  const int bi = a.tile_i[tile], bj = a.tile_j[tile];
   const int t = threadIdx.x;
-  const int i0 = a.xb_dof_start[bi], nI = a.xb_dof_start[bi + 1] - i0;
-  const int j0 = a.yb_dof_start[bj], nJ = a.yb_dof_start[bj + 1] - j0;
-  const int l0 = a.xb_loc_start[bi], nu = a.xb_loc_start[bi + 1] - l0;
-  const int r0 = a.yb_rec_start[bj], nrec = a.yb_rec_start[bj + 1] - r0;
-  const int xs0 = a.xsup_start[i0], nxs = a.xsup_start[i0 + nI] - xs0;
+  const int4* dp = reinterpret_cast<const int4*>(a.tiles + blockIdx.x);
+  const int4 d0 = __ldg(dp), d1 = __ldg(dp + 1), d2 = __ldg(dp + 2);
+  const int i0 = d0.x, nI = d0.y, j0 = d0.z, nJ = d0.w;
+  const int l0 = d1.x, nu = d1.y, r0 = d1.z, nrec = d1.w;
+  const int xs0 = d2.x, nxs = d2.y;
+  const uint32_t zero_rows = (uint32_t)d2.z;
 
   // stage: records and x support lists.  Records run in descending first-slot
   // order, so each H row is first written by its own run flush (a plain store);
   // only rows without a run (host bitmask) are zero-filled.
-  const uint32_t zero_rows = a.yb_zero[bj];
   if (zero_rows)
     for (int e = t; e < nJ * kUCap; e += kAsmThreads)
       if ((zero_rows >> (e / kUCap)) & 1u) S.H[e] = make_double2(0.0, 0.0);

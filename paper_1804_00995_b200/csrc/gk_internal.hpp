@@ -172,21 +172,26 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
 // overrides.  Y may be null (symmetric: Y = X).
 TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps);
 
+struct TileDesc {  // everything a k_assemble CTA needs to stage its tile
+  int32_t i0, nI;      // x block: first permuted row, rows
+  int32_t j0, nJ;      // y block: first permuted column, columns
+  int32_t l0, nu;      // x locations
+  int32_t r0, nrec;    // y records
+  int32_t xs0, nxs;    // x support entries
+  uint32_t zero_rows;  // H rows without a run (zero-filled)
+  int32_t pad;
+};
+static_assert(sizeof(TileDesc) == 48, "TileDesc is loaded as three 16-byte vectors");
+
 struct AsmArgs {
-  const int32_t* tile_i;
-  const int32_t* tile_j;
-  const int32_t* xb_dof_start;
-  const int32_t* xb_loc_start;
+  const TileDesc* tiles;
   const double* xl_x;
   const double* xl_y;
   const double* xl_z;
   const int32_t* xsup_start;
   const int32_t* xsup_u;
   const double* xsup_c;
-  const int32_t* yb_dof_start;
-  const int32_t* yb_rec_start;
   const YRec* yrec;
-  const uint32_t* yb_zero;
   const int32_t* xperm;
   const int32_t* yperm;
   void* A;
