@@ -61,6 +61,24 @@ __device__ __forceinline__ YRec load_rec(const YRec* p) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <bool HELM, bool MASK, int SLOTS>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -73,28 +91,34 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int xs0 = d2.x, nxs = d2.y;
   const uint32_t zero_rows = (uint32_t)d2.z;
 
-  // stage: records and x support lists.  Records run in descending first-slot
-  // order, so each H row is first written by its own run flush (a plain store);
-  // only rows without a run (host bitmask) are zero-filled.
+  // stage with cp.async (no register staging): group 0 = the records the pair
+  // loop needs now; group 1 = the x support lists and dof maps the gather
+  // needs only after the pair loop, so their latency hides behind it.
+  // Records run in descending first-slot order, so each H row is first
+  // written by its own run flush (a plain store); only rows without a run
+  // (host bitmask) are zero-filled.
   if (zero_rows)
     for (int e = t; e < nJ * kUCap; e += kAsmThreads)
       if ((zero_rows >> (e / kUCap)) & 1u) S.H[e] = make_double2(0.0, 0.0);
   {
     const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
     double2* dst = reinterpret_cast<double2*>(S.rec);
-    for (int e = t; e < nrec * 3; e += kAsmThreads) dst[e] = __ldg(src + e);
+    for (int e = t; e < nrec * 3; e += kAsmThreads) cp_async16(dst + e, src + e);
   }
+  cp_async_commit();
   for (int e = t; e < nxs; e += kAsmThreads) {
-    S.xs_c[e] = __ldg(a.xsup_c + xs0 + e);
-    S.xs_u[e] = __ldg(a.xsup_u + xs0 + e);
+    cp_async8(S.xs_c + e, a.xsup_c + xs0 + e);
+    cp_async4(S.xs_u + e, a.xsup_u + xs0 + e);
   }
-  for (int e = t; e <= nI; e += kAsmThreads) S.xs_start[e] = __ldg(a.xsup_start + i0 + e) - xs0;
-  for (int e = t; e < nI; e += kAsmThreads) S.orow[e] = __ldg(a.xperm + i0 + e);
-  for (int e = t; e < nJ; e += kAsmThreads) S.ocol[e] = __ldg(a.yperm + j0 + e);
+  for (int e = t; e <= nI; e += kAsmThreads) cp_async4(S.xs_start + e, a.xsup_start + i0 + e);  // global offsets
+  for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
+  for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
+  cp_async_commit();
   // my x location; idle columns are far away (finite, never gathered)
   const double ux = t < nu ? __ldg(a.xl_x + l0 + t) : 1e100;
   const double uy = t < nu ? __ldg(a.xl_y + l0 + t) : 0.0;
   const double uz = t < nu ? __ldg(a.xl_z + l0 + t) : 0.0;
+  cp_async_wait<1>();
   __syncthreads();
 
   const double eps2 = a.eps2, kappa = a.kappa;
@@ -159,6 +183,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
     fold(p, cs[0], sn[0], rinv[0]);
   }
   if (nrec > 0) flush();
+  cp_async_wait<0>();
   __syncthreads();
 
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
@@ -175,8 +200,8 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
 #pragma unroll
     for (int q = 0; q < kGC; ++q) re[q] = im[q] = 0.0;
     const double2* Hr = S.H + jb * kUCap;  // rows past nJ hold stale values that are never stored
-    const int s1 = S.xs_start[ii + 1];
-    for (int s = S.xs_start[ii]; s < s1; ++s) {
+    const int s1 = S.xs_start[ii + 1] - xs0;
+    for (int s = S.xs_start[ii] - xs0; s < s1; ++s) {
       const double c = S.xs_c[s];
       const int u = S.xs_u[s];
 #pragma unroll
