@@ -20,6 +20,9 @@
  *       matrix-free Green-kernel matvec with the evaluate_blocks semantics
  *       (distance mask, kernels.cpp:104-111) contracted with a weighted charge
  *       vector (make_point_side + bem_product, assembly.cpp:173-222).
+ *   gk_evaluator_*
+ *       replace GalerkinEvaluator::eval (assembly.cpp:240-291), the entry
+ *       generator HMatrix::assemble / aca call (hmatrix.hpp:45-52), batched.
  *   gk_nearfield_*
  *       replace regularize (assembly.cpp:609-697) including close_pairs
  *       (:370-401), YContext gauss/exact (:447-544), accurate_cell /
@@ -196,6 +199,30 @@ gk_status gk_nearfield_triplets(gk_nearfield* nf, int32_t* rows, int32_t* cols, 
 gk_status gk_nearfield_stats(const gk_nearfield* nf, int64_t* analytic_calls,
                              int64_t depth_hist[8]);
 gk_status gk_nearfield_destroy(gk_nearfield* nf);
+
+/* ---- block evaluation (entry generator of the compressed / H-matrix path) --- */
+/* Replaces GalerkinEvaluator (assembly.cpp:225-299), the BlockEvaluator
+ * plugin that HMatrix::assemble (hmatrix.hpp:45-52, hmatrix.cpp:811-866)
+ * calls for ACA row/column panels and dense leaves.  eps is taken from the
+ * full sides (assembly.cpp:231) and the distance mask is always on. */
+typedef struct gk_evaluator gk_evaluator;
+gk_status gk_evaluator_create(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
+                              gk_evaluator** out);
+gk_status gk_evaluator_dims(const gk_evaluator* ev, int64_t* rows, int64_t* cols);
+/* One BlockEvaluator::eval(row_ids, col_ids, out) request.  All host memory:
+ * ids are free-dof indices (duplicates allowed), out is nrows x ncols
+ * column-major with leading dimension ldo >= nrows. */
+typedef struct gk_block {
+  int32_t nrows, ncols;
+  const int32_t* row_ids;
+  const int32_t* col_ids;
+  gk_cplx* out;
+  int64_t ldo;
+} gk_block;
+/* Evaluates a batch of blocks with one copy in, one launch and one copy out
+ * (returns after the results are in the callers' buffers). */
+gk_status gk_evaluator_eval(gk_evaluator* ev, int32_t nblocks, const gk_block* blocks, gk_stream stream);
+gk_status gk_evaluator_destroy(gk_evaluator* ev);
 
 /* ---- device memory helpers for callers without a CUDA allocator ----------- */
 gk_status gk_device_alloc(uint64_t bytes, void** ptr);

@@ -490,6 +490,69 @@ std::vector<cplx> radiation_dense(const std::vector<V3>& points, const Mesh& my,
 }
 
 namespace {
+// GalerkinEvaluator::eval (assembly.cpp:227-233 constructor eps, :240-291):
+// unique supporting points in first-seen order, K over them with mask=true,
+// out = lt * (K * ru).  Dense products summed in ascending index order.
+std::vector<cplx> galerkin_eval(const Side& tst, const Side& tri, const Kernel& K, const std::vector<int>& rows,
+                                const std::vector<int>& cols) {
+  const double eps = singular_guard_radius(tst.points, tri.points);
+  const ColLists xs = by_dof(tst), ys = by_dof(tri);
+  const int64_t nr = (int64_t)rows.size(), nc = (int64_t)cols.size();
+  std::vector<int64_t> xlocal(tst.points.size(), -1), ylocal(tri.points.size(), -1);
+  std::vector<int64_t> xids, yids;
+  for (int a : rows)
+    for (int64_t p = xs.start[a]; p < xs.start[a + 1]; ++p)
+      if (xlocal[xs.pt[p]] < 0) {
+        xlocal[xs.pt[p]] = (int64_t)xids.size();
+        xids.push_back(xs.pt[p]);
+      }
+  for (int b : cols)
+    for (int64_t p = ys.start[b]; p < ys.start[b + 1]; ++p)
+      if (ylocal[ys.pt[p]] < 0) {
+        ylocal[ys.pt[p]] = (int64_t)yids.size();
+        yids.push_back(ys.pt[p]);
+      }
+  const int64_t nx = (int64_t)xids.size(), ny = (int64_t)yids.size();
+  std::vector<V3> X(nx), Y(ny);
+  for (int64_t i = 0; i < nx; ++i) X[i] = tst.points[xids[i]];
+  for (int64_t i = 0; i < ny; ++i) Y[i] = tri.points[yids[i]];
+  std::vector<cplx> Km;  // nx x ny col-major
+  evaluate_blocks(K, X.data(), nx, Y, Km, eps, /*mask=*/true);
+  std::vector<double> lt((size_t)(nr * nx), 0.0), ru((size_t)(ny * nc), 0.0);
+  for (int64_t a = 0; a < nr; ++a)
+    for (int64_t p = xs.start[rows[a]]; p < xs.start[rows[a] + 1]; ++p) lt[a + nr * xlocal[xs.pt[p]]] = xs.val[p];
+  for (int64_t b = 0; b < nc; ++b)
+    for (int64_t p = ys.start[cols[b]]; p < ys.start[cols[b] + 1]; ++p) ru[ylocal[ys.pt[p]] + ny * b] = ys.val[p];
+  std::vector<cplx> tmp((size_t)(nx * nc), cplx(0.0, 0.0)), out((size_t)(nr * nc), cplx(0.0, 0.0));
+  for (int64_t b = 0; b < nc; ++b)
+    for (int64_t y = 0; y < ny; ++y) {
+      const double r = ru[y + ny * b];
+      if (r == 0.0) continue;
+      for (int64_t x = 0; x < nx; ++x) tmp[x + nx * b] += Km[x + nx * y] * r;
+    }
+  for (int64_t b = 0; b < nc; ++b)
+    for (int64_t x = 0; x < nx; ++x) {
+      const cplx v = tmp[x + nx * b];
+      for (int64_t a = 0; a < nr; ++a) {
+        const double l = lt[a + nr * x];
+        if (l != 0.0) out[a + nr * b] += l * v;
+      }
+    }
+  return out;
+}
+}  // namespace
+
+std::vector<cplx> block_eval(const Mesh& mx, int gx, Family fx, const Mesh& my, int gy, Family fy, const Kernel& K,
+                             const std::vector<int>& rows, const std::vector<int>& cols) {
+  return galerkin_eval(make_side(mx, gx, fx), make_side(my, gy, fy), K, rows, cols);
+}
+
+std::vector<cplx> block_eval_points(const std::vector<V3>& points, const Mesh& my, int gy, Family fy,
+                                    const Kernel& K, const std::vector<int>& rows, const std::vector<int>& cols) {
+  return galerkin_eval(make_point_side(points), make_side(my, gy, fy), K, rows, cols);
+}
+
+namespace {
 std::vector<cplx> bem_product(const Side& tst, const Side& tri, const Kernel& K,
                               const BemOptions& opt, const std::vector<int>* rows) {  // :192-222
   const int64_t mxp = (int64_t)tst.points.size(), myp = (int64_t)tri.points.size();

@@ -139,6 +139,12 @@ std::vector<cplx> bem_dense(const Mesh& mx, int gx, Family fx, const Mesh& my, i
 // radiation_dense (assembly.cpp:173-190, 334-341): point side x dom_y side
 std::vector<cplx> radiation_dense(const std::vector<V3>& points, const Mesh& my, int gy, Family fy,
                                   const Kernel& K, const BemOptions& opt);
+// GalerkinEvaluator::eval (assembly.cpp:225-291): rows x cols block, col-major
+std::vector<cplx> block_eval(const Mesh& mx, int gx, Family fx, const Mesh& my, int gy, Family fy,
+                             const Kernel& K, const std::vector<int>& rows, const std::vector<int>& cols);
+// the same with a point test side (radiation_h, assembly.cpp:343-356)
+std::vector<cplx> block_eval_points(const std::vector<V3>& points, const Mesh& my, int gy, Family fy,
+                                    const Kernel& K, const std::vector<int>& rows, const std::vector<int>& cols);
 // tests/support/oracles.cpp:332-360
 std::vector<cplx> naive_bem(const Mesh& mx, int gx, Family fx, const Mesh& my, int gy,
                             Family fy, const Kernel& K);

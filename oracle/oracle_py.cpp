@@ -140,6 +140,18 @@ PYBIND11_MODULE(_oracle, m) {
     auto A = radiation_dense(P, my, gy, (Family)fy, green_kernel(name, k), BemOptions{});
     return colmajor(std::move(A), (int64_t)P.size(), dof_count(my, (Family)fy));
   });
+  m.def("block_eval", [](F64 vx, I32 ex, int gx, int fx, F64 vy, I32 ey, int gy, int fy, const std::string& name,
+                         double k, const std::vector<int>& rows, const std::vector<int>& cols) {
+    Mesh mx = to_mesh(vx, ex), my = to_mesh(vy, ey);
+    auto B = block_eval(mx, gx, (Family)fx, my, gy, (Family)fy, green_kernel(name, k), rows, cols);
+    return colmajor(std::move(B), (int64_t)rows.size(), (int64_t)cols.size());
+  });
+  m.def("block_eval_points", [](F64 pts, F64 vy, I32 ey, int gy, int fy, const std::string& name, double k,
+                                const std::vector<int>& rows, const std::vector<int>& cols) {
+    Mesh my = to_mesh(vy, ey);
+    auto B = block_eval_points(to_pts(pts), my, gy, (Family)fy, green_kernel(name, k), rows, cols);
+    return colmajor(std::move(B), (int64_t)rows.size(), (int64_t)cols.size());
+  });
   m.def("naive_bem", [](F64 vx, I32 ex, int gx, int fx, F64 vy, I32 ey, int gy, int fy,
                         const std::string& name, double k) {
     Mesh mx = to_mesh(vx, ex), my = to_mesh(vy, ey);

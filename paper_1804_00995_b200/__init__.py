@@ -54,6 +54,7 @@ regularize_radiation = _native.regularize_radiation
 AssemblyPlan = _native.AssemblyPlan
 GreenPlan = _native.GreenPlan
 NearField = _native.NearField
+GalerkinEvaluator = _native.GalerkinEvaluator
 NEAR_REF = _native.NEAR_REF
 NEAR_2HBAR = _native.NEAR_2HBAR
 matvec = _native.matvec

@@ -554,6 +554,67 @@ gk_plan_info AssemblyPlan::info() const {
 int AssemblyPlan::launches() const { return gk_plan_launches(plan_); }
 
 // ---------------------------------------------------------------------------------
+GalerkinEvaluator::GalerkinEvaluator(const Domain& dom_x, const Domain& dom_y, const FemSpace& test,
+                                     const Kernel& kernel, const FemSpace& trial) {
+  const SideTables tst = make_side_tables(dom_x, test);
+  const SideTables tri = make_side_tables(dom_y, trial);
+  const gk_side a = tst.abi(), b = tri.abi();
+  const gk_kernel k = kernel.abi();
+  throw_status(gk_evaluator_create(&a, &b, &k, &ev_));
+}
+
+GalerkinEvaluator::GalerkinEvaluator(const std::vector<Vec3>& points, const Domain& dom_y, const Kernel& kernel,
+                                     const FemSpace& trial) {
+  const SideTables tst = make_point_side_tables(points);
+  const SideTables tri = make_side_tables(dom_y, trial);
+  const gk_side a = tst.abi(), b = tri.abi();
+  const gk_kernel k = kernel.abi();
+  throw_status(gk_evaluator_create(&a, &b, &k, &ev_));
+}
+
+GalerkinEvaluator::~GalerkinEvaluator() {
+  if (ev_) gk_evaluator_destroy(ev_);
+}
+
+int64_t GalerkinEvaluator::rows() const {
+  int64_t r = 0;
+  throw_status(gk_evaluator_dims(ev_, &r, nullptr));
+  return r;
+}
+
+int64_t GalerkinEvaluator::cols() const {
+  int64_t c = 0;
+  throw_status(gk_evaluator_dims(ev_, nullptr, &c));
+  return c;
+}
+
+void GalerkinEvaluator::eval(const std::vector<int>& row_ids, const std::vector<int>& col_ids,
+                             MatrixXcd& out) const {
+  std::vector<std::pair<std::vector<int>, std::vector<int>>> req{{row_ids, col_ids}};
+  out = std::move(eval_batch(req)[0]);
+}
+
+std::vector<MatrixXcd> GalerkinEvaluator::eval_batch(
+    const std::vector<std::pair<std::vector<int>, std::vector<int>>>& req) const {
+  std::vector<MatrixXcd> out;
+  out.reserve(req.size());
+  std::vector<gk_block> blocks(req.size());
+  for (size_t b = 0; b < req.size(); ++b) {
+    const auto& [r, c] = req[b];
+    out.emplace_back((int64_t)r.size(), (int64_t)c.size());
+    gk_block& B = blocks[b];
+    B.nrows = (int32_t)r.size();
+    B.ncols = (int32_t)c.size();
+    B.row_ids = r.data();
+    B.col_ids = c.data();
+    B.out = reinterpret_cast<gk_cplx*>(out.back().data());
+    B.ldo = std::max<int64_t>(1, (int64_t)r.size());
+  }
+  throw_status(gk_evaluator_eval(ev_, (int32_t)blocks.size(), blocks.data(), nullptr));
+  return out;
+}
+
+// ---------------------------------------------------------------------------------
 std::vector<double> uniform01(uint64_t seed, int64_t n) {
   std::vector<double> out(n);
   uint64_t s = seed;

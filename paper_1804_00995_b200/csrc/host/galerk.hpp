@@ -194,6 +194,28 @@ class AssemblyPlan {
   gk_plan* plan_ = nullptr;
 };
 
+// BlockEvaluator (hmatrix.hpp:45-52) backed by the device: the Galerkin entry
+// generator of bem_h / radiation_h (assembly.cpp:225-299, 322-356).
+class GalerkinEvaluator {
+ public:
+  GalerkinEvaluator(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const Kernel& kernel,
+                    const FemSpace& trial);
+  // radiation_h form: point rows (make_point_side, assembly.cpp:173-190)
+  GalerkinEvaluator(const std::vector<Vec3>& points, const Domain& dom_y, const Kernel& kernel,
+                    const FemSpace& trial);
+  ~GalerkinEvaluator();
+  GalerkinEvaluator(const GalerkinEvaluator&) = delete;
+  GalerkinEvaluator& operator=(const GalerkinEvaluator&) = delete;
+  int64_t rows() const;
+  int64_t cols() const;
+  void eval(const std::vector<int>& row_ids, const std::vector<int>& col_ids, MatrixXcd& out) const;
+  // many eval() requests in one device round trip (ACA panels of many blocks, dense leaves)
+  std::vector<MatrixXcd> eval_batch(const std::vector<std::pair<std::vector<int>, std::vector<int>>>& req) const;
+
+ private:
+  gk_evaluator* ev_ = nullptr;
+};
+
 // ---- harness RNG: SplitMix64 -> U[0,1) -> Box-Muller -------------
 std::vector<double> uniform01(uint64_t seed, int64_t n);
 std::vector<double> normal(uint64_t seed, int64_t n);          // cos branch first

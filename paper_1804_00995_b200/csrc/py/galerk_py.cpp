@@ -309,6 +309,42 @@ PYBIND11_MODULE(_galerk, m) {
            py::arg("stream") = 0)
       .def("info", &GreenPlan::info);
 
+  py::class_<GalerkinEvaluator>(m, "GalerkinEvaluator")
+      .def(py::init<const Domain&, const Domain&, const FemSpace&, const Kernel&, const FemSpace&>(),
+           py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"))
+      .def_static(
+          "points",
+          [](F64 pts, const Domain& dy, const Kernel& k, const FemSpace& u) {
+            return std::make_unique<GalerkinEvaluator>(to_points(pts), dy, k, u);
+          },
+          py::arg("points"), py::arg("dom_y"), py::arg("kernel"), py::arg("trial"))
+      .def("rows", &GalerkinEvaluator::rows)
+      .def("cols", &GalerkinEvaluator::cols)
+      .def(
+          "eval",
+          [](const GalerkinEvaluator& e, const std::vector<int>& r, const std::vector<int>& c) {
+            MatrixXcd out;
+            {
+              py::gil_scoped_release rel;
+              e.eval(r, c, out);
+            }
+            return to_numpy(std::move(out));
+          },
+          py::arg("row_ids"), py::arg("col_ids"))
+      .def(
+          "eval_batch",
+          [](const GalerkinEvaluator& e, const std::vector<std::pair<std::vector<int>, std::vector<int>>>& req) {
+            std::vector<MatrixXcd> out;
+            {
+              py::gil_scoped_release rel;
+              out = e.eval_batch(req);
+            }
+            py::list l;
+            for (auto& M : out) l.append(to_numpy(std::move(M)));
+            return l;
+          },
+          py::arg("requests"));
+
   py::class_<NearField>(m, "NearField")
       .def(py::init<const Domain&, const Domain&, const FemSpace&, const std::string&, const FemSpace&, int,
                     double>(),

@@ -329,3 +329,19 @@ def test_regularized_collocation_near_the_surface(oracle, where):
            "outside": 1.001 * v[:5]}[where]
     pot = _collocation_potential(oracle, v, e, pts)
     assert np.all(np.abs(pot - 1.0) < 0.02)
+
+
+def test_block_eval_equals_dense_submatrix(oracle):
+    # GalerkinEvaluator::eval (assembly.cpp:240-291) reproduces the dense
+    # matrix's entries on any row/column selection (the structural identity
+    # bem_h relies on, test_assembly.cpp:262-285), duplicates included.
+    v, e = oracle.build_sphere(162, 1.0)
+    for name, k, fam in [("[exp(ikr)/r]", 3.0, P1), ("[1/r]", 0.0, P0)]:
+        A = oracle.bem_dense(v, e, 3, fam, v, e, 3, fam, name, k)
+        rows, cols = [5, 0, 17, 5, 40], [3, 100, 7, 3]
+        B = oracle.block_eval(v, e, 3, fam, v, e, 3, fam, name, k, rows, cols)
+        assert np.abs(B - A[np.ix_(rows, cols)]).max() <= 1e-14 * np.abs(A).max()
+    pts = np.array([[0.0, 0.0, 2.0], [1.5, 0.1, 0.2], [0.3, -1.2, 0.1]])
+    R = oracle.radiation_dense(pts, v, e, 3, P1, "[exp(ikr)/r]", 2.0)
+    B = oracle.block_eval_points(pts, v, e, 3, P1, "[exp(ikr)/r]", 2.0, [2, 0], [1, 50, 161])
+    assert np.abs(B - R[np.ix_([2, 0], [1, 50, 161])]).max() <= 1e-14 * np.abs(R).max()
