@@ -224,6 +224,32 @@ typedef struct gk_block {
 gk_status gk_evaluator_eval(gk_evaluator* ev, int32_t nblocks, const gk_block* blocks, gk_stream stream);
 gk_status gk_evaluator_destroy(gk_evaluator* ev);
 
+/* ---- solve step on the device-resident matrix ------------------------------ */
+/* Partial-pivot LU in place, replacing Eigen's partialPivLu()
+ * (test_assembly.cpp:227).  A: device n x n column-major; ipiv: device
+ * int64[n]; singular_at (host, optional): 0, or the 1-based index of an
+ * exactly zero pivot (the factorisation still completes, as Eigen's does). */
+gk_status gk_lu_factor(gk_cplx* A, int64_t n, int64_t lda, int64_t* ipiv, int64_t* singular_at, gk_stream stream);
+/* B <- A^{-1} B with the factors of gk_lu_factor; B: device n x nrhs. */
+gk_status gk_lu_solve(const gk_cplx* LU, int64_t n, int64_t lda, const int64_t* ipiv, gk_cplx* B, int64_t ldb,
+                      int64_t nrhs, gk_stream stream);
+/* SolveInfo (linsolve.hpp:26-31); history_len entries of the relative
+ * residual history were written if a history array was given. */
+typedef struct gk_solve_info {
+  int32_t converged;
+  int32_t iterations;
+  double residual;
+  int32_t history_len;
+  int32_t reserved;
+} gk_solve_info;
+/* Restarted GMRES (linsolve.cpp:19-121) with the stored matrix as operator
+ * (LinearOperator::from_matrix, linsolve.hpp:20-23), no preconditioner.
+ * A, b, x: device; x is overwritten with the solution (start 0).
+ * history: host double[maxit] or NULL.  tol <= 0 -> GK_EINVAL "gmres: tol
+ * must be positive" (linsolve.cpp:24). */
+gk_status gk_gmres(const gk_cplx* A, int64_t n, int64_t lda, const gk_cplx* b, gk_cplx* x, double tol,
+                   int32_t restart, int32_t maxit, gk_solve_info* info, double* history, gk_stream stream);
+
 /* ---- device memory helpers for callers without a CUDA allocator ----------- */
 gk_status gk_device_alloc(uint64_t bytes, void** ptr);
 gk_status gk_device_free(void* ptr);

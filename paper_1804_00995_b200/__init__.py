@@ -59,6 +59,9 @@ NEAR_REF = _native.NEAR_REF
 NEAR_2HBAR = _native.NEAR_2HBAR
 matvec = _native.matvec
 matvec_launches = _native.matvec_launches
+lu_factor = _native.lu_factor
+lu_solve = _native.lu_solve
+gmres = _native.gmres
 side_tables = _native.side_tables
 uniform01 = _native.uniform01
 normal = _native.normal

@@ -19,7 +19,7 @@ OUT = os.path.join(PKG, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["gk_abi.cu", "gk_assembly.cu", "gk_matvec.cu", "gk_green.cu", "gk_nearfield.cu", "gk_blockeval.cu",
+CU_SOURCES = ["gk_abi.cu", "gk_assembly.cu", "gk_matvec.cu", "gk_green.cu", "gk_nearfield.cu", "gk_blockeval.cu", "gk_solve.cu",
               "gk_diag.cu"]
 CXX_SOURCES = ["gk_plan.cpp", "host/galerk.cpp"]
 HEADERS = ["gk_internal.hpp", "gk_math.cuh", "host/galerk.hpp", "../../include/galerk_b200_diag.h"]

@@ -302,6 +302,50 @@ PYBIND11_MODULE(_galerk, m) {
       py::arg("A"), py::arg("rows"), py::arg("cols"), py::arg("lda"), py::arg("x"), py::arg("y"),
       py::arg("stream") = 0);
   m.def("matvec_launches", &gk_matvec_launches);
+  m.def(
+      "lu_factor",
+      [](uintptr_t A, int64_t n, int64_t lda, uintptr_t ipiv, uintptr_t stream) {
+        int64_t singular_at = 0;
+        {
+          py::gil_scoped_release rel;
+          throw_status(gk_lu_factor(reinterpret_cast<gk_cplx*>(A), n, lda, reinterpret_cast<int64_t*>(ipiv),
+                                    &singular_at, as_stream(stream)));
+        }
+        return singular_at;
+      },
+      py::arg("A"), py::arg("n"), py::arg("lda"), py::arg("ipiv"), py::arg("stream") = 0);
+  m.def(
+      "lu_solve",
+      [](uintptr_t LU, int64_t n, int64_t lda, uintptr_t ipiv, uintptr_t B, int64_t ldb, int64_t nrhs,
+         uintptr_t stream) {
+        py::gil_scoped_release rel;
+        throw_status(gk_lu_solve(reinterpret_cast<const gk_cplx*>(LU), n, lda, reinterpret_cast<const int64_t*>(ipiv),
+                                 reinterpret_cast<gk_cplx*>(B), ldb, nrhs, as_stream(stream)));
+      },
+      py::arg("LU"), py::arg("n"), py::arg("lda"), py::arg("ipiv"), py::arg("B"), py::arg("ldb"), py::arg("nrhs"),
+      py::arg("stream") = 0);
+  m.def(
+      "gmres",
+      [](uintptr_t A, int64_t n, int64_t lda, uintptr_t b, uintptr_t x, double tol, int restart, int maxit,
+         uintptr_t stream) {
+        gk_solve_info info{};
+        std::vector<double> hist(std::max(0, maxit));
+        {
+          py::gil_scoped_release rel;
+          throw_status(gk_gmres(reinterpret_cast<const gk_cplx*>(A), n, lda, reinterpret_cast<const gk_cplx*>(b),
+                                reinterpret_cast<gk_cplx*>(x), tol, restart, maxit, &info, hist.data(),
+                                as_stream(stream)));
+        }
+        hist.resize(std::min<size_t>(hist.size(), (size_t)std::max(0, info.history_len)));
+        py::dict d;
+        d["converged"] = info.converged != 0;
+        d["iterations"] = info.iterations;
+        d["residual"] = info.residual;
+        d["history"] = hist;
+        return d;
+      },
+      py::arg("A"), py::arg("n"), py::arg("lda"), py::arg("b"), py::arg("x"), py::arg("tol") = 1e-6,
+      py::arg("restart") = 50, py::arg("maxit") = 1000, py::arg("stream") = 0);
 
   py::class_<GreenPlan>(m, "GreenPlan")
       .def(py::init<F64, F64, const Kernel&>(), py::arg("targets"), py::arg("sources"), py::arg("kernel"))
