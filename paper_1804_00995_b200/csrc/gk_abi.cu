@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <unordered_map>
 
 #include "../../include/galerk_b200_diag.h"
@@ -292,18 +293,47 @@ gk_status gk_plan_destroy(gk_plan* P) {
 gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kernel* kernel, const gk_options* opts,
                        gk_cplx* A_host, int64_t lda) {
   return guard([&] {
+    const bool timing = std::getenv("GK_TIMING") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      cudaDeviceSynchronize();
+      const auto t1 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[gk_bem_dense] %-10s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
     auto P = make_plan(test, trial, kernel, opts);
+    lap("plan");
     if (P->rows == 0 || P->cols == 0) return;
     if (!A_host) throw std::invalid_argument("gk_bem_dense: null output matrix");
     if (lda < P->rows) throw std::invalid_argument("gk_bem_dense: lda < rows");
-    DevBuf A;
-    A.alloc(sizeof(gk_cplx) * (size_t)P->rows * (size_t)P->cols);
+    // The device matrix: a grow-only scratch buffer kept between calls up to
+    // 16 GB (one-shot callers repeat with the same size, and mapping a fresh
+    // 1.7 GB allocation costs ~9 ms); larger matrices are allocated per call.
+    static std::mutex scratch_mutex;
+    static DevBuf scratch;
+    std::unique_lock<std::mutex> hold(scratch_mutex, std::defer_lock);
+    DevBuf own;
+    const size_t bytes = sizeof(gk_cplx) * (size_t)P->rows * (size_t)P->cols;
+    void* A = nullptr;
+    if (bytes <= (16ull << 30)) {
+      hold.lock();
+      if (scratch.bytes < bytes) scratch.alloc(bytes);
+      A = scratch.p;
+    } else {
+      own.alloc(bytes);
+      A = own.p;
+    }
     cudaStream_t s = nullptr;
-    assemble(P.get(), A.as<gk_cplx>(), P->rows, s);
-    cuda_check(cudaMemcpy2DAsync(A_host, sizeof(gk_cplx) * lda, A.p, sizeof(gk_cplx) * P->rows,
+    lap("alloc");
+    assemble(P.get(), static_cast<gk_cplx*>(A), P->rows, s);
+    lap("assemble");
+    cuda_check(cudaMemcpy2DAsync(A_host, sizeof(gk_cplx) * lda, A, sizeof(gk_cplx) * P->rows,
                                  sizeof(gk_cplx) * P->rows, P->cols, cudaMemcpyDeviceToHost, s),
                "cudaMemcpy2DAsync D2H");
     cuda_check(cudaStreamSynchronize(s), "gk_bem_dense");
+    lap("d2h");
   });
 }
 

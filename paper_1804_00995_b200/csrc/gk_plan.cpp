@@ -9,6 +9,9 @@
 #include <cstdio>
 #include <numeric>
 #include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <unordered_map>
 
 #include "gk_internal.hpp"
@@ -340,124 +343,215 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
   return B;
 }
 
+namespace {
+// Static-partition parallel loop over [0, n) on up to GK_THREADS (default:
+// hardware threads, capped at 16) host threads; fn(begin, end) per chunk.
+template <class F>
+void parallel_for(int64_t n, F&& fn) {
+  static const int nthreads = [] {
+    const char* e = std::getenv("GK_THREADS");
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    return std::max(1, e ? std::atoi(e) : std::min(hw, 16));
+  }();
+  const int nt = (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, n / 8));
+  if (nt <= 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex m;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        fn(n * t / nt, n * (t + 1) / nt);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(m);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+struct XBlock {  // one x block's tables (block-local location indices)
+  std::vector<int32_t> locs, sup_u, sup_n;  // locations; per-entry local index; entries per row
+  std::vector<double> sup_c;
+};
+struct YBlock {  // one y block's records, in descending first-slot order
+  std::vector<YRec> recs;
+  std::vector<int32_t> loc;
+  uint32_t zero = 0;
+  bool second = false, equal = true;
+};
+}  // namespace
+
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
                        const BlockLayout& B) {
   TileTables T;
   const int64_t nrows = X.nfree;
+  const int64_t nIb = (int64_t)B.xb.size() - 1, nJb = (int64_t)B.yb.size() - 1;
+  // ---- x blocks (boundaries from the layout), built in parallel
+  std::vector<XBlock> xb(nIb);
+  parallel_for(nIb, [&](int64_t b0, int64_t b1) {
+    std::vector<int64_t> owner(X.size(), -1);
+    std::vector<int32_t> local(X.size(), 0);
+    for (int64_t blk = b0; blk < b1; ++blk) {
+      XBlock& XB = xb[blk];
+      for (int64_t p = B.xb[blk]; p < B.xb[blk + 1]; ++p) {
+        for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
+          const int32_t u = X.dloc[s];
+          if (owner[u] != blk) {
+            owner[u] = blk;
+            local[u] = (int32_t)XB.locs.size();
+            XB.locs.push_back(u);
+          }
+          XB.sup_u.push_back(local[u]);
+          XB.sup_c.push_back(X.dcoef[s]);
+        }
+        XB.sup_n.push_back((int32_t)(X.dstart[p + 1] - X.dstart[p]));
+      }
+    }
+  });
   std::vector<int32_t> xl_id;  // global x location id of every block entry (parallel to xl_x)
-  // ---- x blocks (boundaries from the layout)
-  std::vector<int64_t> owner(X.size(), -1);
-  std::vector<int32_t> local(X.size(), 0);
+  {
+    size_t nl = 0, ns = 0;
+    for (const XBlock& XB : xb) {
+      nl += XB.locs.size();
+      ns += XB.sup_u.size();
+    }
+    xl_id.reserve(nl);
+    T.xl_x.reserve(nl);
+    T.xl_y.reserve(nl);
+    T.xl_z.reserve(nl);
+    T.xsup_u.reserve(ns);
+    T.xsup_c.reserve(ns);
+  }
   T.xb_dof_start.push_back(0);
   T.xb_loc_start.push_back(0);
   T.xsup_start.assign(nrows + 1, 0);
-  int64_t p = 0;
-  std::vector<int32_t> blk_locs;
-  for (size_t blk = 0; blk + 1 < B.xb.size(); ++blk) {
-    const int64_t end = B.xb[blk + 1];
-    blk_locs.clear();
-    while (p < end) {
-      for (int64_t s = X.dstart[p]; s < X.dstart[p + 1]; ++s) {
-        const int32_t u = X.dloc[s];
-        if (owner[u] != blk) {
-          owner[u] = blk;
-          local[u] = (int32_t)blk_locs.size();
-          blk_locs.push_back(u);
-        }
-        T.xsup_u.push_back(local[u]);
-        T.xsup_c.push_back(X.dcoef[s]);
+  {
+    int64_t p = 0;
+    for (int64_t blk = 0; blk < nIb; ++blk) {
+      const XBlock& XB = xb[blk];
+      for (int32_t n : XB.sup_n) {
+        T.xsup_start[p + 1] = T.xsup_start[p] + n;
+        ++p;
       }
-      T.xsup_start[p + 1] = (int32_t)T.xsup_u.size();
-      ++p;
+      T.xsup_u.insert(T.xsup_u.end(), XB.sup_u.begin(), XB.sup_u.end());
+      T.xsup_c.insert(T.xsup_c.end(), XB.sup_c.begin(), XB.sup_c.end());
+      for (int32_t u : XB.locs) {
+        T.xl_x.push_back(X.x[u]);
+        T.xl_y.push_back(X.y[u]);
+        T.xl_z.push_back(X.z[u]);
+        xl_id.push_back(u);
+      }
+      T.xb_dof_start.push_back((int32_t)p);
+      T.xb_loc_start.push_back((int32_t)T.xl_x.size());
     }
-    for (int32_t u : blk_locs) {
-      T.xl_x.push_back(X.x[u]);
-      T.xl_y.push_back(X.y[u]);
-      T.xl_z.push_back(X.z[u]);
-      xl_id.push_back(u);
-    }
-    T.xb_dof_start.push_back((int32_t)p);
-    T.xb_loc_start.push_back((int32_t)T.xl_x.size());
   }
   // ---- y blocks (boundaries from the layout): records = incident locations,
-  // each carrying <= 2 (slot, coef) pairs, ordered by first slot so that the
-  // kernel can keep a run accumulator for it in registers.
-  std::vector<int64_t> ystamp(Y.size(), -1);
-  int64_t stamp_id = 0;
+  // each carrying <= 2 (slot, coef) pairs.  Descending first slot: second
+  // slots are larger than first slots, so every second-slot update of a row
+  // comes after that row's own run has been flushed — the run flush is the
+  // row's first touch and can be a plain store; rows without a run of their
+  // own are only ever read-modify-written and get zero-filled (bitmask).
+  std::vector<YBlock> yb(nJb);
+  parallel_for(nJb, [&](int64_t b0, int64_t b1) {
+    std::vector<int64_t> ystamp(Y.size(), -1);
+    std::vector<std::pair<int32_t, double>> sl;  // slots of one location inside the block
+    std::vector<YRec> recs;
+    std::vector<int32_t> rec_loc, order;
+    for (int64_t b = b0; b < b1; ++b) {
+      const int64_t q0 = B.yb[b], q1 = B.yb[b + 1];
+      recs.clear();
+      rec_loc.clear();
+      for (int64_t q = q0; q < q1; ++q)
+        for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
+          const int32_t v = Y.dloc[s];
+          if (ystamp[v] == b) continue;
+          ystamp[v] = b;
+          sl.clear();
+          for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
+            const int32_t pq = Y.iperm[Y.cdof[c]];
+            if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
+          }
+          std::stable_sort(sl.begin(), sl.end(), [](const auto& a, const auto& c) { return a.first < c.first; });
+          for (size_t a = 0; a < sl.size(); a += 2) {
+            YRec r;
+            r.x = Y.x[v];
+            r.y = Y.y[v];
+            r.z = Y.z[v];
+            r.off0 = sl[a].first * kUCap * 16;
+            r.c0 = sl[a].second;
+            if (a + 1 < sl.size()) {
+              r.off1 = sl[a + 1].first * kUCap * 16;
+              r.c1 = sl[a + 1].second;
+            } else {
+              r.off1 = -1;
+              r.c1 = 0.0;
+            }
+            recs.push_back(r);
+            rec_loc.push_back(v);
+          }
+        }
+      order.resize(recs.size());
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return recs[a].off0 > recs[c].off0; });
+      YBlock& YB = yb[b];
+      YB.recs.resize(recs.size());
+      YB.loc.resize(recs.size());
+      uint32_t has_run = 0;
+      for (size_t i = 0; i < order.size(); ++i) {
+        const YRec& r = recs[order[i]];
+        YB.recs[i] = r;
+        YB.loc[i] = rec_loc[order[i]];
+        YB.second |= r.off1 >= 0;
+        if (r.off1 >= 0 && std::memcmp(&r.c0, &r.c1, sizeof(double)) != 0) YB.equal = false;
+        has_run |= 1u << (r.off0 / (kUCap * 16));
+      }
+      const uint32_t all = (q1 - q0) >= 32 ? 0xffffffffu : ((1u << (q1 - q0)) - 1u);
+      YB.zero = all & ~has_run;
+    }
+  });
+  // y location -> y blocks holding it (CSR; a location is listed once per block)
+  std::vector<int64_t> yb_start(Y.size() + 1, 0);
+  std::vector<int32_t> yb_list, last(Y.size(), -1);
+  for (int64_t b = 0; b < nJb; ++b)
+    for (int32_t v : yb[b].loc)
+      if (last[v] != (int32_t)b) {
+        last[v] = (int32_t)b;
+        yb_start[v + 1]++;
+      }
+  for (int64_t v = 0; v < Y.size(); ++v) yb_start[v + 1] += yb_start[v];
+  yb_list.resize(yb_start[Y.size()]);
+  {
+    std::vector<int64_t> fill(yb_start.begin(), yb_start.end() - 1);
+    std::fill(last.begin(), last.end(), -1);
+    for (int64_t b = 0; b < nJb; ++b)
+      for (int32_t v : yb[b].loc)
+        if (last[v] != (int32_t)b) {
+          last[v] = (int32_t)b;
+          yb_list[fill[v]++] = (int32_t)b;
+        }
+  }
+  size_t nrec_total = 0;
+  for (const YBlock& YB : yb) nrec_total += YB.recs.size();
+  T.yrec.reserve(nrec_total);
+  T.yb_zero.reserve(nJb);
+  T.yb_dof_start.reserve(nJb + 1);
+  T.yb_rec_start.reserve(nJb + 1);
   T.yb_dof_start.push_back(0);
   T.yb_rec_start.push_back(0);
-  std::vector<YRec> recs;
-  std::vector<int32_t> rec_loc;                  // y location id of each record of the block
-  std::vector<std::vector<int32_t>> yblocks_of(Y.size());  // y location -> y blocks holding it
-  std::vector<std::pair<int32_t, double>> sl;    // slots of one location inside the block
-  auto make_records = [&](int64_t q0, int64_t q1) {
-    recs.clear();
-    rec_loc.clear();
-    ++stamp_id;
-    for (int64_t q = q0; q < q1; ++q)
-      for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
-        const int32_t v = Y.dloc[s];
-        if (ystamp[v] == stamp_id) continue;
-        ystamp[v] = stamp_id;
-        sl.clear();
-        for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
-          const int32_t pq = Y.iperm[Y.cdof[c]];
-          if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
-        }
-        std::stable_sort(sl.begin(), sl.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (size_t a = 0; a < sl.size(); a += 2) {
-          YRec r;
-          r.x = Y.x[v];
-          r.y = Y.y[v];
-          r.z = Y.z[v];
-          r.off0 = sl[a].first * kUCap * 16;
-          r.c0 = sl[a].second;
-          if (a + 1 < sl.size()) {
-            r.off1 = sl[a + 1].first * kUCap * 16;
-            r.c1 = sl[a + 1].second;
-          } else {
-            r.off1 = -1;
-            r.c1 = 0.0;
-          }
-          recs.push_back(r);
-          rec_loc.push_back(v);
-        }
-      }
-    std::vector<int32_t> order(recs.size());
-    std::iota(order.begin(), order.end(), 0);
-    // Descending first slot: second slots are larger than first slots, so every
-    // second-slot update of a row comes after that row's own run has been
-    // flushed — the run flush is the row's first touch and can be a plain store.
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return recs[a].off0 > recs[b].off0; });
-    std::vector<YRec> r2(recs.size());
-    std::vector<int32_t> l2(recs.size());
-    for (size_t i = 0; i < order.size(); ++i) {
-      r2[i] = recs[order[i]];
-      l2[i] = rec_loc[order[i]];
-    }
-    recs.swap(r2);
-    rec_loc.swap(l2);
-  };
-  for (size_t b = 0; b + 1 < B.yb.size(); ++b) {
-    const int64_t q0 = B.yb[b], q1 = B.yb[b + 1];
-    make_records(q0, q1);
-    const int32_t bj = (int32_t)T.yb_dof_start.size() - 1;
-    for (int32_t v : rec_loc)
-      if (yblocks_of[v].empty() || yblocks_of[v].back() != bj) yblocks_of[v].push_back(bj);
-    // rows without a run of their own are only ever read-modify-written: zero them
-    uint32_t has_run = 0;
-    for (const YRec& r : recs) {
-      T.has_second_slot |= r.off1 >= 0;
-      if (r.off1 >= 0 && __builtin_memcmp(&r.c0, &r.c1, sizeof(double)) != 0) T.equal_coefs = false;
-      has_run |= 1u << (r.off0 / (kUCap * 16));
-    }
-    const uint32_t all = (q1 - q0) >= 32 ? 0xffffffffu : ((1u << (q1 - q0)) - 1u);
-    T.yb_zero.push_back(all & ~has_run);
-    T.yrec.insert(T.yrec.end(), recs.begin(), recs.end());
-    T.yb_dof_start.push_back((int32_t)q1);
+  for (int64_t b = 0; b < nJb; ++b) {
+    const YBlock& YB = yb[b];
+    T.has_second_slot |= YB.second;
+    if (YB.second && !YB.equal) T.equal_coefs = false;
+    T.yb_zero.push_back(YB.zero);
+    T.yrec.insert(T.yrec.end(), YB.recs.begin(), YB.recs.end());
+    T.yb_dof_start.push_back((int32_t)B.yb[b + 1]);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
   }
-  const int64_t nIb = (int64_t)T.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
 
@@ -467,13 +561,16 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
   const bool unsafe = C.unsafe;
   std::vector<std::vector<int32_t>> masked_j(nIb);
   if (!unsafe)
-    for (int64_t bi = 0; bi < nIb; ++bi) {
-      for (int32_t e = T.xb_loc_start[bi]; e < T.xb_loc_start[bi + 1]; ++e) {
-        const int32_t v = C.y_of_x[xl_id[e]];
-        if (v >= 0) masked_j[bi].insert(masked_j[bi].end(), yblocks_of[v].begin(), yblocks_of[v].end());
+    parallel_for(nIb, [&](int64_t b0, int64_t b1) {
+      for (int64_t bi = b0; bi < b1; ++bi) {
+        for (int32_t e = T.xb_loc_start[bi]; e < T.xb_loc_start[bi + 1]; ++e) {
+          const int32_t v = C.y_of_x[xl_id[e]];
+          if (v >= 0)
+            masked_j[bi].insert(masked_j[bi].end(), yb_list.begin() + yb_start[v], yb_list.begin() + yb_start[v + 1]);
+        }
+        std::sort(masked_j[bi].begin(), masked_j[bi].end());
       }
-      std::sort(masked_j[bi].begin(), masked_j[bi].end());
-    }
+    });
   // ---- tiles (symmetric: skip tiles strictly below the diagonal)
   for (int64_t bi = 0; bi < nIb; ++bi) {
     int64_t first = 0;
