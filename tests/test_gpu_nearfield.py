@@ -155,3 +155,23 @@ def test_regularize_radiation_edge_cases(galerk):
     assert len(vals) == 0  # no element within 3 R_y of a far point
     with pytest.raises(ValueError):
         galerk.regularize_radiation(far, dom, "[log r]", sp)
+
+
+def test_regularized_collocation_at_vertices_reference_test(galerk, oracle):
+    """test_assembly.cpp:248-260 literally: collocation at the first 5 mesh
+    vertices.  The reference's analytic integral evaluates atan(0/0) there and
+    returns NaN (reproduced by the oracle); the device sums the edge angles as
+    one solid-angle atan2, which is finite at a vertex (the exact integral is),
+    so the reference test's own check |pot - 1| < 0.02 passes on the device."""
+    m, dom, sp, _ = sphere_problem(galerk, 642, 3, "P1")
+    v, e = np.asarray(m.vertices), np.asarray(m.elements)
+    pts = v[:5].copy()
+    colptr, rows, vals, shape = galerk.regularize_radiation(pts, dom, "[1/r]", sp)
+    assert np.all(np.isfinite(vals))
+    cols = np.repeat(np.arange(shape[1]), np.diff(colptr))
+    rad = galerk.radiation_dense(pts, dom, galerk.green_kernel("[1/r]", 0.0), sp)
+    rad[np.asarray(rows), cols] += np.asarray(vals)
+    pot = (rad @ np.ones(shape[1])).real / (4 * math.pi)
+    assert np.all(np.abs(pot - 1.0) < 0.02)
+    _, _, ov = oracle.regularize_radiation(pts, v, e, 3, P1, "[1/r]")
+    assert np.any(np.isnan(ov))  # the restated reference algorithm
