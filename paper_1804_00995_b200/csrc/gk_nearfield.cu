@@ -23,6 +23,7 @@
 #include <memory>
 
 #include "gk_internal.hpp"
+#include "gk_math.cuh"
 
 namespace gk {
 namespace {
@@ -43,6 +44,44 @@ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 __device__ __forceinline__ double nrm(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+// |a| through the refined reciprocal square root (~1 ulp, no slow path); 0 at a = 0
+__device__ __forceinline__ double nrm_fast(V3 a) {
+  const double r2 = fma(a.z, a.z, fma(a.y, a.y, a.x * a.x));
+  return r2 > 0.0 ? r2 * gk::rsqrt_refined(r2) : 0.0;
+}
+
+// log(num / den) for positive normal num, den without forming the quotient:
+// num = mn 2^en, den = md 2^ed with mn, md in [1, 2); one of them is doubled
+// so that mn / md lies in [1/sqrt2, sqrt2), then
+//   log(num/den) = k ln2 + log((1+s)/(1-s)),  s = (mn - md) / (mn + md),
+// |s| <= 0.1716, and log((1+s)/(1-s)) = 2s + s z R(z), z = s^2, with R the
+// atanh series 2/3 + 2z/5 + ... + 2z^8/19 (truncation < 1e-17 relative).
+// mn - md is exact (Sterbenz).  ~1-2 ulp; one division instead of a division
+// plus the library log's own reduction.
+__device__ __forceinline__ double log_ratio(double num, double den) {
+  const int hn = __double2hiint(num), hd = __double2hiint(den);
+  int k = ((hn >> 20) & 0x7ff) - ((hd >> 20) & 0x7ff);
+  double mn = __hiloint2double((hn & 0x800fffff) | 0x3ff00000, __double2loint(num));
+  double md = __hiloint2double((hd & 0x800fffff) | 0x3ff00000, __double2loint(den));
+  const bool up = mn > 1.4142135623730951 * md, dn = mn < 0.7071067811865476 * md;
+  md = up ? 2.0 * md : md;
+  mn = dn ? 2.0 * mn : mn;
+  k += up ? 1 : (dn ? -1 : 0);
+  const double s = (mn - md) / (mn + md);
+  const double z = s * s;
+  double r = 2.0 / 19.0;
+  r = fma(r, z, 2.0 / 17.0);
+  r = fma(r, z, 2.0 / 15.0);
+  r = fma(r, z, 2.0 / 13.0);
+  r = fma(r, z, 2.0 / 11.0);
+  r = fma(r, z, 2.0 / 9.0);
+  r = fma(r, z, 2.0 / 7.0);
+  r = fma(r, z, 2.0 / 5.0);
+  r = fma(r, z, 2.0 / 3.0);
+  const double kd = (double)k;
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  return fma(kd, ln2_hi, 2.0 * s + fma(s * z, r, kd * ln2_lo));
+}
 
 // y-triangle frame shared by all analytic calls of a pair
 struct YTri {
@@ -86,6 +125,7 @@ struct WarpSmem {
   Node stack[kStack];
   double vals[32][kMaxLoc];
   double subs[4][kMaxLoc];
+  double subc[4][9];  // barycentric corners of the current node's 4 sub-cells
   double acc[kMaxLoc];
   YTri tri;
 };
@@ -109,7 +149,7 @@ __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3
   const double w0 = dot(x - T.v[0], T.n);
   rho = x - w0 * T.n;
   const V3 A = T.v[0] - x, B = T.v[1] - x, C = T.v[2] - x;
-  const double rv[3] = {nrm(A), nrm(B), nrm(C)};  // rp of edge i == rm of edge i+1
+  const double rv[3] = {nrm_fast(A), nrm_fast(B), nrm_fast(C)};  // rp of edge i == rm of edge i+1
   const double trip = dot(A, cross(B, C));
   const double vden = fma(rv[0] * rv[1], rv[2], fma(dot(A, B), rv[2], fma(dot(A, C), rv[1], dot(B, C) * rv[0])));
   const double omega = 2.0 * atan2(trip, vden);
@@ -127,7 +167,7 @@ __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3
     const double num = a ? rp + sp : (b ? rm - sm : (rp + sp) * (rm - sm));
     const double den = a ? rm + sm : (b ? rp - sp : r0sq);
     const bool ok = r0sq > 1e-28 * T.len[i] * T.len[i] && T.len[i] > 1e-300;
-    f[i] = ok ? log(num / den) : 0.0;
+    f[i] = ok ? log_ratio(num, den) : 0.0;
     t[i] = T.len[i] > 1e-300 ? ti : 0.0;
     if (MOMENT) mo[i] = r0sq * f[i] + sp * rp - sm * rm;
   }
@@ -322,10 +362,22 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
       const Node nd = S.stack[sp];
       __syncwarp();
       const double frac = 0.25 * nd.frac;
+      if (lane < 3) {  // sub-cell corners, one barycentric component per lane (assembly.cpp:587-594)
+        const int k = lane;
+        const double* nc = S.stack[sp].corners;  // still intact: children are pushed after the evaluation
+        const double c0 = nc[k], c1 = nc[3 + k], c2 = nc[6 + k];
+        const double m01 = 0.5 * (c0 + c1), m12 = 0.5 * (c1 + c2), m20 = 0.5 * (c2 + c0);
+        S.subc[0][k] = c0, S.subc[0][3 + k] = m01, S.subc[0][6 + k] = m20;
+        S.subc[1][k] = c1, S.subc[1][3 + k] = m12, S.subc[1][6 + k] = m01;
+        S.subc[2][k] = c2, S.subc[2][3 + k] = m20, S.subc[2][6 + k] = m12;
+        S.subc[3][k] = m01, S.subc[3][3 + k] = m12, S.subc[3][6 + k] = m20;
+      }
+      __syncwarp();
       if (lane < 28) {
         const int sub = lane / 7, q = lane - 7 * sub;
         double cr[9];
-        sub_corners(nd.corners, sub, cr);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) cr[c] = S.subc[sub][c];
         double b[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c)
@@ -366,10 +418,8 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
         if (lane < 4) {  // push children 3..0 so that sub 0 is processed first
           const int s = 3 - lane;
           Node& ch = S.stack[sp + lane];
-          double cr[9];
-          sub_corners(nd.corners, s, cr);
 #pragma unroll
-          for (int c = 0; c < 9; ++c) ch.corners[c] = cr[c];
+          for (int c = 0; c < 9; ++c) ch.corners[c] = S.subc[s][c];
           for (int t = 0; t < NL; ++t) ch.whole[t] = S.subs[s][t];
           ch.frac = frac;
           ch.tol = 0.5 * nd.tol;
