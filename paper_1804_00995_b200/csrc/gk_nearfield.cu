@@ -67,7 +67,15 @@ __device__ __forceinline__ double log_ratio(double num, double den) {
   md = up ? 2.0 * md : md;
   mn = dn ? 2.0 * mn : mn;
   k += up ? 1 : (dn ? -1 : 0);
-  const double s = (mn - md) / (mn + md);
+  // s = d / sg with sg in [1.7, 6): reciprocal by MUFU.RCP64H + two Newton
+  // steps, then one residual correction of the quotient (~0.5 ulp, no slow path)
+  const double d = mn - md, sg = mn + md;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(sg));
+  y = fma(y, fma(-sg, y, 1.0), y);
+  y = fma(y, fma(-sg, y, 1.0), y);
+  const double q0 = d * y;
+  const double s = fma(fma(-sg, q0, d), y, q0);
   const double z = s * s;
   double r = 2.0 / 19.0;
   r = fma(r, z, 2.0 / 17.0);
