@@ -70,10 +70,10 @@ struct gk_plan {
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false;
   int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0)
-  DevBuf tiles, mtiles;  // TileDesc per unmasked / masked tile
+  DevBuf tiles;  // TileDesc per tile, (x block, y block) order, masked ones flagged
   DevBuf xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c, yrec, xperm, yperm;
   uint64_t device_bytes() const {
-    const DevBuf* b[] = {&tiles, &mtiles, &xl_x, &xl_y, &xl_z, &xsup_start, &xsup_u, &xsup_c, &yrec, &xperm, &yperm};
+    const DevBuf* b[] = {&tiles, &xl_x, &xl_y, &xl_z, &xsup_start, &xsup_u, &xsup_c, &yrec, &xperm, &yperm};
     uint64_t s = 0;
     for (auto* p : b) s += p->bytes;
     return s;
@@ -112,12 +112,12 @@ void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) 
 
 // One self-contained descriptor per tile: the kernel's staging loads then
 // depend on a single descriptor load instead of a chain of table lookups.
-std::vector<TileDesc> make_tile_descs(const TileTables& T, const std::vector<int32_t>& ti,
-                                      const std::vector<int32_t>& tj) {
-  std::vector<TileDesc> d(ti.size());
-  for (size_t k = 0; k < ti.size(); ++k) {
-    const int32_t bi = ti[k], bj = tj[k];
-    TileDesc& D = d[k];
+// Unmasked and masked tiles are merged back into (x block, y block) order and
+// run in one launch; the flag selects the masked pair loop per CTA.
+std::vector<TileDesc> make_tile_descs(const TileTables& T) {
+  const size_t nu = T.tile_i.size(), nm = T.mtile_i.size();
+  std::vector<TileDesc> d(nu + nm);
+  auto fill = [&](TileDesc& D, int32_t bi, int32_t bj, bool masked) {
     D.i0 = T.xb_dof_start[bi];
     D.nI = T.xb_dof_start[bi + 1] - D.i0;
     D.j0 = T.yb_dof_start[bj];
@@ -129,7 +129,19 @@ std::vector<TileDesc> make_tile_descs(const TileTables& T, const std::vector<int
     D.xs0 = T.xsup_start[D.i0];
     D.nxs = T.xsup_start[D.i0 + D.nI] - D.xs0;
     D.zero_rows = T.yb_zero[bj];
-    D.pad = 0;
+    D.masked = masked ? 1 : 0;
+  };
+  size_t a = 0, b = 0, k = 0;
+  while (a < nu || b < nm) {
+    const bool take_m = b < nm && (a >= nu || std::make_pair(T.mtile_i[b], T.mtile_j[b]) <
+                                                  std::make_pair(T.tile_i[a], T.tile_j[a]));
+    if (take_m) {
+      fill(d[k++], T.mtile_i[b], T.mtile_j[b], true);
+      ++b;
+    } else {
+      fill(d[k++], T.tile_i[a], T.tile_j[a], false);
+      ++a;
+    }
   }
   return d;
 }
@@ -185,8 +197,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->nmtiles = (int64_t)T.mtile_i.size();
   P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
-  P->tiles.upload(make_tile_descs(T, T.tile_i, T.tile_j));
-  P->mtiles.upload(make_tile_descs(T, T.mtile_i, T.mtile_j));
+  P->tiles.upload(make_tile_descs(T));
   P->xl_x.upload(T.xl_x);
   P->xl_y.upload(T.xl_y);
   P->xl_z.upload(T.xl_z);
@@ -222,9 +233,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
-  launch_assemble(a, P->ntiles, P->helmholtz, /*mask=*/false, P->slots, stream);
-  a.tiles = P->mtiles.as<TileDesc>();
-  launch_assemble(a, P->nmtiles, P->helmholtz, /*mask=*/true, P->slots, stream);
+  launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
 }
 
 }  // namespace
@@ -283,7 +292,7 @@ gk_status gk_plan_assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream
 }
 
 int32_t gk_plan_launches(const gk_plan* P) {
-  return P ? (P->ntiles > 0 ? 1 : 0) + (P->nmtiles > 0 ? 1 : 0) : 0;
+  return P ? (P->ntiles + P->nmtiles > 0 ? 1 : 0) : 0;
 }
 
 gk_status gk_plan_destroy(gk_plan* P) {

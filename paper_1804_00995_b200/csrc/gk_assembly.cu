@@ -19,11 +19,14 @@
 // fixed order) and write them; with identical sides only tiles on or above
 // the diagonal are computed and mirrored (G is symmetric).
 //
-// Specialisations: MASK (tile may hold a coincident pair -> r^2 <= eps^2
-// mask); SLOTS = 0 (no record has a second slot: P0 with twin-free rules),
+// Tiles that may hold a coincident pair (host-flagged) run the pair loop with
+// the r^2 <= eps^2 mask, all others without it, in the same launch.
+// Specialisation SLOTS = 0 (no record has a second slot: P0 with twin-free rules),
 // 1 (second slots), 2 (second slots whose coefficient equals the first one in
 // every record — the P1 edge-midpoint rule — so c*rinv is formed once).
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "gk_internal.hpp"
 #include "gk_math.cuh"
@@ -79,7 +82,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <bool HELM, bool MASK, int SLOTS>
+template <bool HELM, int SLOTS>
 __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   const int l0 = d1.x, nu = d1.y, r0 = d1.z, nrec = d1.w;
   const int xs0 = d2.x, nxs = d2.y;
   const uint32_t zero_rows = (uint32_t)d2.z;
+  const bool masked = d2.w != 0;
 
   // stage with cp.async (no register staging): group 0 = the records the pair
   // loop needs now; group 1 = the x support lists and dof maps the gather
@@ -156,32 +160,39 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
       *h = v;
     }
   };
-  int r = 0;
-  for (; r + kRecUnroll <= nrec; r += kRecUnroll) {
-    // the whole group's records into registers first (3 LDS.128 each): the H
-    // stores in fold() would otherwise force re-loads of every field
-    YRec rr[kRecUnroll];
+  auto pair_loop = [&](auto mask_tag) {
+    constexpr bool MASK = decltype(mask_tag)::value;
+    int r = 0;
+    for (; r + kRecUnroll <= nrec; r += kRecUnroll) {
+      // the whole group's records into registers first (3 LDS.128 each): the H
+      // stores in fold() would otherwise force re-loads of every field
+      YRec rr[kRecUnroll];
 #pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) rr[k] = load_rec(&S.rec[r + k]);
-    double dx[kRecUnroll], dy[kRecUnroll], dz[kRecUnroll];
+      for (int k = 0; k < kRecUnroll; ++k) rr[k] = load_rec(&S.rec[r + k]);
+      double dx[kRecUnroll], dy[kRecUnroll], dz[kRecUnroll];
 #pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) {
-      dx[k] = ux - rr[k].x;
-      dy[k] = uy - rr[k].y;
-      dz[k] = uz - rr[k].z;
+      for (int k = 0; k < kRecUnroll; ++k) {
+        dx[k] = ux - rr[k].x;
+        dy[k] = uy - rr[k].y;
+        dz[k] = uz - rr[k].z;
+      }
+      double cs[kRecUnroll], sn[kRecUnroll], rinv[kRecUnroll];
+      green_parts_n<HELM, kRecUnroll, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+#pragma unroll
+      for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], cs[k], sn[k], rinv[k]);
     }
-    double cs[kRecUnroll], sn[kRecUnroll], rinv[kRecUnroll];
-    green_parts_n<HELM, kRecUnroll, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
-#pragma unroll
-    for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], cs[k], sn[k], rinv[k]);
-  }
-  for (; r < nrec; ++r) {
-    const YRec p = load_rec(&S.rec[r]);
-    double dx[1] = {ux - p.x}, dy[1] = {uy - p.y}, dz[1] = {uz - p.z};
-    double cs[1], sn[1], rinv[1];
-    green_parts_n<HELM, 1, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
-    fold(p, cs[0], sn[0], rinv[0]);
-  }
+    for (; r < nrec; ++r) {
+      const YRec p = load_rec(&S.rec[r]);
+      double dx[1] = {ux - p.x}, dy[1] = {uy - p.y}, dz[1] = {uz - p.z};
+      double cs[1], sn[1], rinv[1];
+      green_parts_n<HELM, 1, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+      fold(p, cs[0], sn[0], rinv[0]);
+    }
+  };
+  if (masked)  // uniform per CTA
+    pair_loop(std::true_type{});
+  else
+    pair_loop(std::false_type{});
   if (nrec > 0) flush();
   cp_async_wait<0>();
   __syncthreads();
@@ -225,39 +236,38 @@ __global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
   }
 }
 
-template <bool HELM, bool MASK, int SLOTS>
+template <bool HELM, int SLOTS>
 void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
   const size_t smem = sizeof(AsmSmem);
   static bool configured = false;  // one flag per instantiation
   if (!configured) {
-    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, MASK, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem),
+    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
-  k_assemble<HELM, MASK, SLOTS><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+  k_assemble<HELM, SLOTS><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
 }
 
-template <bool HELM, bool MASK>
+template <bool HELM>
 void launch_slots(const AsmArgs& a, int64_t ntiles, int slots, cudaStream_t s) {
   if (slots == 0)
-    launch_one<HELM, MASK, 0>(a, ntiles, s);
+    launch_one<HELM, 0>(a, ntiles, s);
   else if (slots == 1)
-    launch_one<HELM, MASK, 1>(a, ntiles, s);
+    launch_one<HELM, 1>(a, ntiles, s);
   else
-    launch_one<HELM, MASK, 2>(a, ntiles, s);
+    launch_one<HELM, 2>(a, ntiles, s);
 }
 
 }  // namespace
 
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, int slots, void* stream) {
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream) {
   if (ntiles <= 0) return;
   if (ntiles > INT32_MAX) throw std::invalid_argument("bem_dense: too many tiles");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (helmholtz)
-    mask ? launch_slots<true, true>(a, ntiles, slots, s) : launch_slots<true, false>(a, ntiles, slots, s);
+    launch_slots<true>(a, ntiles, slots, s);
   else
-    mask ? launch_slots<false, true>(a, ntiles, slots, s) : launch_slots<false, false>(a, ntiles, slots, s);
+    launch_slots<false>(a, ntiles, slots, s);
   cuda_check(cudaGetLastError(), "k_assemble launch");
 }
 

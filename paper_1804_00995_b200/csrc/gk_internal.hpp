@@ -179,7 +179,7 @@ struct TileDesc {  // everything a k_assemble CTA needs to stage its tile
   int32_t r0, nrec;    // y records
   int32_t xs0, nxs;    // x support entries
   uint32_t zero_rows;  // H rows without a run (zero-filled)
-  int32_t pad;
+  int32_t masked;      // 1: the tile may hold a coincident pair (distance mask on)
 };
 static_assert(sizeof(TileDesc) == 48, "TileDesc is loaded as three 16-byte vectors");
 
@@ -201,7 +201,7 @@ struct AsmArgs {
   int32_t symmetric;
 };
 // slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0
-void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, bool mask, int slots, void* stream);
+void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream);
 
 // ---- matvec ---------------------------------------------------------------------------
 void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,
