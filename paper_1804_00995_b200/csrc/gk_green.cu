@@ -62,20 +62,69 @@ __global__ void __launch_bounds__(kGThreads) k_green64(const GreenArgs a, const 
       sq[s] = Q[b + s];
     }
     __syncthreads();
-    for (int s = 0; s < n; ++s) {
-      const double px = sx[s], py = sy[s], pz = sz[s];
-      const double2 q = sq[s];
-      const c64 g0 = green<HELM>(x0 - px, y0 - py, z0 - pz, eps2, kappa);
-      const c64 g1 = green<HELM>(x1 - px, y1 - py, z1 - pz, eps2, kappa);
-      r0 = fma(g0.re, q.x, r0);
-      r0 = fma(-g0.im, q.y, r0);
-      i0 = fma(g0.re, q.y, i0);
-      i0 = fma(g0.im, q.x, i0);
-      r1 = fma(g1.re, q.x, r1);
-      r1 = fma(-g1.im, q.y, r1);
-      i1 = fma(g1.re, q.y, i1);
-      i1 = fma(g1.im, q.x, i1);
+    // two targets x two sources per step: four independent pair evaluations in
+    // lockstep (green_parts_n), each folded as (cs + i sn) * (q / r) — the
+    // charge times 1/r is formed once (two DMUL) and the complex product
+    // accumulates with four DFMA; sources stay in ascending order per target
+    double ra[2] = {r0, r1}, ia[2] = {i0, i1};
+    const double tx[2] = {x0, x1}, ty[2] = {y0, y1}, tz[2] = {z0, z1};
+    auto fold = [&](int k, double cs, double sn, double rinv, double2 q) {
+      const double wr = q.x * rinv, wi = q.y * rinv;
+      ra[k] = fma(cs, wr, fma(-sn, wi, ra[k]));
+      ia[k] = fma(cs, wi, fma(sn, wr, ia[k]));
+    };
+    int s = 0;
+    for (; s + 2 <= n; s += 2) {
+      double dx[4], dy[4], dz[4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          dx[2 * u + k] = tx[k] - sx[s + u];
+          dy[2 * u + k] = ty[k] - sy[s + u];
+          dz[2 * u + k] = tz[k] - sz[s + u];
+        }
+      double cs[4], sn[4], rinv[4];
+      green_parts_n<HELM, 4, true>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+      const double2 q0 = sq[s], q1 = sq[s + 1];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (HELM) {
+          fold(k, cs[k], sn[k], rinv[k], q0);
+          fold(k, cs[2 + k], sn[2 + k], rinv[2 + k], q1);
+        } else {
+          ra[k] = fma(rinv[k], q0.x, ra[k]);
+          ia[k] = fma(rinv[k], q0.y, ia[k]);
+          ra[k] = fma(rinv[2 + k], q1.x, ra[k]);
+          ia[k] = fma(rinv[2 + k], q1.y, ia[k]);
+        }
+      }
     }
+    for (; s < n; ++s) {
+      double dx[2], dy[2], dz[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        dx[k] = tx[k] - sx[s];
+        dy[k] = ty[k] - sy[s];
+        dz[k] = tz[k] - sz[s];
+      }
+      double cs[2], sn[2], rinv[2];
+      green_parts_n<HELM, 2, true>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+      const double2 q = sq[s];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (HELM) {
+          fold(k, cs[k], sn[k], rinv[k], q);
+        } else {
+          ra[k] = fma(rinv[k], q.x, ra[k]);
+          ia[k] = fma(rinv[k], q.y, ia[k]);
+        }
+      }
+    }
+    r0 = ra[0];
+    r1 = ra[1];
+    i0 = ia[0];
+    i1 = ia[1];
   }
   if (v0) Y[t0] = make_double2(r0, i0);
   if (v1) Y[t0 + 1] = make_double2(r1, i1);
