@@ -85,6 +85,9 @@ struct gk_green_plan {
   bool helmholtz = false;
   double eps = 0.0, k = 0.0;
   DevBuf tx, ty, tz, txf, tyf, tzf, sx, sy, sz, sxf, syf, szf, src_start, src_list, tgt_loc, Q, Y;
+  bool symmetric = false;  // targets == sources: fp64 path evaluates each unordered pair once
+  int sym_group = 0;
+  DevBuf sym_R, sym_C;     // per-group row / column partials
 };
 
 namespace {
@@ -419,6 +422,23 @@ gk_status gk_green_plan_create(int64_t nt, const double* tx, const double* ty, c
     P->tgt_loc.upload(tloc);
     P->Q.alloc(sizeof(gk_cplx) * std::max<int64_t>(1, P->ns));
     P->Y.alloc(sizeof(gk_cplx) * std::max<int64_t>(1, P->nt));
+    // identical target and source sets (after the same twin merge): symmetric
+    // fp64 path with ~512 MB of per-group partials (GK_GREEN_SYM=0 disables)
+    const char* sym_env = std::getenv("GK_GREEN_SYM");
+    const bool same = nt == ns && nt > 0 && std::memcmp(tx, sx, sizeof(double) * nt) == 0 &&
+                      std::memcmp(ty, sy, sizeof(double) * nt) == 0 && std::memcmp(tz, sz, sizeof(double) * nt) == 0;
+    if (same && !(sym_env && std::atoi(sym_env) == 0)) {
+      const int64_t B = green_sym_block();
+      const int64_t nb = (P->nt + B - 1) / B;
+      const int64_t per_row = nb * B * (int64_t)sizeof(gk_cplx);
+      const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nb, (512ll << 20) / std::max<int64_t>(1, per_row)));
+      if (nb * G < INT32_MAX) {
+        P->symmetric = true;
+        P->sym_group = (int)G;
+        P->sym_R.alloc((size_t)(per_row * G));
+        P->sym_C.alloc((size_t)(per_row * G));
+      }
+    }
     *out = P.release();
   });
 }
@@ -454,6 +474,9 @@ gk_status gk_green_matvec(gk_green_plan* P, const gk_cplx* q, gk_cplx* y, int32_
     a.kappa = 2.0 * P->k / M_PI;
     a.eps2f = (float)a.eps2;
     a.kappaf = (float)a.kappa;
+    a.sym_R = P->symmetric ? P->sym_R.p : nullptr;
+    a.sym_C = P->symmetric ? P->sym_C.p : nullptr;
+    a.sym_group = P->sym_group;
     launch_green(a, q, P->Q.p, P->Y.p, y, precision, P->helmholtz, stream);
   });
 }

@@ -13,6 +13,8 @@
 // per-tile fp32 partial sum folded into an fp64 accumulator.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gk_internal.hpp"
 #include "gk_math.cuh"
 
@@ -195,7 +197,152 @@ __global__ void __launch_bounds__(kGThreads) k_green32(const GreenArgs a, const 
   if (v0) Y[t0] = make_double2(R0, I0);
   if (v1) Y[t0 + 1] = make_double2(R1, I1);
 }
+// ---- symmetric fp64 matvec (targets == sources): each unordered block pair
+// once.  G is symmetric, so tile (I, J), J > I, yields both the row sums
+// y_I += G_IJ q_J and the column sums y_J += G_IJ^T q_I from one set of pair
+// evaluations.  Inside a warp the column accumulators rotate through the
+// lanes (one shuffle per pair and component pair): lane l evaluates its two
+// targets against source (l + j) mod 32 at step j and passes the running
+// column sum to lane l - 1, so after 32 steps every lane holds the complete
+// warp sum for one source — no atomics, fixed order.  Tiles write row and
+// column partials; a second kernel adds them into y in a fixed order.
+constexpr int kSB = 256;  // locations per symmetric block (4 warps x 64 targets)
+
+__device__ __forceinline__ void tile_of(int tile, int I0, int nb, int& I, int& J) {
+  int off = 0;
+  I = I0;
+  while (off + (nb - I) <= tile) {
+    off += nb - I;
+    ++I;
+  }
+  J = I + (tile - off);
+}
+
+template <bool HELM>
+__global__ void __launch_bounds__(128) k_green64_sym(const GreenArgs a, const double2* __restrict__ Q, int I0,
+                                                    int nb, double2* __restrict__ R, double2* __restrict__ C) {
+  __shared__ double sx[kSB], sy[kSB], sz[kSB];
+  __shared__ double2 sq[kSB];
+  __shared__ double2 colp[4][32];
+  int I, J;
+  tile_of(blockIdx.x, I0, nb, I, J);
+  const long long U = a.nt;
+  for (int e = threadIdx.x; e < kSB; e += 128) {
+    const long long v = (long long)J * kSB + e;
+    const bool ok = v < U;
+    // padding (last block only): zero charge at a distant point; kr stays far
+    // inside the quarter-turn reduction's range so every product is finite and
+    // the zero charges contribute exactly 0 to real rows and columns
+    sx[e] = ok ? a.tx[v] : 1e6;
+    sy[e] = ok ? a.ty[v] : 0.0;
+    sz[e] = ok ? a.tz[v] : 0.0;
+    sq[e] = ok ? Q[v] : make_double2(0.0, 0.0);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double tx[2], ty[2], tz[2];
+  double2 tq[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const long long v = (long long)I * kSB + w * 64 + 32 * k + lane;
+    const bool ok = v < U;
+    tx[k] = ok ? a.tx[v] : -1e6;
+    ty[k] = ok ? a.ty[v] : 0.0;
+    tz[k] = ok ? a.tz[v] : 0.0;
+    tq[k] = ok ? Q[v] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const double eps2 = a.eps2, kappa = a.kappa;
+  double ra[2] = {0.0, 0.0}, ia[2] = {0.0, 0.0};
+  const int src_lane = (lane + 1) & 31;
+  for (int c = 0; c < kSB / 32; ++c) {
+    double cr = 0.0, ci = 0.0;  // column sum of source c*32 + ((lane + j) & 31) at step j
+    for (int j = 0; j < 32; j += 2) {
+      // steps j and j+1 evaluated in lockstep (2 targets x 2 sources)
+      int sidx[2];
+      double dx[4], dy[4], dz[4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        sidx[u] = c * 32 + ((lane + j + u) & 31);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          dx[2 * u + k] = tx[k] - sx[sidx[u]];
+          dy[2 * u + k] = ty[k] - sy[sidx[u]];
+          dz[2 * u + k] = tz[k] - sz[sidx[u]];
+        }
+      }
+      double cs[4], sn[4], rinv[4];
+      green_parts_n<HELM, 4, true>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double2 q = sq[sidx[u]];
+        double pr = 0.0, pi = 0.0;  // this step's column contribution (both targets)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const double g = rinv[2 * u + k];
+          if (HELM) {
+            const double c_ = cs[2 * u + k], s_ = sn[2 * u + k];
+            const double wr = q.x * g, wi = q.y * g;  // row: G q_s
+            ra[k] = fma(c_, wr, fma(-s_, wi, ra[k]));
+            ia[k] = fma(c_, wi, fma(s_, wr, ia[k]));
+            const double vr = tq[k].x * g, vi = tq[k].y * g;  // column: G q_t
+            pr = fma(c_, vr, fma(-s_, vi, pr));
+            pi = fma(c_, vi, fma(s_, vr, pi));
+          } else {
+            ra[k] = fma(g, q.x, ra[k]);
+            ia[k] = fma(g, q.y, ia[k]);
+            pr = fma(g, tq[k].x, pr);
+            pi = fma(g, tq[k].y, pi);
+          }
+        }
+        cr += pr;
+        ci += pi;
+        cr = __shfl_sync(0xffffffffu, cr, src_lane);
+        ci = __shfl_sync(0xffffffffu, ci, src_lane);
+      }
+    }
+    // lane l now holds the warp's column sum of source c*32 + l
+    colp[w][lane] = make_double2(cr, ci);
+    __syncthreads();
+    if (w == 0) {
+      const double2 s0 = colp[0][lane], s1 = colp[1][lane], s2 = colp[2][lane], s3 = colp[3][lane];
+      C[(long long)blockIdx.x * kSB + c * 32 + lane] =
+          make_double2(((s0.x + s1.x) + s2.x) + s3.x, ((s0.y + s1.y) + s2.y) + s3.y);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) R[(long long)blockIdx.x * kSB + w * 64 + 32 * k + lane] = make_double2(ra[k], ia[k]);
+}
+
+// y[v] += sum_{J >= I} R(I, J)[e]  (rows of the group)  +  sum_{I < J} C(I, J)[e]
+// (columns from the group's rows), v = J*kSB + e; fixed order.
+__global__ void k_green_sym_reduce(const double2* __restrict__ R, const double2* __restrict__ C, int I0, int I1,
+                                   int nb, long long U, double2* __restrict__ Y, int first) {
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= U) return;
+  const int b = (int)(v / kSB), e = (int)(v - (long long)b * kSB);
+  double re = first ? 0.0 : Y[v].x, im = first ? 0.0 : Y[v].y;
+  int off = 0;  // tile index of (I, I) within the group
+  for (int I = I0; I < I1; ++I) {
+    if (I == b) {
+      for (int J = I; J < nb; ++J) {
+        const double2 r = R[(long long)(off + J - I) * kSB + e];
+        re += r.x;
+        im += r.y;
+      }
+    } else if (I < b) {
+      const double2 c = C[(long long)(off + b - I) * kSB + e];
+      re += c.x;
+      im += c.y;
+    }
+    off += nb - I;
+  }
+  Y[v] = make_double2(re, im);
+}
+
 }  // namespace
+
+int green_sym_block() { return kSB; }
 
 void launch_green(const GreenArgs& a, const void* q, void* Q, void* Yu, void* y, int precision, bool helmholtz,
                   void* stream) {
@@ -210,7 +357,21 @@ void launch_green(const GreenArgs& a, const void* q, void* Q, void* Yu, void* y,
   if (grid > 0) {
     const double2* Qc = static_cast<const double2*>(Q);
     double2* Yc = static_cast<double2*>(Yu);
-    if (precision == GK_FP32) {
+    if (precision != GK_FP32 && a.sym_R) {
+      const int nb = (int)((a.nt + kSB - 1) / kSB);
+      const int G = a.sym_group;
+      for (int I0 = 0; I0 < nb; I0 += G) {
+        const int I1 = std::min(nb, I0 + G);
+        const long long tiles = (long long)(I1 - I0) * nb - ((long long)I1 * (I1 - 1) / 2 - (long long)I0 * (I0 - 1) / 2);
+        double2* Rb = static_cast<double2*>(a.sym_R);
+        double2* Cb = static_cast<double2*>(a.sym_C);
+        if (helmholtz)
+          k_green64_sym<true><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+        else
+          k_green64_sym<false><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+        k_green_sym_reduce<<<(unsigned)((a.nt + 255) / 256), 256, 0, s>>>(Rb, Cb, I0, I1, nb, a.nt, Yc, I0 == 0);
+      }
+    } else if (precision == GK_FP32) {
       if (helmholtz)
         k_green32<true><<<grid, kGThreads, 0, s>>>(a, Qc, Yc);
       else

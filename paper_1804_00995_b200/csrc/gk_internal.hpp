@@ -230,7 +230,11 @@ struct GreenArgs {
   double kappa;
   float eps2f;
   float kappaf;
+  void* sym_R;    // targets == sources: per-group row / column partials (null: general path)
+  void* sym_C;
+  int32_t sym_group;  // target blocks per group
 };
+int green_sym_block();  // locations per block of the symmetric path
 void launch_green(const GreenArgs& a, const void* q, void* Q, void* Y, void* y, int precision,
                   bool helmholtz, void* stream);
 
