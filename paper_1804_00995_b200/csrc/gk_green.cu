@@ -314,6 +314,87 @@ __global__ void __launch_bounds__(128) k_green64_sym(const GreenArgs a, const do
   for (int k = 0; k < 2; ++k) R[(long long)blockIdx.x * kSB + w * 64 + 32 * k + lane] = make_double2(ra[k], ia[k]);
 }
 
+// fp32 variant of the symmetric tile: fp32 pair math and fp32 sums inside the
+// tile (256 sources per row sum, 64 targets per rotating column sum), written
+// as fp64 partials and added across tiles in fp64 by k_green_sym_reduce.
+template <bool HELM>
+__global__ void __launch_bounds__(128) k_green32_sym(const GreenArgs a, const double2* __restrict__ Q, int I0,
+                                                    int nb, double2* __restrict__ R, double2* __restrict__ C) {
+  __shared__ float sx[kSB], sy[kSB], sz[kSB];
+  __shared__ float2 sq[kSB];
+  __shared__ float2 colp[4][32];
+  int I, J;
+  tile_of(blockIdx.x, I0, nb, I, J);
+  const long long U = a.nt;
+  for (int e = threadIdx.x; e < kSB; e += 128) {
+    const long long v = (long long)J * kSB + e;
+    const bool ok = v < U;
+    sx[e] = ok ? a.txf[v] : 1e6f;  // padding as in the fp64 tile
+    sy[e] = ok ? a.tyf[v] : 0.f;
+    sz[e] = ok ? a.tzf[v] : 0.f;
+    const double2 qq = ok ? Q[v] : make_double2(0.0, 0.0);
+    sq[e] = make_float2((float)qq.x, (float)qq.y);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float tx[2], ty[2], tz[2];
+  float2 tq[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const long long v = (long long)I * kSB + w * 64 + 32 * k + lane;
+    const bool ok = v < U;
+    tx[k] = ok ? a.txf[v] : -1e6f;
+    ty[k] = ok ? a.tyf[v] : 0.f;
+    tz[k] = ok ? a.tzf[v] : 0.f;
+    const double2 qq = ok ? Q[v] : make_double2(0.0, 0.0);
+    tq[k] = make_float2((float)qq.x, (float)qq.y);
+  }
+  __syncthreads();
+  const float eps2 = a.eps2f, kappa = a.kappaf;
+  float ra[2] = {0.f, 0.f}, ia[2] = {0.f, 0.f};
+  const int src_lane = (lane + 1) & 31;
+  for (int c = 0; c < kSB / 32; ++c) {
+    float cr = 0.f, ci = 0.f;
+    for (int j = 0; j < 32; j += 2) {
+      float2 g[4];
+      int sidx[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        sidx[u] = c * 32 + ((lane + j + u) & 31);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          g[2 * u + k] = green_f<HELM>(tx[k] - sx[sidx[u]], ty[k] - sy[sidx[u]], tz[k] - sz[sidx[u]], eps2, kappa);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float2 q = sq[sidx[u]];
+        float pr = 0.f, pi = 0.f;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float2 gg = g[2 * u + k];
+          ra[k] = fmaf(gg.x, q.x, fmaf(-gg.y, q.y, ra[k]));
+          ia[k] = fmaf(gg.x, q.y, fmaf(gg.y, q.x, ia[k]));
+          pr = fmaf(gg.x, tq[k].x, fmaf(-gg.y, tq[k].y, pr));
+          pi = fmaf(gg.x, tq[k].y, fmaf(gg.y, tq[k].x, pi));
+        }
+        cr += pr;
+        ci += pi;
+        cr = __shfl_sync(0xffffffffu, cr, src_lane);
+        ci = __shfl_sync(0xffffffffu, ci, src_lane);
+      }
+    }
+    colp[w][lane] = make_float2(cr, ci);
+    __syncthreads();
+    if (w == 0) {
+      const float2 s0 = colp[0][lane], s1 = colp[1][lane], s2 = colp[2][lane], s3 = colp[3][lane];
+      C[(long long)blockIdx.x * kSB + c * 32 + lane] =
+          make_double2(((double)s0.x + s1.x) + s2.x + s3.x, ((double)s0.y + s1.y) + s2.y + s3.y);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) R[(long long)blockIdx.x * kSB + w * 64 + 32 * k + lane] = make_double2(ra[k], ia[k]);
+}
+
 // y[v] += sum_{J >= I} R(I, J)[e]  (rows of the group)  +  sum_{I < J} C(I, J)[e]
 // (columns from the group's rows), v = J*kSB + e; fixed order.
 __global__ void k_green_sym_reduce(const double2* __restrict__ R, const double2* __restrict__ C, int I0, int I1,
@@ -357,7 +438,7 @@ void launch_green(const GreenArgs& a, const void* q, void* Q, void* Yu, void* y,
   if (grid > 0) {
     const double2* Qc = static_cast<const double2*>(Q);
     double2* Yc = static_cast<double2*>(Yu);
-    if (precision != GK_FP32 && a.sym_R) {
+    if (a.sym_R) {
       const int nb = (int)((a.nt + kSB - 1) / kSB);
       const int G = a.sym_group;
       for (int I0 = 0; I0 < nb; I0 += G) {
@@ -365,10 +446,17 @@ void launch_green(const GreenArgs& a, const void* q, void* Q, void* Yu, void* y,
         const long long tiles = (long long)(I1 - I0) * nb - ((long long)I1 * (I1 - 1) / 2 - (long long)I0 * (I0 - 1) / 2);
         double2* Rb = static_cast<double2*>(a.sym_R);
         double2* Cb = static_cast<double2*>(a.sym_C);
-        if (helmholtz)
-          k_green64_sym<true><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
-        else
-          k_green64_sym<false><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+        if (precision == GK_FP32) {
+          if (helmholtz)
+            k_green32_sym<true><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+          else
+            k_green32_sym<false><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+        } else {
+          if (helmholtz)
+            k_green64_sym<true><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+          else
+            k_green64_sym<false><<<(unsigned)tiles, 128, 0, s>>>(a, Qc, I0, nb, Rb, Cb);
+        }
         k_green_sym_reduce<<<(unsigned)((a.nt + 255) / 256), 256, 0, s>>>(Rb, Cb, I0, I1, nb, a.nt, Yc, I0 == 0);
       }
     } else if (precision == GK_FP32) {
