@@ -167,6 +167,38 @@ def test_config3_p0_rule6_perturbed_sampled_rows(galerk, oracle):
     assert rel_fro(got, ref) <= TOL
 
 
+def test_config4_p0_l6_chunk_rows_and_matvecs(galerk, oracle):
+    """BASELINE cfg 4 at full size (81920^2 complex128 = 107 GB in HBM): the
+    complete rows of 8 uniformly spaced 1024-point x chunks against
+    the oracle, then the 10 stored-matrix matvecs (seed 3) on those rows."""
+    torch = _torch()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120 * 2 ** 30:
+        pytest.skip("needs ~110 GB of free device memory")
+    m, dom, sp, hbar = sphere_problem(galerk, 40962, 3, "P0")
+    k = 2 * math.pi / (10 * hbar)
+    opts = galerk.BemOptions()
+    opts.memory_cap_bytes = 2 * 10 ** 11
+    n = 81920
+    plan, info, A, lda = assemble_device(galerk, dom, dom, sp, galerk.green_kernel("[exp(ikr)/r]", k), sp, opts)
+    assert info["pairs_reference"] == 245760 ** 2 and info["x_locations"] == 122880
+    M = 245760
+    rows = sorted({p // 3 for c in range(8) for p in range(c * (M // 8), c * (M // 8) + 1024)})
+    ref = oracle.bem_dense(m.vertices, m.elements, 3, P0, m.vertices, m.elements, 3, P0, "[exp(ikr)/r]", k,
+                           rows=rows, threads=16, cap=1e12)
+    got = A.view(n, lda)[:, rows].cpu().numpy().T
+    assert rel_fro(got, ref) <= TOL
+    X = galerk.complex_normal(3, 10 * n).reshape(10, n)  # vectors i = 0..9 drawn consecutively
+    yd = torch.empty(n, dtype=torch.complex128, device="cuda")
+    for i in range(10):
+        xd = torch.tensor(X[i], device="cuda")
+        galerk.matvec(A.data_ptr(), n, n, lda, xd.data_ptr(), yd.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert rel_fro(yd.cpu().numpy()[rows], ref @ X[i]) <= TOL
+    del A
+    torch.cuda.empty_cache()
+
+
 def test_matvec_random_shapes(galerk):
     torch = _torch()
     rng = np.random.default_rng(5)
