@@ -81,3 +81,25 @@ def test_green_matvec_symmetric_path(galerk, oracle, monkeypatch, name, npts):
     ids = sorted(set(np.random.default_rng(2).choice(len(pts), 48, replace=False).tolist()) | {0, len(pts) - 1})
     ref = np.array(oracle.green_matvec(name, kk, pts, pts, q, plan_g.info()["eps"], ids, 8))
     assert rel_fro(ysn[ids], ref) <= 1e-10
+
+
+def test_config5_full_size_sampled_targets(galerk, oracle):
+    """BASELINE cfg 5 at full size: L7 sphere, 983,040 Gauss points as targets
+    and sources (symmetric path, 1,920 blocks in groups), charges = weight x
+    complex N(0,1) from seed 4; sampled targets vs the oracle (fp64 1e-10,
+    fp32 within FP32_TOL)."""
+    torch, m, pts, q, k = _setup(galerk, 163842)
+    assert len(pts) == 983040
+    plan = galerk.GreenPlan(pts, pts, galerk.green_kernel("[exp(ikr)/r]", k))
+    info = plan.info()
+    assert info["unique_targets"] == 491520
+    qd = torch.tensor(q, device="cuda")
+    y64 = torch.empty(len(pts), dtype=torch.complex128, device="cuda")
+    y32 = torch.empty_like(y64)
+    plan.matvec(qd.data_ptr(), y64.data_ptr(), galerk.FP64, 0)
+    plan.matvec(qd.data_ptr(), y32.data_ptr(), galerk.FP32, 0)
+    torch.cuda.synchronize()
+    ids = sorted(set(np.random.default_rng(5).choice(len(pts), 24, replace=False).tolist()) | {0, len(pts) - 1})
+    ref = np.array(oracle.green_matvec("[exp(ikr)/r]", k, pts, pts, q, info["eps"], ids, 16))
+    assert rel_fro(y64.cpu().numpy()[ids], ref) <= 1e-10
+    assert rel_fro(y32.cpu().numpy()[ids], ref) <= FP32_TOL
