@@ -189,19 +189,6 @@ __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3
   }
 }
 
-// barycentric corners of sub-cell s (assembly.cpp:587-594):
-// sub[0]=(c0,m01,m20) sub[1]=(c1,m12,m01) sub[2]=(c2,m20,m12) sub[3]=(m01,m12,m20)
-__device__ __forceinline__ void sub_corners(const double* c, int s, double o[9]) {
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const double c0 = c[k], c1 = c[3 + k], c2 = c[6 + k];
-    const double m01 = 0.5 * (c0 + c1), m12 = 0.5 * (c1 + c2), m20 = 0.5 * (c2 + c0);
-    o[k] = s == 0 ? c0 : s == 1 ? c1 : s == 2 ? c2 : m01;
-    o[3 + k] = s == 0 ? m01 : s == 1 ? m12 : s == 2 ? m20 : m12;
-    o[6 + k] = s == 0 ? m20 : s == 1 ? m01 : s == 2 ? m12 : m20;
-  }
-}
-
 template <int NT, int NTR>
 __device__ __forceinline__ void exact_values(const YTri& T, double newton, V3 moment, V3 rho, double d[NTR]) {
   if (NTR == 1) {
