@@ -35,11 +35,12 @@ HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json i
 #  - canonical probe: the reference formula kernels.cpp:94-114 with
 #    libdevice sqrt/sin/cos/division + one complex x real accumulate:
 #    43 DFMA + 13 DMUL + 7 DADD = 106 flops/pair (DFMA = 2 flops);
-#  - production formula (gk_math.cuh green_n + accumulate):
-#    20 DFMA + 8 DMUL + 6 DADD = 54 flops/pair.
-# Laplace ("[1/r]", cfg 1): 11 FP64 instructions + accumulate = 23 flops.
+#  - production formula: SASS count of k_assemble's pair loop (cuobjdump, P1
+#    cfg 2, y-side accumulation included): 24 DFMA + 7 DMUL + 4 DADD = 59
+#    flops/pair; Laplace: 5 DFMA + 4 DMUL + 5 DADD = 19.
+# Laplace ("[1/r]", cfg 1) probe: 11 FP64 instructions + accumulate = 23 flops.
 F_PAIR_PROBE_FLOPS = {True: 106.0, False: 23.0}
-F_PAIR_PROD_FLOPS = {True: 54.0, False: 23.0}
+F_PAIR_PROD_FLOPS = {True: 59.0, False: 19.0}
 
 
 def parse():
@@ -425,6 +426,8 @@ def reference_arm(args, rank, world, dist):
 
 
 def bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k, hbar):
+    """cfg 5: matrix-free Green matvec (K5).  A step is one fp64 matvec of the
+    983,040 Gauss points against themselves; the fp32 variant is timed beside it."""
     pts, w, _ = g.quadrature(dom)
     q = np.asarray(w) * g.complex_normal(spec["seed"], len(w))
     plan = g.GreenPlan(pts, pts, kern)
@@ -432,23 +435,61 @@ def bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k
     qd = torch.tensor(q, device=dev)
     y = torch.empty(len(w), dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
+    fp64_peak_gflops = g.diag_fp64_peak(20000, stream.cuda_stream)
     res = {}
+    clocks = None
     for prec, label in ((g.FP64, "fp64"), (g.FP32, "fp32")):
-        plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+        for _ in range(max(3, args.warmup)):
+            plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / args.steps
-        res[label] = {"ms": ms, "pairs_per_s": len(w) ** 2 / (ms * 1e-3),
-                      "unique_pairs_per_s": info["unique_targets"] * info["unique_sources"] / (ms * 1e-3)}
+        with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, dev)
+        if label == "fp64":
+            clocks = clk.summary()
+        U = info["unique_targets"]
+        res[label] = {"ms": ms, "pairs_per_s": world * len(w) ** 2 / (ms * 1e-3),
+                      "unique_pairs_per_s": world * U * U / (ms * 1e-3)}
     if rank == 0:
-        print(json.dumps({"metric": "matrix-free Green matvec pair evals/s (reference-equivalent)",
-                          "value": res["fp64"]["pairs_per_s"], "unit": "pairs/s", "n_gpus": world,
-                          "steps": args.steps, "detail": res, "info": info, "higher_is_better": True}))
+        U = info["unique_targets"]
+        helm = k != 0.0
+        # evaluated pairs: the symmetric path evaluates each unordered unique pair once
+        evaluated = U * (U + 1) / 2 if info.get("symmetric") else U * U
+        t = res["fp64"]["ms"] * 1e-3
+        peak = fp64_peak_gflops / 1e3
+        achieved = evaluated * F_PAIR_PROBE_FLOPS[helm] / t / 1e12
+        out = {
+            "metric": "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)",
+            "value": res["fp64"]["pairs_per_s"], "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["fp64"]["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 (complex128); fp32 variant in detail",
+            "data": "synthetic (seeded icosphere L7 Gauss nodes, SplitMix64/Box-Muller charges)",
+            "config": {"workload": "cfg5: matrix-free Helmholtz Green matvec, 983040 targets = sources (icosphere L7, "
+                                   "3-pt), self-interaction masked", "M": len(w), "unique": U, "k": k, "hbar": hbar,
+                       "parallelism": f"replicas x{world}",
+                       "l2": "sources re-streamed from L2 per tile; no matrix (matrix-free)"},
+            "detail": res, "info": info,
+            "roofline": {"bound": "fp64", "kernel": "k_green64_sym (K5)", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": "DFMA microbenchmark measured in this run",
+                         "work": "evaluated unique pairs (%s) x %.0f flops/pair (probe F_pair)"
+                                 % ("symmetric: U(U+1)/2" if info.get("symmetric") else "U^2",
+                                    F_PAIR_PROBE_FLOPS[helm])},
+            "clocks": clocks,
+            "gpu_launches": plan.launches(g.FP64) * args.steps,
+        }
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

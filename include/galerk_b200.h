@@ -160,6 +160,10 @@ gk_status gk_green_matvec(gk_green_plan* plan, const gk_cplx* q, gk_cplx* y, int
                           gk_stream stream);
 gk_status gk_green_plan_get_info(const gk_green_plan* plan, int64_t* unique_targets,
                                  int64_t* unique_sources, double* eps);
+/* 1 if targets == sources and the symmetric path (each unordered pair once) is used. */
+int32_t gk_green_plan_is_symmetric(const gk_green_plan* plan);
+/* Kernel launches one gk_green_matvec issues (for launch accounting). */
+int32_t gk_green_plan_launches(const gk_green_plan* plan, int32_t precision);
 gk_status gk_green_plan_destroy(gk_green_plan* plan);
 
 /* ---- near-field singular correction (regularize) -------------------------- */

@@ -490,6 +490,21 @@ gk_status gk_green_plan_get_info(const gk_green_plan* P, int64_t* nt, int64_t* n
   });
 }
 
+int32_t gk_green_plan_is_symmetric(const gk_green_plan* P) { return P && P->symmetric ? 1 : 0; }
+
+int32_t gk_green_plan_launches(const gk_green_plan* P, int32_t precision) {
+  if (!P || P->nt_orig <= 0) return 0;
+  int32_t n = (P->ns > 0 ? 1 : 0) + 1;  // merge charges, scatter targets
+  if (P->symmetric) {
+    const int64_t B = green_sym_block(), nb = (P->nt + B - 1) / B;
+    n += 2 * (int32_t)((nb + P->sym_group - 1) / P->sym_group);  // tiles + reduce per group
+  } else if (P->nt > 0) {
+    n += 1;
+  }
+  (void)precision;
+  return n;
+}
+
 gk_status gk_green_plan_destroy(gk_green_plan* P) {
   return guard([&] { delete P; });
 }

@@ -93,11 +93,13 @@ class GreenPlan {
     throw_status(gk_green_matvec(p_, reinterpret_cast<const gk_cplx*>(q), reinterpret_cast<gk_cplx*>(y), precision,
                                  as_stream(stream)));
   }
+  int launches(int precision) const { return gk_green_plan_launches(p_, precision); }
   py::dict info() const {
     int64_t nt = 0, ns = 0;
     double eps = 0;
     throw_status(gk_green_plan_get_info(p_, &nt, &ns, &eps));
     py::dict d;
+    d["symmetric"] = gk_green_plan_is_symmetric(p_) != 0;
     d["unique_targets"] = nt;
     d["unique_sources"] = ns;
     d["eps"] = eps;
@@ -351,7 +353,8 @@ PYBIND11_MODULE(_galerk, m) {
       .def(py::init<F64, F64, const Kernel&>(), py::arg("targets"), py::arg("sources"), py::arg("kernel"))
       .def("matvec", &GreenPlan::matvec, py::arg("q"), py::arg("y"), py::arg("precision") = 0,
            py::arg("stream") = 0)
-      .def("info", &GreenPlan::info);
+      .def("info", &GreenPlan::info)
+      .def("launches", &GreenPlan::launches, py::arg("precision") = 0);
 
   py::class_<GalerkinEvaluator>(m, "GalerkinEvaluator")
       .def(py::init<const Domain&, const Domain&, const FemSpace&, const Kernel&, const FemSpace&>(),
