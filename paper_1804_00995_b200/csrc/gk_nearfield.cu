@@ -171,6 +171,7 @@ struct WarpSmem {
   double subc[4][9];  // barycentric corners of the current node's 4 sub-cells
   double acc[kMaxLoc];
   YTri tri;
+  unsigned long long leaves[7];  // accepted leaves per depth (this warp), flushed at exit
 };
 
 // kernels.cpp:151-207 with the y-triangle frame precomputed, written for ILP:
@@ -263,6 +264,8 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
   constexpr int NL = NT * NTR;
+  if (lane < 7) S.leaves[lane] = 0ull;
+  unsigned long long calls = 0;
   while (true) {
     unsigned long long p = 0;
     if (lane == 0) p = atomicAdd(a.work, 1ull);
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
 #pragma unroll
     for (int t = 0; t < NL; ++t) adapt[t] = 0.0;
     int sp = 1;
-    unsigned long long calls = 7;
+    calls += 7;  // the probe
     __syncwarp();
     // ---- accurate_adaptive (assembly.cpp:581-605), explicit DFS stack
     while (sp > 0) {
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
       if (dmax <= nd.tol || nd.depth >= 6) {
 #pragma unroll
         for (int t = 0; t < NL; ++t) adapt[t] += split[t];
-        if (lane == 0) atomicAdd(a.stats + 1 + min(nd.depth, 6), 1ull);
+        if (lane == 0) S.leaves[min(nd.depth, 6)] += 1ull;
       } else {
         if (lane < 4) {  // push children 3..0 so that sub 0 is processed first
           const int s = 3 - lane;
@@ -459,12 +462,13 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
       }
       __syncwarp();
     }
-    if (lane == 0) {
+    if (lane == 0)
       for (int t = 0; t < NL; ++t) a.local[p * kMaxLoc + t] = S.acc[t] + adapt[t];
-      atomicAdd(a.stats, calls);
-    }
     __syncwarp();
   }
+  __syncwarp();
+  if (lane == 0) atomicAdd(a.stats, calls);
+  if (lane < 7 && S.leaves[lane]) atomicAdd(a.stats + 1 + lane, S.leaves[lane]);
 }
 
 // regularize_radiation (assembly.cpp:725-745): one thread per (point, element)
