@@ -8,13 +8,16 @@
 // counter (costs range from ~500 to ~50k analytic integrals per pair; the
 // processing order does not change any result).  The recursion of
 // accurate_adaptive (:581-605) runs on an explicit per-warp stack in shared
-// memory in the same depth-first order as the reference.  Each node needs the
-// 4 sub-cells x 7 points = 28 analytic_triangle_integrals calls
-// (kernels.cpp:151-207) — one per lane — and the parent's 'whole' value is the
-// child's sub-cell value, so it is carried on the stack instead of being
-// recomputed (the reference recomputes it: ~20% of its calls).  Per-triangle
-// quantities of the y element (normal, edge frames) are computed once per pair.
+// memory, up to eight nodes per step with one lane per (node, sub-cell): each
+// lane evaluates its sub-cell's 7 analytic_triangle_integrals calls
+// (kernels.cpp:151-207) in registers, so a full step keeps all 32 lanes busy
+// (see k_nearfield_b).  The parent's 'whole' value is the child's sub-cell
+// value, so it is carried on the stack instead of being recomputed (the
+// reference recomputes it: ~20% of its calls).  Per-triangle quantities of the
+// y element (normal, edge frames) are computed once per pair.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include <algorithm>
 #include <array>
@@ -29,7 +32,6 @@ namespace gk {
 namespace {
 
 constexpr int kNfWarps = 4;       // warps per CTA
-constexpr int kStack = 32;        // DFS stack entries per warp (depth <= 6 -> <= 3*6+4)
 constexpr int kMaxLoc = 9;        // local matrix entries (P1 x P1)
 
 struct V3 {
@@ -157,23 +159,6 @@ struct NfArgs {
 __constant__ double c_r7_bary[7][3];
 __constant__ double c_r7_w[7];
 
-struct Node {
-  double corners[9];
-  double whole[kMaxLoc];
-  double frac, tol;
-  int depth;
-};
-
-struct WarpSmem {
-  Node stack[kStack];
-  double vals[32][kMaxLoc];
-  double subs[4][kMaxLoc];
-  double subc[4][9];  // barycentric corners of the current node's 4 sub-cells
-  double acc[kMaxLoc];
-  YTri tri;
-  unsigned long long leaves[7];  // accepted leaves per depth (this warp), flushed at exit
-};
-
 // kernels.cpp:151-207 with the y-triangle frame precomputed, written for ILP:
 // the three edges are independent chains (unrolled, branch-free selects for
 // the cancellation-safe log argument).  The reference sums, per edge,
@@ -258,12 +243,43 @@ __device__ __forceinline__ void exact_values(const YTri& T, double newton, V3 mo
   }
 }
 
+// ---- batched traversal (B): lane = (node k of the batch, sub-cell) -------------
+// Up to eight stack nodes are processed per iteration.  Lane 4k+s owns sub-cell
+// s of node k and evaluates its seven 7-point-rule points in q order (the
+// accurate_cell sum, assembly.cpp:562-575) in registers; the four sub values of
+// a node meet in its leader lane by shuffles (split = 0 + s0 + s1 + s2 + s3),
+// which applies the accept test (assembly.cpp:598-604) and accumulates the
+// accepted split; refused nodes' children (sub-cell corners, sub value as
+// their `whole`, depth + 1) are pushed by the four lanes that computed them.
+// The set of accepted leaves is the reference's (each decision depends only on
+// its own node); only the order in which leaves are summed differs.  Nodes are
+// compact: barycentric corners are dyadic (midpoints of midpoints) and stored
+// exactly as integers in units of 1/128; tol and frac follow from the depth.
+constexpr int kStackB = 160;  // >= 8 + 24 * 5 + 32 for batch 8, branching 4, depth 6
+constexpr int kUnit = 128;    // corner coordinates in units of 1/128 (depth <= 6)
+
+template <int NL>
+struct NodeB {
+  double whole[NL];
+  int16_t c[6];  // (b0, b1) of the three corners, units of 1/kUnit (b2 = 1 - b0 - b1)
+  int16_t depth;
+};
+
+template <int NL>
+struct WarpSmemB {
+  NodeB<NL> stack[kStackB];
+  double vals[8][kMaxLoc];  // Gauss part / probe scratch (<= 7 lanes)
+  double acc[kMaxLoc];
+  YTri tri;
+  unsigned long long leaves[7];
+};
+
 template <int NT, int NTR>
-__global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
-  extern __shared__ unsigned char smem_raw[];
-  WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x / 32];
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a) {
   constexpr int NL = NT * NTR;
+  extern __shared__ unsigned char smem_raw[];
+  WarpSmemB<NL>& S = reinterpret_cast<WarpSmemB<NL>*>(smem_raw)[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
   if (lane < 7) S.leaves[lane] = 0ull;
   unsigned long long calls = 0;
   while (true) {
@@ -283,7 +299,6 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
       const double area2 = nrm(cr);
       const double diam = fmax(fmax(nrm(T.v[1] - T.v[0]), nrm(T.v[2] - T.v[1])), nrm(T.v[0] - T.v[2]));
       if (area2 <= 1e-14 * diam * diam) atomicExch(a.stats + 8, 1ull);
-      T.n = (1.0 / area2) * cr;
       T.n = mk(cr.x / area2, cr.y / area2, cr.z / area2);
       for (int i = 0; i < 3; ++i) {
         const V3 pm = T.v[i], pp = T.v[i == 2 ? 0 : i + 1];
@@ -342,12 +357,13 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
     if (lane < NL) {  // local(i,j) -= w * acc, in x-point order
       double s = 0.0;
       for (int k = 0; k < a.gx; ++k) s += S.vals[k][lane];
-      S.acc[lane] = s;  // holds the Gauss part until the adaptive part is added
+      S.acc[lane] = s;
     }
     __syncwarp();
 
     // ---- probe = accurate_cell(whole) (lanes 0..6)
     double pv[NL];
+    double tol0;
     {
       if (lane < 7) {
         const double* b = c_r7_bary[lane];
@@ -372,95 +388,119 @@ __global__ void __launch_bounds__(32 * kNfWarps) k_nearfield(const NfArgs a) {
         pv[t] = s;
         pmax = fmax(pmax, fabs(s));
       }
+      tol0 = 1e-8 * fmax(pmax, 1e-300);
       __syncwarp();
       if (lane == 0) {
-        Node& r = S.stack[0];
-        const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-        for (int c = 0; c < 9; ++c) r.corners[c] = I[c];
+        NodeB<NL>& r = S.stack[0];
+        const int16_t I[6] = {kUnit, 0, 0, kUnit, 0, 0};
+        for (int c = 0; c < 6; ++c) r.c[c] = I[c];
         for (int t = 0; t < NL; ++t) r.whole[t] = pv[t];
-        r.frac = 1.0;
-        r.tol = 1e-8 * fmax(pmax, 1e-300);
         r.depth = 0;
       }
     }
-    double adapt[NL];
+    calls += 7;  // the probe
+    double adapt[NL];  // leader lanes: accepted splits, in acceptance order
 #pragma unroll
     for (int t = 0; t < NL; ++t) adapt[t] = 0.0;
     int sp = 1;
-    calls += 7;  // the probe
+    const int k = lane >> 2, sub = lane & 3;
     __syncwarp();
-    // ---- accurate_adaptive (assembly.cpp:581-605), explicit DFS stack
+    // ---- accurate_adaptive (assembly.cpp:581-605), batched
     while (sp > 0) {
-      --sp;
-      const Node nd = S.stack[sp];
-      __syncwarp();
-      const double frac = 0.25 * nd.frac;
-      if (lane < 3) {  // sub-cell corners, one barycentric component per lane (assembly.cpp:587-594)
-        const int k = lane;
-        const double* nc = S.stack[sp].corners;  // still intact: children are pushed after the evaluation
-        const double c0 = nc[k], c1 = nc[3 + k], c2 = nc[6 + k];
-        const double m01 = 0.5 * (c0 + c1), m12 = 0.5 * (c1 + c2), m20 = 0.5 * (c2 + c0);
-        S.subc[0][k] = c0, S.subc[0][3 + k] = m01, S.subc[0][6 + k] = m20;
-        S.subc[1][k] = c1, S.subc[1][3 + k] = m12, S.subc[1][6 + k] = m01;
-        S.subc[2][k] = c2, S.subc[2][3 + k] = m20, S.subc[2][6 + k] = m12;
-        S.subc[3][k] = m01, S.subc[3][3 + k] = m12, S.subc[3][6 + k] = m20;
+      const int K = min(8, sp), base = sp - K;
+      const bool active = k < K;
+      double sv[NL], whole[NL];
+#pragma unroll
+      for (int t = 0; t < NL; ++t) sv[t] = whole[t] = 0.0;
+      int depth = 0, cc[6] = {0, 0, 0, 0, 0, 0};
+      if (active) {
+        const NodeB<NL>& nd = S.stack[base + k];
+        depth = nd.depth;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) whole[t] = nd.whole[t];
+        // sub-cell corners (assembly.cpp:587-594) in integer units, exact:
+        // sub 0 = (c0, m01, m20), 1 = (c1, m12, m01), 2 = (c2, m20, m12), 3 = (m01, m12, m20)
+        const int u0 = nd.c[0], v0 = nd.c[1], u1 = nd.c[2], v1 = nd.c[3], u2 = nd.c[4], v2 = nd.c[5];
+        const int mu01 = (u0 + u1) >> 1, mv01 = (v0 + v1) >> 1, mu12 = (u1 + u2) >> 1, mv12 = (v1 + v2) >> 1;
+        const int mu20 = (u2 + u0) >> 1, mv20 = (v2 + v0) >> 1;
+        cc[0] = sub == 0 ? u0 : sub == 1 ? u1 : sub == 2 ? u2 : mu01;
+        cc[1] = sub == 0 ? v0 : sub == 1 ? v1 : sub == 2 ? v2 : mv01;
+        cc[2] = sub == 0 ? mu01 : sub == 1 ? mu12 : sub == 2 ? mu20 : mu12;
+        cc[3] = sub == 0 ? mv01 : sub == 1 ? mv12 : sub == 2 ? mv20 : mv12;
+        cc[4] = sub == 0 ? mu20 : sub == 1 ? mu01 : sub == 2 ? mu12 : mu20;
+        cc[5] = sub == 0 ? mv20 : sub == 1 ? mv01 : sub == 2 ? mv12 : mv20;
+        const double inv = 1.0 / kUnit;
+        double cr[9];  // (b0, b1, b2) of the three corners, exact dyadics
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          cr[3 * i] = cc[2 * i] * inv;
+          cr[3 * i + 1] = cc[2 * i + 1] * inv;
+          cr[3 * i + 2] = (kUnit - cc[2 * i] - cc[2 * i + 1]) * inv;
+        }
+        const double frac = ldexp(1.0, -2 * (depth + 1));  // 0.25^(depth+1), as repeated quartering
+#pragma unroll 1
+        for (int q = 0; q < 7; ++q) {
+          // re-read the y-triangle frame from shared memory every point instead
+          // of keeping ~60 registers of it live across the loop
+          asm volatile("" ::: "memory");
+          double b[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            b[c] = c_r7_bary[q][0] * cr[c] + c_r7_bary[q][1] * cr[3 + c] + c_r7_bary[q][2] * cr[6 + c];
+          const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
+          const double w = c_r7_w[q] * (measure_x * frac);
+          double nw;
+          V3 mo, rho;
+          analytic<NTR == 3>(T, x, nw, mo, rho);
+          double d[NTR];
+          exact_values<NT, NTR>(T, nw, mo, rho, d);
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NTR; ++j) sv[i * NTR + j] += w * ((NT == 1 ? 1.0 : b[i]) * d[j]);
+        }
       }
-      __syncwarp();
-      if (lane < 28) {
-        const int sub = lane / 7, q = lane - 7 * sub;
-        double cr[9];
-#pragma unroll
-        for (int c = 0; c < 9; ++c) cr[c] = S.subc[sub][c];
-        double b[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          b[c] = c_r7_bary[q][0] * cr[c] + c_r7_bary[q][1] * cr[3 + c] + c_r7_bary[q][2] * cr[6 + c];
-        const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
-        const double w = c_r7_w[q] * (measure_x * frac);
-        double nw;
-        V3 mo, rho;
-        analytic<NTR == 3>(T, x, nw, mo, rho);
-        double d[NTR];
-        exact_values<NT, NTR>(T, nw, mo, rho, d);
-#pragma unroll
-        for (int i = 0; i < NT; ++i)
-#pragma unroll
-          for (int j = 0; j < NTR; ++j) S.vals[lane][i * NTR + j] = w * ((NT == 1 ? 1.0 : b[i]) * d[j]);
-      }
-      calls += 28;
-      __syncwarp();
-      for (int e = lane; e < 4 * NL; e += 32) {  // sub-cell sums in q order (accurate_cell :562-575)
-        const int sub = e / NL, t = e - sub * NL;
-        double s = 0.0;
-        for (int q = 0; q < 7; ++q) s += S.vals[sub * 7 + q][t];
-        S.subs[sub][t] = s;
-      }
-      __syncwarp();
+      calls += 28 * K;
+      // split = 0 + s0 + s1 + s2 + s3 at the node's leader lane (sub 0)
       double split[NL];
       double dmax = 0.0;
 #pragma unroll
       for (int t = 0; t < NL; ++t) {
-        split[t] = 0.0 + S.subs[0][t] + S.subs[1][t] + S.subs[2][t] + S.subs[3][t];
-        dmax = fmax(dmax, fabs(split[t] - nd.whole[t]));
+        const double s1 = __shfl_down_sync(0xffffffffu, sv[t], 1);
+        const double s2 = __shfl_down_sync(0xffffffffu, sv[t], 2);
+        const double s3 = __shfl_down_sync(0xffffffffu, sv[t], 3);
+        split[t] = 0.0 + sv[t] + s1 + s2 + s3;
+        dmax = fmax(dmax, fabs(split[t] - whole[t]));
       }
-      if (dmax <= nd.tol || nd.depth >= 6) {
+      const bool leader = active && sub == 0;
+      const bool accept = dmax <= ldexp(tol0, -depth) || depth >= 6;
+      if (leader && accept) {
 #pragma unroll
         for (int t = 0; t < NL; ++t) adapt[t] += split[t];
-        if (lane == 0) S.leaves[min(nd.depth, 6)] += 1ull;
-      } else {
-        if (lane < 4) {  // push children 3..0 so that sub 0 is processed first
-          const int s = 3 - lane;
-          Node& ch = S.stack[sp + lane];
-#pragma unroll
-          for (int c = 0; c < 9; ++c) ch.corners[c] = S.subc[s][c];
-          for (int t = 0; t < NL; ++t) ch.whole[t] = S.subs[s][t];
-          ch.frac = frac;
-          ch.tol = 0.5 * nd.tol;
-          ch.depth = nd.depth + 1;
-        }
-        sp += 4;
+        atomicAdd(&S.leaves[min(depth, 6)], 1ull);
       }
+      const unsigned refused = __ballot_sync(0xffffffffu, leader && !accept);
+      const bool mine = (refused >> (lane & ~3)) & 1u;  // my node is refused: push my sub-cell
+      __syncwarp();  // every lane has read its node before children overwrite the slots
+      if (active && mine) {
+        const int rank = __popc(refused & ((1u << (lane & ~3)) - 1u));
+        NodeB<NL>& ch = S.stack[base + 4 * rank + sub];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) ch.c[c] = (int16_t)cc[c];
+#pragma unroll
+        for (int t = 0; t < NL; ++t) ch.whole[t] = sv[t];
+        ch.depth = (int16_t)(depth + 1);
+      }
+      sp = base + 4 * __popc(refused);
       __syncwarp();
+    }
+    // accepted leaves of the eight leader lanes, summed in lane order
+#pragma unroll
+    for (int t = 0; t < NL; ++t) {
+      double tot = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) tot += __shfl_sync(0xffffffffu, adapt[t], 4 * kk);
+      adapt[t] = tot;
     }
     if (lane == 0)
       for (int t = 0; t < NL; ++t) a.local[p * kMaxLoc + t] = S.acc[t] + adapt[t];
@@ -906,8 +946,8 @@ gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const size_t smem = sizeof(WarpSmem) * kNfWarps;
-      auto launch = [&](auto kern) {
+      auto launch = [&](auto kern, size_t warp_smem) {
+        const size_t smem = warp_smem * kNfWarps;
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kNfWarps, smem);
@@ -922,13 +962,13 @@ gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
         else
           k_nf_points<3><<<grid, 128, 0, s>>>(a);
       } else if (N->nt == 1 && N->ntr == 1)
-        launch(k_nearfield<1, 1>);
+        launch(k_nearfield_b<1, 1>, sizeof(WarpSmemB<1>));
       else if (N->nt == 3 && N->ntr == 3)
-        launch(k_nearfield<3, 3>);
+        launch(k_nearfield_b<3, 3>, sizeof(WarpSmemB<9>));
       else if (N->nt == 1)
-        launch(k_nearfield<1, 3>);
+        launch(k_nearfield_b<1, 3>, sizeof(WarpSmemB<3>));
       else
-        launch(k_nearfield<3, 1>);
+        launch(k_nearfield_b<3, 1>, sizeof(WarpSmemB<3>));
       cuda_check(cudaGetLastError(), "k_nearfield launch");
     }
     if (N->nentries > 0) {
