@@ -134,6 +134,7 @@ struct YTri {
   V3 n;          // unit normal
   V3 s_hat[3], m_hat[3];
   double len[3];
+  double r0min[3];  // 1e-28 len^2 (the log guard, kernels.cpp:184); +inf for an empty edge
   V3 g_bary[3];  // P1 tangential barycentric gradients (femspace.cpp:254-277)
 };
 
@@ -195,7 +196,7 @@ __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3
     const bool a = sm >= 0.0, b = sp <= 0.0;
     const double num = a ? rp + sp : (b ? rm - sm : (rp + sp) * (rm - sm));
     const double den = a ? rm + sm : (b ? rp - sp : r0sq);
-    const bool ok = r0sq > 1e-28 * T.len[i] * T.len[i] && T.len[i] > 1e-300;
+    const bool ok = r0sq > T.r0min[i];  // same test as r0sq > 1e-28 len^2 && len > 1e-300
     f[i] = ok ? log_ratio(num, den) : 0.0;
     t[i] = T.len[i] > 1e-300 ? ti : 0.0;
     if (MOMENT) mo[i] = r0sq * f[i] + sp * rp - sm * rm;
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
         const V3 pm = T.v[i], pp = T.v[i == 2 ? 0 : i + 1];
         const double len = nrm(pp - pm);
         T.len[i] = len;
+        T.r0min[i] = len > 1e-300 ? 1e-28 * len * len : __longlong_as_double(0x7ff0000000000000ll);
         const V3 d = pp - pm;
         T.s_hat[i] = mk(d.x / len, d.y / len, d.z / len);
         T.m_hat[i] = cross(T.s_hat[i], T.n);
@@ -477,7 +479,14 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
       if (leader && accept) {
 #pragma unroll
         for (int t = 0; t < NL; ++t) adapt[t] += split[t];
-        atomicAdd(&S.leaves[min(depth, 6)], 1ull);
+      }
+      {  // leaf histogram: one ballot per depth, lane 0 updates the warp's counters
+        const bool leaf = leader && accept;
+#pragma unroll
+        for (int d = 0; d < 7; ++d) {
+          const unsigned m = __ballot_sync(0xffffffffu, leaf && min(depth, 6) == d);
+          if (lane == 0 && m) S.leaves[d] += (unsigned long long)__popc(m);
+        }
       }
       const unsigned refused = __ballot_sync(0xffffffffu, leader && !accept);
       const bool mine = (refused >> (lane & ~3)) & 1u;  // my node is refused: push my sub-cell
@@ -533,6 +542,7 @@ __global__ void __launch_bounds__(128) k_nf_points(const NfArgs a) {
     const V3 d = T.v[i == 2 ? 0 : i + 1] - T.v[i];
     const double len = nrm(d);
     T.len[i] = len;
+    T.r0min[i] = len > 1e-300 ? 1e-28 * len * len : __longlong_as_double(0x7ff0000000000000ll);
     T.s_hat[i] = mk(d.x / len, d.y / len, d.z / len);
     T.m_hat[i] = cross(T.s_hat[i], T.n);
   }
