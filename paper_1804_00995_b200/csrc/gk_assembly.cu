@@ -6,7 +6,7 @@
 // A += (W_x Phi)^T kr (assembly.cpp:218).
 //
 // Tile = (x block I, y block J), one CTA.  Thread t owns x location t of the
-// block (twins merged, <= 256 per block).  The block's y records (unique y
+// block (twins merged, <= kUCap per block).  The block's y records (unique y
 // locations with their <= 2 (slot, coef) pairs, in descending first-slot
 // order) and the x support lists are staged in shared memory.  All threads
 // walk the same record list (broadcast reads), kRecUnroll records at a time so
@@ -83,7 +83,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <bool HELM, int SLOTS>
-__global__ void __launch_bounds__(kAsmThreads, 2) k_assemble(const AsmArgs a) {
+__global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int t = threadIdx.x;

@@ -103,15 +103,20 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
                         int64_t nb, const double* bx, const double* by, const double* bz);
 
 // ---- assembly tiling ----------------------------------------------------------------
-// Tile shape (measured on B200: DFMA dependent latency ~9 cycles; the FP64 pipe
-// needs ~16 warps/SM at 2-3 independent chains per warp).  Two 256-thread CTAs
-// per SM: shared memory per CTA = H (kJCap x kUCap x 16 B = 96 KB) + staged
-// records and x supports (~15 KB).
-constexpr int kUCap = 256;   // x locations per tile, one per thread (two per thread measured slower: 8 warps/SM)
-constexpr int kJCap = 24;    // y dofs per tile (H accumulator rows)
-constexpr int kIMax = 256;   // x dofs per tile
-constexpr int kRCap = 128;   // y records per tile (staged in shared memory)
-constexpr int kXsCap = 640;  // x support entries per tile (staged in shared memory)
+// Tile shape.  A CTA alternates an FP64-bound pair loop with a latency-bound
+// staging + gather phase, so the SM needs several independent CTAs at random
+// phases to keep the FP64 pipe fed: four 128-thread CTAs per SM (16 warps;
+// 121 registers x 512 threads fits the register file), shared memory per CTA
+// = H (kJCap x kUCap x 16 B = 40 KB) + staged records and x supports (~10 KB).
+// Measured on cfg 2: 2 x 256-thread CTAs (24-dof y blocks) 2.81 ms; 4 x
+// 128-thread CTAs (20-dof y blocks) 2.67 ms although the smaller blocks
+// evaluate 12% more pairs (halo 1.81 vs 1.61).
+constexpr int kUCap = 128;   // x locations per tile, one per thread
+constexpr int kJCap = 20;    // y dofs per tile (H accumulator rows)
+constexpr int kIMax = 128;   // x dofs per tile
+constexpr int kRCap = 112;   // y records per tile (staged in shared memory)
+constexpr int kXsCap = 320;  // x support entries per tile (staged in shared memory)
+constexpr int kAsmCtasPerSm = 4;
 constexpr int kAsmThreads = kUCap;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 
