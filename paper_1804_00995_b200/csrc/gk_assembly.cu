@@ -36,7 +36,7 @@ namespace gk {
 namespace {
 
 constexpr int kRecUnroll = 4;  // records per group = independent evaluations per thread
-constexpr int kGC = 4;         // gather: columns per work item
+constexpr int kGC = 2;         // gather: columns per work item (divides kJCap)
 static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
 
 struct AsmSmem {

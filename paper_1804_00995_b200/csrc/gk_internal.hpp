@@ -107,12 +107,12 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // staging + gather phase, so the SM needs several independent CTAs at random
 // phases to keep the FP64 pipe fed: four 128-thread CTAs per SM (16 warps;
 // 121 registers x 512 threads fits the register file), shared memory per CTA
-// = H (kJCap x kUCap x 16 B = 40 KB) + staged records and x supports (~10 KB).
+// = H (kJCap x kUCap x 16 B = 44 KB) + staged records and x supports (~10 KB).
 // Measured on cfg 2: 2 x 256-thread CTAs (24-dof y blocks) 2.81 ms; 4 x
-// 128-thread CTAs (20-dof y blocks) 2.67 ms although the smaller blocks
-// evaluate 12% more pairs (halo 1.81 vs 1.61).
+// 128-thread CTAs (22-dof y blocks) 2.57 ms although the smaller blocks
+// evaluate 7% more pairs (halo 1.71 vs 1.61).
 constexpr int kUCap = 128;   // x locations per tile, one per thread
-constexpr int kJCap = 20;    // y dofs per tile (H accumulator rows)
+constexpr int kJCap = 22;    // y dofs per tile (H accumulator rows)
 constexpr int kIMax = 128;   // x dofs per tile
 constexpr int kRCap = 112;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 320;  // x support entries per tile (staged in shared memory)
