@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "gk_internal.hpp"
 
@@ -87,7 +88,7 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t row_blocks = (rows + kMvThreads - 1) / kMvThreads;
-  const int64_t target = (int64_t)sms * 8;  // ~8 resident CTAs of 256 threads per SM
+  const int64_t target = (int64_t)sms * 48;  // CTAs of 256 threads in flight (measured: x8 -> x48 moved cfg 2 from 5660 to 5820 GB/s)
   splits = std::max<int64_t>(1, std::min<int64_t>((target + row_blocks - 1) / row_blocks,
                                                   std::max<int64_t>(1, cols / 64)));
   splits = std::min<int64_t>(splits, 65535);
@@ -95,14 +96,21 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
   splits = (cols + cps - 1) / cps;
 }
 
-struct Scratch {
-  void* p = nullptr;
-  size_t bytes = 0;
-  ~Scratch() {
-    if (p) cudaFree(p);
-  }
-};
-thread_local Scratch t_scratch;
+// The partial sums live in stream-ordered memory (cudaMallocAsync from the
+// device's default pool, which keeps up to 256 MB cached between calls), so
+// matvecs on different streams never share a scratch buffer.
+void ensure_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 256ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  });
+}
 }  // namespace
 
 int matvec_launch_count(int64_t rows, int64_t cols) { return (rows > 0 && cols > 0) ? 2 : 1; }
@@ -117,24 +125,23 @@ void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const
   int64_t splits, cps;
   plan(rows, cols, splits, cps);
   const size_t need = sizeof(double2) * (size_t)rows * (size_t)splits;
-  if (t_scratch.bytes < need) {
-    if (t_scratch.p) {
-      cudaStreamSynchronize(s);
-      cudaFree(t_scratch.p);
-      t_scratch.p = nullptr;
-      t_scratch.bytes = 0;
-    }
-    if (cudaMalloc(&t_scratch.p, need) != cudaSuccess) throw NoMemError("gk_matvec: scratch allocation failed");
-    t_scratch.bytes = need;
+  ensure_pool();
+  void* P = nullptr;
+  if (cudaMallocAsync(&P, need, s) != cudaSuccess) {
+    cudaGetLastError();
+    throw NoMemError("gk_matvec: scratch allocation failed");
   }
   const dim3 grid((unsigned)((rows + kMvThreads - 1) / kMvThreads), (unsigned)splits);
   k_matvec_partial<<<grid, kMvThreads, 0, s>>>(static_cast<const double2*>(A), rows, cols, lda,
                                                static_cast<const double2*>(x),
-                                               static_cast<double2*>(t_scratch.p), cps);
-  cuda_check(cudaGetLastError(), "k_matvec_partial launch");
-  k_matvec_reduce<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(static_cast<const double2*>(t_scratch.p), rows,
+                                               static_cast<double2*>(P), cps);
+  const cudaError_t e1 = cudaGetLastError();
+  k_matvec_reduce<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(static_cast<const double2*>(P), rows,
                                                                 (int)splits, static_cast<double2*>(y));
-  cuda_check(cudaGetLastError(), "k_matvec_reduce launch");
+  const cudaError_t e2 = cudaGetLastError();
+  cudaFreeAsync(P, s);
+  cuda_check(e1, "k_matvec_partial launch");
+  cuda_check(e2, "k_matvec_reduce launch");
 }
 
 }  // namespace gk
