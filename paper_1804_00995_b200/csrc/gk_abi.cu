@@ -58,6 +58,66 @@ void DevBuf::upload(const void* src, size_t n) {
   if (n) cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
 }
 
+void ensure_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 256ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  });
+}
+
+void DevArena::upload() {
+  release();
+  bytes = host.size();
+  if (bytes) {
+    ensure_pool();
+    if (cudaMallocAsync(&p, bytes, nullptr) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      bytes = 0;
+      throw NoMemError("device allocation of " + std::to_string(host.size()) + " bytes failed");
+    }
+    // through a grow-only pinned staging buffer: a pageable copy of a few MB
+    // runs at a few GB/s, a pinned one at PCIe speed
+    static std::mutex staging_mutex;
+    static void* staging = nullptr;
+    static size_t staging_bytes = 0;
+    std::lock_guard<std::mutex> hold(staging_mutex);
+    if (staging_bytes < bytes) {
+      if (staging) cudaFreeHost(staging);
+      staging = nullptr;
+      staging_bytes = 0;
+      if (cudaMallocHost(&staging, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        staging = nullptr;
+      } else {
+        staging_bytes = bytes;
+      }
+    }
+    if (staging) {
+      std::memcpy(staging, host.data(), bytes);
+      cuda_check(cudaMemcpy(p, staging, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    } else {
+      cuda_check(cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    }
+  }
+  std::vector<char>().swap(host);
+}
+
+void DevArena::release() {
+  if (p) {
+    cudaDeviceSynchronize();  // the tables may still be read by work on any stream
+    cudaFreeAsync(p, nullptr);
+  }
+  p = nullptr;
+  bytes = 0;
+}
+
 }  // namespace gk
 
 using namespace gk;
@@ -70,14 +130,12 @@ struct gk_plan {
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false;
   int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0)
-  DevBuf tiles;  // TileDesc per tile, (x block, y block) order, masked ones flagged
-  DevBuf xl_x, xl_y, xl_z, xsup_start, xsup_u, xsup_c, yrec, xperm, yperm;
-  uint64_t device_bytes() const {
-    const DevBuf* b[] = {&tiles, &xl_x, &xl_y, &xl_z, &xsup_start, &xsup_u, &xsup_c, &yrec, &xperm, &yperm};
-    uint64_t s = 0;
-    for (auto* p : b) s += p->bytes;
-    return s;
-  }
+  // device tables in one arena: TileDesc per tile ((x block, y block) order,
+  // masked ones flagged), x locations, x supports, y records, dof maps
+  DevArena arena;
+  size_t o_tiles = 0, o_xl_x = 0, o_xl_y = 0, o_xl_z = 0, o_xsup_start = 0, o_xsup_u = 0, o_xsup_c = 0, o_yrec = 0,
+         o_xperm = 0, o_yperm = 0;
+  uint64_t device_bytes() const { return arena.bytes; }
 };
 
 struct gk_green_plan {
@@ -200,16 +258,24 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->nmtiles = (int64_t)T.mtile_i.size();
   P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
-  P->tiles.upload(make_tile_descs(T));
-  P->xl_x.upload(T.xl_x);
-  P->xl_y.upload(T.xl_y);
-  P->xl_z.upload(T.xl_z);
-  P->xsup_start.upload(T.xsup_start);
-  P->xsup_u.upload(T.xsup_u);
-  P->xsup_c.upload(T.xsup_c);
-  P->yrec.upload(T.yrec);
-  P->xperm.upload(X.perm);
-  P->yperm.upload(Yr.perm);
+  DevArena& Ar = P->arena;
+  const std::vector<TileDesc> descs = make_tile_descs(T);
+  lap("tile descriptors");
+  Ar.host.reserve(descs.size() * sizeof(TileDesc) + (T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
+                  (T.xsup_start.size() + T.xsup_u.size() + X.perm.size() + Yr.perm.size()) * sizeof(int32_t) +
+                  T.yrec.size() * sizeof(YRec) + 16 * 256);
+  P->o_tiles = Ar.add(descs);
+  P->o_xl_x = Ar.add(T.xl_x);
+  P->o_xl_y = Ar.add(T.xl_y);
+  P->o_xl_z = Ar.add(T.xl_z);
+  P->o_xsup_start = Ar.add(T.xsup_start);
+  P->o_xsup_u = Ar.add(T.xsup_u);
+  P->o_xsup_c = Ar.add(T.xsup_c);
+  P->o_yrec = Ar.add(T.yrec);
+  P->o_xperm = Ar.add(X.perm);
+  P->o_yperm = Ar.add(Yr.perm);
+  lap("stage");
+  Ar.upload();
   lap("upload");
   return P;
 }
@@ -220,16 +286,17 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   if (!A) throw std::invalid_argument("gk_plan_assemble: null matrix");
   if (lda < P->rows) throw std::invalid_argument("gk_plan_assemble: lda < rows");
   AsmArgs a;
-  a.tiles = P->tiles.as<TileDesc>();
-  a.xl_x = P->xl_x.as<double>();
-  a.xl_y = P->xl_y.as<double>();
-  a.xl_z = P->xl_z.as<double>();
-  a.xsup_start = P->xsup_start.as<int32_t>();
-  a.xsup_u = P->xsup_u.as<int32_t>();
-  a.xsup_c = P->xsup_c.as<double>();
-  a.yrec = P->yrec.as<YRec>();
-  a.xperm = P->xperm.as<int32_t>();
-  a.yperm = P->yperm.as<int32_t>();
+  const DevArena& Ar = P->arena;
+  a.tiles = Ar.at<TileDesc>(P->o_tiles);
+  a.xl_x = Ar.at<double>(P->o_xl_x);
+  a.xl_y = Ar.at<double>(P->o_xl_y);
+  a.xl_z = Ar.at<double>(P->o_xl_z);
+  a.xsup_start = Ar.at<int32_t>(P->o_xsup_start);
+  a.xsup_u = Ar.at<int32_t>(P->o_xsup_u);
+  a.xsup_c = Ar.at<double>(P->o_xsup_c);
+  a.yrec = Ar.at<YRec>(P->o_yrec);
+  a.xperm = Ar.at<int32_t>(P->o_xperm);
+  a.yperm = Ar.at<int32_t>(P->o_yperm);
   a.A = A;
   a.lda = lda;
   a.eps2 = P->eps * P->eps;
@@ -346,6 +413,8 @@ gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kerne
                "cudaMemcpy2DAsync D2H");
     cuda_check(cudaStreamSynchronize(s), "gk_bem_dense");
     lap("d2h");
+    P.reset();
+    lap("destroy");
   });
 }
 

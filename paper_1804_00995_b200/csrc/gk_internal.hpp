@@ -76,6 +76,38 @@ struct DevBuf {
   }
 };
 
+// One device allocation for many read-only tables: staged on the host at
+// 256-byte aligned offsets, then one stream-ordered allocation from the
+// device's default pool (cached between plans) and one copy.  Replaces a
+// cudaMalloc/cudaMemcpy/cudaFree per table (~10 ms per one-shot plan).
+struct DevArena {
+  void* p = nullptr;
+  size_t bytes = 0;
+  std::vector<char> host;
+  DevArena() = default;
+  DevArena(const DevArena&) = delete;
+  DevArena& operator=(const DevArena&) = delete;
+  ~DevArena() { release(); }
+  template <class T>
+  size_t add(const T* data, size_t n) {
+    const size_t off = (host.size() + 255) & ~size_t(255);
+    host.resize(off + n * sizeof(T));
+    if (n) std::memcpy(host.data() + off, data, n * sizeof(T));
+    return off;
+  }
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    return add(v.data(), v.size());
+  }
+  void upload();  // allocate + copy; releases the host staging
+  void release();
+  template <class T>
+  T* at(size_t off) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p) + off);
+  }
+};
+void ensure_pool();  // default memory pool keeps up to 256 MB cached
+
 // ---- unique quadrature locations of one side (host) -----------------------------
 // Points that are bit-identical (the edge-midpoint rule's twins, SURVEY trap 1)
 // are merged into one location carrying the summed (dof, w*phi) contributions.

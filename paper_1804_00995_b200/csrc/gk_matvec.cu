@@ -97,20 +97,8 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
 }
 
 // The partial sums live in stream-ordered memory (cudaMallocAsync from the
-// device's default pool, which keeps up to 256 MB cached between calls), so
-// matvecs on different streams never share a scratch buffer.
-void ensure_pool() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = 256ull << 20;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  });
-}
+// device's default pool, see ensure_pool), so matvecs on different streams
+// never share a scratch buffer.
 }  // namespace
 
 int matvec_launch_count(int64_t rows, int64_t cols) { return (rows > 0 && cols > 0) ? 2 : 1; }

@@ -23,12 +23,14 @@ struct Key {
   uint64_t a, b, c;
   bool operator==(const Key& o) const { return a == o.a && b == o.b && c == o.c; }
 };
-struct KeyHash {
+struct KeyHash {  // splitmix64-style mixing of the three coordinate bit patterns
+  static uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
   size_t operator()(const Key& k) const {
-    uint64_t h = k.a * 0x9E3779B97F4A7C15ULL;
-    h ^= (k.b + 0x632BE59BD9B4E019ULL + (h << 6) + (h >> 2));
-    h ^= (k.c + 0x85157AF5ULL + (h << 6) + (h >> 2));
-    return (size_t)(h ^ (h >> 29));
+    return (size_t)mix(k.a ^ mix(k.b ^ mix(k.c + 0x9E3779B97F4A7C15ULL)));
   }
 };
 uint64_t bits(double v) {
@@ -88,20 +90,31 @@ Locations build_locations(const gk_side& s, const char* who) {
   L.npts = s.npts;
   L.nfree = s.nfree;
   L.point_loc.resize(s.npts);
-  std::unordered_map<Key, int64_t, KeyHash> index;
-  index.reserve((size_t)s.npts);
+  // open-addressing table of location ids keyed by the coordinate bit
+  // patterns (linear probing, load <= 1/2); ids in first-seen point order
+  size_t cap = 16;
+  while (cap < 2 * (size_t)s.npts) cap <<= 1;
+  std::vector<int64_t> slot(cap, -1);
+  std::vector<Key> keys;
+  keys.reserve((size_t)s.npts);
+  L.x.reserve((size_t)s.npts);
+  L.y.reserve((size_t)s.npts);
+  L.z.reserve((size_t)s.npts);
+  const KeyHash hasher;
   for (int64_t k = 0; k < s.npts; ++k) {
     const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
-    auto it = index.find(key);
-    if (it == index.end()) {
+    size_t h = hasher(key) & (cap - 1);
+    while (slot[h] >= 0 && !(keys[(size_t)slot[h]] == key)) h = (h + 1) & (cap - 1);
+    if (slot[h] < 0) {
       const int64_t u = (int64_t)L.x.size();
-      index.emplace(key, u);
+      slot[h] = u;
+      keys.push_back(key);
       L.x.push_back(s.x[k]);
       L.y.push_back(s.y[k]);
       L.z.push_back(s.z[k]);
       L.point_loc[k] = u;
     } else {
-      L.point_loc[k] = it->second;
+      L.point_loc[k] = slot[h];
     }
   }
   const int64_t U = L.size();

@@ -1,6 +1,10 @@
 // Python binding of the galerk_b200 host API (csrc/host/galerk.hpp).
 // std::invalid_argument -> ValueError, std::runtime_error -> RuntimeError, so
 // Python tests read like the reference's doctest cases.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
@@ -430,15 +434,23 @@ PYBIND11_MODULE(_galerk, m) {
       [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
          const BemOptions& o, uintptr_t host_ptr, int64_t lda) {
         py::gil_scoped_release rel;
-        const SideTables a = make_side_tables(dx, t), b = make_side_tables(dy, u);
-        const gk_side sa = a.abi(), sb = b.abi();
+        const auto t0 = std::chrono::steady_clock::now();
+        // bem_dense(dom, dom, V, k, V): one side-table build serves both sides
+        const bool same = &dx == &dy && &t == &u;
+        const SideTables a = make_side_tables(dx, t);
+        const SideTables b = same ? SideTables{} : make_side_tables(dy, u);
+        const SideTables& bb = same ? a : b;
+        if (std::getenv("GK_TIMING"))
+          std::fprintf(stderr, "[bem_dense_into] side tables %8.2f ms\n",
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        const gk_side sa = a.abi(), sb = bb.abi();
         const gk_kernel kk = k.abi();
         gk_options go;
         gk_options_default(&go);
         go.memory_cap_bytes = o.memory_cap_bytes;
         go.chunk = o.chunk;
         throw_status(gk_bem_dense(&sa, &sb, &kk, &go, reinterpret_cast<gk_cplx*>(host_ptr), lda));
-        return (int64_t)(a.qs.size() * 32 + b.qs.size() * 32 + a.elem_dofs.size() * 4 + b.elem_dofs.size() * 4);
+        return (int64_t)(a.qs.size() * 32 + bb.qs.size() * 32 + a.elem_dofs.size() * 4 + bb.elem_dofs.size() * 4);
       },
       py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"), py::arg("opts"),
       py::arg("host_ptr"), py::arg("lda"));
