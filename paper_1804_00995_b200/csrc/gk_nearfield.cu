@@ -176,21 +176,26 @@ __constant__ double c_r7_w[7];
 // does in the reference (|w| = 0, sgn(w) = 0).
 template <bool MOMENT>
 __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3& moment, V3& rho) {
-  const double w0 = dot(x - T.v[0], T.n);
-  rho = x - w0 * T.n;
-  const V3 A = T.v[0] - x, B = T.v[1] - x, C = T.v[2] - x;
-  const double rv[3] = {nrm_fast(A), nrm_fast(B), nrm_fast(C)};  // rp of edge i == rm of edge i+1
-  const double trip = dot(A, cross(B, C));
-  const double vden = fma(rv[0] * rv[1], rv[2], fma(dot(A, B), rv[2], fma(dot(A, C), rv[1], dot(B, C) * rv[0])));
+  // vertices relative to x, shared by the edge terms and the solid angle.  The
+  // edge coordinates t = (v_i - rho).m_hat and s = (v - rho).s_hat equal
+  // (v - x).m_hat and (v - x).s_hat because rho - x is along the normal,
+  // which is orthogonal to both in-plane unit vectors; rho itself is only
+  // needed for the P1 barycentric weights.
+  const V3 Av[3] = {T.v[0] - x, T.v[1] - x, T.v[2] - x};
+  const double w0 = -dot(Av[0], T.n);  // (x - v0).n
+  rho = MOMENT ? x - w0 * T.n : x;
+  const double rv[3] = {nrm_fast(Av[0]), nrm_fast(Av[1]), nrm_fast(Av[2])};  // rp of edge i == rm of edge i+1
+  const double trip = dot(Av[0], cross(Av[1], Av[2]));
+  const double vden = fma(rv[0] * rv[1], rv[2],
+                          fma(dot(Av[0], Av[1]), rv[2], fma(dot(Av[0], Av[2]), rv[1], dot(Av[1], Av[2]) * rv[0])));
   const double omega = 2.0 * atan2_fast(trip, vden);
   double f[3], t[3], mo[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int ip = i == 2 ? 0 : i + 1;
-    const V3 dm = T.v[i] - rho, dp = T.v[ip] - rho;
-    const double ti = dot(dm, T.m_hat[i]);
-    const double sm = dot(dm, T.s_hat[i]);
-    const double sp = dot(dp, T.s_hat[i]);
+    const double ti = dot(Av[i], T.m_hat[i]);
+    const double sm = dot(Av[i], T.s_hat[i]);
+    const double sp = dot(Av[ip], T.s_hat[i]);
     const double rm = rv[i], rp = rv[ip];
     const double r0sq = ti * ti + w0 * w0;
     const bool a = sm >= 0.0, b = sp <= 0.0;
