@@ -280,13 +280,13 @@ __global__ void __launch_bounds__(128) k_green64_sym(const GreenArgs a, const do
         for (int k = 0; k < 2; ++k) {
           const double g = rinv[2 * u + k];
           if (HELM) {
-            const double c_ = cs[2 * u + k], s_ = sn[2 * u + k];
-            const double wr = q.x * g, wi = q.y * g;  // row: G q_s
-            ra[k] = fma(c_, wr, fma(-s_, wi, ra[k]));
-            ia[k] = fma(c_, wi, fma(s_, wr, ia[k]));
-            const double vr = tq[k].x * g, vi = tq[k].y * g;  // column: G q_t
-            pr = fma(c_, vr, fma(-s_, vi, pr));
-            pi = fma(c_, vi, fma(s_, vr, pi));
+            // G = (cs + i sn) / r formed once (two DMUL) and shared by the row
+            // (G q_s) and column (G q_t) accumulations
+            const double gr = cs[2 * u + k] * g, gi = sn[2 * u + k] * g;
+            ra[k] = fma(gr, q.x, fma(-gi, q.y, ra[k]));
+            ia[k] = fma(gr, q.y, fma(gi, q.x, ia[k]));
+            pr = fma(gr, tq[k].x, fma(-gi, tq[k].y, pr));
+            pi = fma(gr, tq[k].y, fma(gi, tq[k].x, pi));
           } else {
             ra[k] = fma(g, q.x, ra[k]);
             ia[k] = fma(g, q.y, ia[k]);
