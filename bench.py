@@ -220,6 +220,8 @@ def main():
     import torch
 
     dist = None
+    if args.impl == "b200" and torch.cuda.is_available():
+        torch.cuda.set_device(local)  # before NCCL init, so each rank's communicator binds its own GPU
     if world > 1:
         import torch.distributed as dist
 
