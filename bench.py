@@ -176,15 +176,19 @@ def measured_peaks():
         return {}
 
 
-def profile_traffic(cfg):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def profile_summary(cfg):
+    """The committed ncu capture of the dominant kernel (profiles/ncu_summary.json)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(f"cfg{cfg}", {}).get("k_assemble_dram_bytes_per_launch")
+            return json.load(f).get(f"cfg{cfg}", {})
     except Exception:
-        return None
+        return {}
+
+
+def profile_traffic(cfg):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    return profile_summary(cfg).get("k_assemble_dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------------------------
@@ -343,7 +347,9 @@ def main():
                          "work": "pairs_unique (twins merged, symmetric half) x %.0f flops/pair = canonical "
                                  "libdevice probe F_pair (SURVEY 8d)" % F_PAIR_PROBE_FLOPS[helm],
                          "frac_production_formula": achieved_prod / peak,
-                         "frac_executed_pairs_production_formula": exec_prod / peak},
+                         "frac_executed_pairs_production_formula": exec_prod / peak,
+                         "ncu_fp64_pipe_pct": profile_summary(args.config).get("fp64_pipe_pct"),
+                         "ncu_sfu_xu_pipe_pct": profile_summary(args.config).get("xu_pipe_pct")},
             "roofline_matvec": {"bound": "hbm", "achieved": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak": hbm,
                                 "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},

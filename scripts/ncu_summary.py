@@ -14,6 +14,9 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock (Hz)"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active (% of peak)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy (%)"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU pipe (SFU: MUFU rsqrt/rcp) % of peak"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe % of peak"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % of peak"),
     ("sm__warps_active.avg.per_cycle_active", "active warps / SM"),
     ("launch__registers_per_thread", "registers / thread"),
     ("launch__shared_mem_per_block_dynamic", "dynamic smem / block (B)"),
@@ -66,6 +69,7 @@ def main():
                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         summary.append({"kernel": d.get("Kernel Name", ""), "duration_ms": num("gpu__time_duration.sum"),
                         "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                        "xu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
                         "dram_bytes": dram})
         lines.append("")
     open(dst, "w").write("\n".join(lines) + "\n")
@@ -78,7 +82,8 @@ def main():
         except Exception:
             allj = {}
         allj[key] = {"k_assemble_dram_bytes_per_launch": summary[0]["dram_bytes"], "report": rep,
-                     "fp64_pipe_pct": summary[0]["fp64_pipe_pct"], "duration_ms": summary[0]["duration_ms"]}
+                     "fp64_pipe_pct": summary[0]["fp64_pipe_pct"], "xu_pipe_pct": summary[0]["xu_pipe_pct"],
+                     "duration_ms": summary[0]["duration_ms"]}
         json.dump(allj, open(path, "w"), indent=1)
 
 
