@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
           cr[3 * i + 2] = (kUnit - cc[2 * i] - cc[2 * i + 1]) * inv;
         }
         const double frac = ldexp(1.0, -2 * (depth + 1));  // 0.25^(depth+1), as repeated quartering
-#pragma unroll 1
+#pragma unroll 2
         for (int q = 0; q < 7; ++q) {
           // re-read the y-triangle frame from shared memory every point instead
           // of keeping ~60 registers of it live across the loop
