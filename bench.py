@@ -411,6 +411,8 @@ def reference_arm(args, rank, world, dist):
     oracle = load_oracle()
     spec, mesh, dom, space, kern, k, hbar, kname = config_problem(g, args.config)
     threads = os.cpu_count() or 1
+    if args.config == 5:
+        return reference_arm_green(args, g, oracle, spec, mesh, dom, k, kname, threads, world, dist)
     fam = 1 if spec["fam"] == "P1" else 0
     M = mesh.element_count() * spec["gauss"]
     rows, npts = cpu_sample_rows(oracle, mesh, spec["gauss"], fam, target_points=min(M, 2048))
@@ -418,6 +420,16 @@ def reference_arm(args, rank, world, dist):
         run_cpu(oracle, mesh, spec, k, kname, rows[:8], threads)
     ts = [run_cpu(oracle, mesh, spec, k, kname, rows, threads) for _ in range(args.steps)]
     t = float(np.mean(ts))
+    if args.config == 3:
+        # cfg 3's step includes the near-field correction: the reference's
+        # regularize (assembly.cpp:609-697) for the same test elements (P0: row = element)
+        nt = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            oracle.regularize(mesh.vertices, mesh.elements, spec["gauss"], 0, mesh.vertices, mesh.elements,
+                              spec["gauss"], 0, "[1/r]", 0, 0.0, list(rows), threads)
+            nt.append(time.perf_counter() - t0)
+        t += float(np.mean(nt))
     value = npts * M / t
     out = {"impl": "reference", "metric": "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per assembly, fp64)",
            "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -426,7 +438,38 @@ def reference_arm(args, rank, world, dist):
            "config": {"workload": workload_name(args.config, spec, mesh), "N": space.free_count() if space else None},
            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
                             "sample": f"oracle bem_product restatement (OpenMP over trial columns), {len(rows)} "
-                                      f"complete test rows = {npts} x-points x {M} y-points per step"},
+                                      f"complete test rows = {npts} x-points x {M} y-points per step"
+                                      + (" + regularize of those test elements" if args.config == 3 else "")},
+           "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def reference_arm_green(args, g, oracle, spec, mesh, dom, k, kname, threads, world, dist):
+    """cfg 5 reference arm: the oracle's matrix-free Green matvec (the reference's
+    evaluate_blocks(mask=true) x weighted charges) on a sample of targets."""
+    pts, w, _ = g.quadrature(dom)
+    q = np.asarray(w) * g.complex_normal(spec["seed"], len(w))
+    M = len(w)
+    ids = list(range(0, M, M // 96))[:96]
+    lo, hi = np.asarray(pts).min(axis=0), np.asarray(pts).max(axis=0)
+    eps = 1e-12 * float(np.linalg.norm(hi - lo))  # singular_guard_radius (kernels.cpp:14-19)
+    oracle.green_matvec(kname, k, pts, pts, q, eps, ids[:4], threads)  # warm-up
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.green_matvec(kname, k, pts, pts, q, eps, ids, threads)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    value = len(ids) * M / t
+    out = {"impl": "reference", "metric": "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)",
+           "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64 (complex128)", "data": "synthetic",
+           "config": {"workload": "cfg5: matrix-free Helmholtz Green matvec, 983040 targets = sources", "M": M},
+           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                            "sample": f"oracle Green matvec, {len(ids)} targets x {M} sources per step"},
            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     if dist:
