@@ -172,6 +172,7 @@ def test_config4_p0_l6_chunk_rows_and_matvecs(galerk, oracle):
     complete rows of 8 uniformly spaced 1024-point x chunks against
     the oracle, then the 10 stored-matrix matvecs (seed 3) on those rows."""
     torch = _torch()
+    torch.cuda.empty_cache()  # earlier tests' matrices may still sit in torch's cache
     free, _ = torch.cuda.mem_get_info()
     if free < 120 * 2 ** 30:
         pytest.skip("needs ~110 GB of free device memory")
