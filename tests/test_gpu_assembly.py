@@ -97,6 +97,28 @@ def test_nonsymmetric_mixed_spaces_and_meshes(galerk, oracle):
     assert A.shape == (42, 320) and rel_fro(A, ref) <= TOL
 
 
+def test_near_coincident_unwelded_mesh_masks_like_the_reference(galerk, oracle):
+    """Collisions that are not bitwise twins: an unwelded P0 mesh whose triangles
+    carry their own vertex copies, each nudged by ~1e-14.  Quadrature points of
+    neighbouring triangles then sit closer than eps (~3e-12) without being equal,
+    so the reference's r^2 <= eps^2 mask (kernels.cpp:104-111) zeroes those pairs;
+    the plan must notice (no exact coincidence) and mask every tile."""
+    base = galerk.build_sphere(162, 1.0)
+    v0, e0 = np.asarray(base.vertices), np.asarray(base.elements)
+    rng = np.random.default_rng(9)
+    v = (v0[e0].reshape(-1, 3) * (1.0 + 1e-14 * rng.uniform(-1, 1, size=(3 * len(e0), 1))))
+    e = np.arange(3 * len(e0), dtype=np.int32).reshape(-1, 3)
+    m = galerk.Mesh(v, e)
+    dom = galerk.make_domain(m, 3)
+    sp = galerk.make_fem(m, "P0")
+    kern = galerk.green_kernel("[exp(ikr)/r]", 4.0)
+    A = galerk.bem_dense(dom, dom, sp, kern, sp)
+    ref = oracle.bem_dense(v, e, 3, P0, v, e, 3, P0, "[exp(ikr)/r]", 4.0)
+    assert np.all(np.isfinite(A)) and rel_fro(A, ref) <= TOL
+    info = galerk.plan_info_dry(dom, dom, sp, kern, sp)
+    assert info["masked_tiles"] == info["tiles"]  # unsafe near-coincidences: mask everywhere
+
+
 def test_lda_padding_and_determinism(galerk):
     m, dom, sp, _ = sphere_problem(galerk, 642, 3, "P1")
     k = galerk.green_kernel("[exp(ikr)/r]", 4.2)
