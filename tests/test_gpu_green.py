@@ -103,3 +103,30 @@ def test_config5_full_size_sampled_targets(galerk, oracle):
     ref = np.array(oracle.green_matvec("[exp(ikr)/r]", k, pts, pts, q, info["eps"], ids, 16))
     assert rel_fro(y64.cpu().numpy()[ids], ref) <= 1e-10
     assert rel_fro(y32.cpu().numpy()[ids], ref) <= FP32_TOL
+
+
+def test_green_matvec_near_coincident_points(galerk, oracle):
+    """Points closer than eps but not bitwise equal (an unwelded mesh nudged by
+    ~1e-14): the distance mask, not the twin merge, must drop those pairs, on
+    the symmetric and the general path alike."""
+    import torch
+
+    base = galerk.build_sphere(162, 1.0)
+    v0, e0 = np.asarray(base.vertices), np.asarray(base.elements)
+    rng = np.random.default_rng(9)
+    v = v0[e0].reshape(-1, 3) * (1.0 + 1e-14 * rng.uniform(-1, 1, size=(3 * len(e0), 1)))
+    e = np.arange(3 * len(e0), dtype=np.int32).reshape(-1, 3)
+    dom = galerk.make_domain(galerk.Mesh(v, e), 3)
+    pts, w, _ = galerk.quadrature(dom)
+    q = np.asarray(w) * galerk.complex_normal(4, len(w))
+    kern = galerk.green_kernel("[exp(ikr)/r]", 4.0)
+    plan = galerk.GreenPlan(pts, pts, kern)
+    assert plan.info()["symmetric"]
+    qd = torch.tensor(q, device="cuda")
+    y = torch.empty(len(pts), dtype=torch.complex128, device="cuda")
+    plan.matvec(qd.data_ptr(), y.data_ptr(), galerk.FP64, 0)
+    torch.cuda.synchronize()
+    ids = list(range(0, len(pts), 7))
+    ref = np.array(oracle.green_matvec("[exp(ikr)/r]", 4.0, pts, pts, q, plan.info()["eps"], ids, 8))
+    yn = y.cpu().numpy()
+    assert np.all(np.isfinite(yn)) and rel_fro(yn[ids], ref) <= 1e-10
