@@ -33,7 +33,7 @@ def _worker(rank, world, port, out):
 
 def test_two_rank_max_and_aggregate():
     port = _free_port()
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork of a process that already runs OpenMP threads
     out = mgr.dict()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] == out[1]
