@@ -4,6 +4,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -175,20 +180,22 @@ void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) 
 // depend on a single descriptor load instead of a chain of table lookups.
 // Unmasked and masked tiles are merged back into (x block, y block) order and
 // run in one launch; the flag selects the masked pair loop per CTA.
-std::vector<TileDesc> make_tile_descs(const TileTables& T) {
+// TX holds the x-block tables, T the y-block tables and the tile lists (the
+// same object for whole-matrix plans).
+std::vector<TileDesc> make_tile_descs(const TileTables& TX, const TileTables& T) {
   const size_t nu = T.tile_i.size(), nm = T.mtile_i.size();
   std::vector<TileDesc> d(nu + nm);
   auto fill = [&](TileDesc& D, int32_t bi, int32_t bj, bool masked) {
-    D.i0 = T.xb_dof_start[bi];
-    D.nI = T.xb_dof_start[bi + 1] - D.i0;
+    D.i0 = TX.xb_dof_start[bi];
+    D.nI = TX.xb_dof_start[bi + 1] - D.i0;
     D.j0 = T.yb_dof_start[bj];
     D.nJ = T.yb_dof_start[bj + 1] - D.j0;
-    D.l0 = T.xb_loc_start[bi];
-    D.nu = T.xb_loc_start[bi + 1] - D.l0;
+    D.l0 = TX.xb_loc_start[bi];
+    D.nu = TX.xb_loc_start[bi + 1] - D.l0;
     D.r0 = T.yb_rec_start[bj];
     D.nrec = T.yb_rec_start[bj + 1] - D.r0;
-    D.xs0 = T.xsup_start[D.i0];
-    D.nxs = T.xsup_start[D.i0 + D.nI] - D.xs0;
+    D.xs0 = TX.xsup_start[D.i0];
+    D.nxs = TX.xsup_start[D.i0 + D.nI] - D.xs0;
     D.zero_rows = T.yb_zero[bj];
     D.masked = masked ? 1 : 0;
   };
@@ -259,7 +266,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
   DevArena& Ar = P->arena;
-  const std::vector<TileDesc> descs = make_tile_descs(T);
+  const std::vector<TileDesc> descs = make_tile_descs(T, T);
   lap("tile descriptors");
   Ar.host.reserve(descs.size() * sizeof(TileDesc) + (T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
                   (T.xsup_start.size() + T.xsup_u.size() + X.perm.size() + Yr.perm.size()) * sizeof(int32_t) +
@@ -304,6 +311,329 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.symmetric = P->symmetric ? 1 : 0;
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
   launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
+}
+
+
+// ---- one-shot assembly streamed to the host in column slabs ------------------
+// gk_bem_dense's cost is the host plan (~18 ms on cfg 2) followed by the
+// device->host copy of the matrix (29 ms at the PCIe limit), the kernel being
+// ~3 ms.  Streaming overlaps them: the x side is located, ordered and tiled
+// once; the columns are cut into contiguous slabs (host-contiguous in the
+// column-major output) whose y tables worker threads build ahead while the
+// GPU assembles slab s (non-symmetric tiles, x blocks x the slab's y blocks)
+// and the copy engine drains slab s-1.  Pageable destinations go through
+// pinned bounce buffers and a threaded host copy.
+struct SlabTables {
+  std::vector<char> blob;  // descs | yrec | yperm, 256-byte aligned sections
+  size_t o_desc = 0, o_yrec = 0, o_yperm = 0;
+  int64_t ntiles = 0;
+  int slots = 0;
+  bool ready = false;
+  std::exception_ptr err;
+};
+
+template <class T>
+size_t blob_add(std::vector<char>& b, const std::vector<T>& v) {
+  const size_t off = (b.size() + 255) & ~size_t(255);
+  b.resize(off + v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(b.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+int host_threads() {
+  const char* e = std::getenv("GK_THREADS");
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  return std::max(1, e ? std::atoi(e) : std::min(hw, 16));
+}
+
+// Column-slab width for a streamed one-shot call, or 0 for the whole-matrix path.
+int64_t stream_slab_cols(int64_t rows, int64_t cols) {
+  const char* force = std::getenv("GK_SLAB_COLS");
+  if (force) return std::max<int64_t>(0, std::atoll(force));
+  const char* off = std::getenv("GK_STREAM");
+  if (off && std::atoi(off) == 0) return 0;
+  const double total = 16.0 * (double)rows * (double)cols;
+  if (total < 64e6) return 0;
+  const double target = std::min(256e6, std::max(32e6, total / 16.0));
+  int64_t w = (int64_t)(target / (16.0 * (double)rows));
+  w = std::max<int64_t>(64, (w + 63) / 64 * 64);
+  return (cols + w - 1) / w >= 3 ? w : 0;
+}
+
+void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kernel* kernel, const gk_options& o,
+                        gk_cplx* A_host, int64_t lda, int64_t w) {
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gk_stream] %-14s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  const int64_t rows = test->nfree, cols = trial->nfree;
+  const bool helm = kernel->kind == GK_HELMHOLTZ && kernel->k != 0.0;
+  const double k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;
+  const double eps = guard_radius(*test, *trial);
+  const bool same = sides_identical(*test, *trial);
+  Locations X = build_locations(*test, "bem_dense(test)");
+  Locations Y;
+  if (!same) Y = build_locations(*trial, "bem_dense(trial)");
+  lap("locations");
+  const OrderChoice O = choose_order(X, same ? nullptr : &Y, false, eps);
+  const Locations& Yf = same ? X : Y;
+  lap("order");
+  TileTables TX;
+  std::vector<int32_t> xl_id;
+  build_x_tables(X, O.B, TX, xl_id);
+  lap("x tables");
+  DevArena AX;
+  AX.host.reserve((TX.xl_x.size() * 3 + TX.xsup_c.size()) * sizeof(double) +
+                  (TX.xsup_start.size() + TX.xsup_u.size() + X.perm.size()) * sizeof(int32_t) + 8 * 256);
+  const size_t o_xl_x = AX.add(TX.xl_x), o_xl_y = AX.add(TX.xl_y), o_xl_z = AX.add(TX.xl_z),
+               o_xsup_start = AX.add(TX.xsup_start), o_xsup_u = AX.add(TX.xsup_u), o_xsup_c = AX.add(TX.xsup_c),
+               o_xperm = AX.add(X.perm);
+  AX.upload();
+  lap("x upload");
+
+  // ---- slab table builders (look-ahead bounded to keep host memory flat)
+  const int64_t nslab = (cols + w - 1) / w;
+  std::vector<SlabTables> S(nslab);
+  std::mutex m;
+  std::condition_variable cv;
+  int64_t next = 0, consumed = 0;
+  bool stop = false;
+  const int nworkers = (int)std::min<int64_t>(nslab, std::max(1, host_threads() - 1));
+  const int64_t ahead = 2 * nworkers + 2;
+  std::atomic<int64_t> build_us{0};
+  auto build_slab = [&](int64_t s) {
+    const auto b0 = std::chrono::steady_clock::now();
+    SlabTables& T = S[s];
+    const int64_t c0 = s * w, c1 = std::min(cols, c0 + w);
+    std::vector<int32_t> slab_of_full;
+    Locations Ys = restrict_cols(Yf, c0, c1, slab_of_full);
+    set_order(Ys, O.natural);
+    BlockLayout Bs;
+    layout_y_blocks(Ys, Bs);
+    TileTables TY;
+    std::vector<int64_t> yb_start;
+    std::vector<int32_t> yb_list;
+    build_y_tables(Ys, Bs, TY, yb_start, yb_list);
+    Coincidence Cs;
+    Cs.unsafe = O.C.unsafe;
+    if (!Cs.unsafe) {
+      Cs.y_of_x.resize(O.C.y_of_x.size());
+      for (size_t u = 0; u < Cs.y_of_x.size(); ++u) {
+        const int32_t v = O.C.y_of_x[u];
+        Cs.y_of_x[u] = v >= 0 ? slab_of_full[v] : -1;
+      }
+    }
+    build_tile_list(TX, TY, false, Cs, xl_id, yb_start, yb_list);
+    const std::vector<TileDesc> descs = make_tile_descs(TX, TY);
+    T.blob.reserve(descs.size() * sizeof(TileDesc) + TY.yrec.size() * sizeof(YRec) + Ys.perm.size() * 4 + 768);
+    T.o_desc = blob_add(T.blob, descs);
+    T.o_yrec = blob_add(T.blob, TY.yrec);
+    T.o_yperm = blob_add(T.blob, Ys.perm);
+    T.ntiles = (int64_t)descs.size();
+    T.slots = !TY.has_second_slot ? 0 : (TY.equal_coefs ? 2 : 1);
+    build_us += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - b0).count();
+  };
+  std::vector<std::thread> workers;
+  auto stop_workers = [&] {
+    {
+      std::lock_guard<std::mutex> g(m);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : workers) t.join();
+    workers.clear();
+  };
+  for (int t = 0; t < nworkers; ++t)
+    workers.emplace_back([&] {
+      planner_serial(true);
+      for (;;) {
+        int64_t s;
+        {
+          std::unique_lock<std::mutex> g(m);
+          cv.wait(g, [&] { return stop || next >= nslab || next < consumed + ahead; });
+          if (stop || next >= nslab) return;
+          s = next++;
+        }
+        std::exception_ptr err;
+        try {
+          build_slab(s);
+        } catch (...) {
+          err = std::current_exception();
+        }
+        {
+          std::lock_guard<std::mutex> g(m);
+          S[s].err = err;
+          S[s].ready = true;
+        }
+        cv.notify_all();
+      }
+    });
+
+  // ---- device pipeline: tables H2D + kernel on ks, matrix D2H on cs
+  // Streams, events, table staging and slab buffers persist between calls
+  // (one-shot callers repeat; pinned allocations and frees cost milliseconds
+  // and synchronise the device).
+  struct Stage {
+    void* host = nullptr;      // pinned, mapped table staging
+    void* host_dev = nullptr;  // its device view
+    size_t host_bytes = 0;
+    void* dev = nullptr;       // device tables
+    size_t dev_bytes = 0;
+    void* bounce = nullptr;    // pinned bounce buffer (pageable destinations)
+    size_t bounce_bytes = 0;
+    cudaEvent_t h2d = nullptr, kern = nullptr, d2h = nullptr;
+  };
+  struct Resources {
+    Stage st[2];
+    DevBuf slab[2];
+    cudaStream_t ks = nullptr, cs = nullptr;
+  };
+  static std::mutex res_mutex;
+  static Resources R;
+  std::lock_guard<std::mutex> hold(res_mutex);
+  Stage* st = R.st;
+  cudaPointerAttributes pa{};
+  const bool pinned_dst = cudaPointerGetAttributes(&pa, A_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const size_t slab_bytes = sizeof(gk_cplx) * (size_t)rows * (size_t)w;
+  auto cleanup = [&] {
+    stop_workers();
+    if (R.ks) cudaStreamSynchronize(R.ks);
+    if (R.cs) cudaStreamSynchronize(R.cs);
+    cudaGetLastError();
+  };
+  // host copy of a finished pageable slab: bounce -> A_host columns, threaded
+  auto drain = [&](int64_t s) {
+    const Stage& g = st[s & 1];
+    cuda_check(cudaEventSynchronize(g.d2h), "gk_bem_dense D2H");
+    const int64_t c0 = s * w, nc = std::min(cols, c0 + w) - c0;
+    const int nt = (int)std::min<int64_t>(host_threads(), std::max<int64_t>(1, nc / 4));
+    auto copy = [&](int64_t a, int64_t b) {
+      for (int64_t c = a; c < b; ++c)
+        std::memcpy(A_host + (c0 + c) * lda, static_cast<const gk_cplx*>(g.bounce) + c * rows,
+                    sizeof(gk_cplx) * rows);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(copy, nc * t / nt, nc * (t + 1) / nt);
+    copy(0, nc / nt);
+    for (auto& t : pool) t.join();
+  };
+  try {
+    if (!R.ks) cuda_check(cudaStreamCreateWithFlags(&R.ks, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!R.cs) cuda_check(cudaStreamCreateWithFlags(&R.cs, cudaStreamNonBlocking), "cudaStreamCreate");
+    const cudaStream_t ks = R.ks, cs = R.cs;
+    for (DevBuf& b : R.slab)
+      if (b.bytes < slab_bytes) b.alloc(slab_bytes);
+    for (int i = 0; i < 2; ++i) {
+      Stage& g = st[i];
+      for (cudaEvent_t* e : {&g.h2d, &g.kern, &g.d2h})
+        if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+      if (!pinned_dst && g.bounce_bytes < slab_bytes) {
+        if (g.bounce) cudaFreeHost(g.bounce);
+        g.bounce = nullptr;
+        g.bounce_bytes = 0;
+        cuda_check(cudaMallocHost(&g.bounce, slab_bytes), "cudaMallocHost bounce");
+        g.bounce_bytes = slab_bytes;
+      }
+      // the first slab's events must not refer to a previous call's work
+      cuda_check(cudaEventRecord(g.h2d, ks), "cudaEventRecord");
+      cuda_check(cudaEventRecord(g.d2h, cs), "cudaEventRecord");
+    }
+    lap("setup");
+    AsmArgs a;
+    a.xl_x = AX.at<double>(o_xl_x);
+    a.xl_y = AX.at<double>(o_xl_y);
+    a.xl_z = AX.at<double>(o_xl_z);
+    a.xsup_start = AX.at<int32_t>(o_xsup_start);
+    a.xsup_u = AX.at<int32_t>(o_xsup_u);
+    a.xsup_c = AX.at<double>(o_xsup_c);
+    a.xperm = AX.at<int32_t>(o_xperm);
+    a.lda = rows;
+    a.eps2 = eps * eps;
+    a.kappa = 2.0 * k / M_PI;
+    a.symmetric = 0;
+    double wait_ms = 0.0;
+    for (int64_t s = 0; s < nslab; ++s) {
+      {
+        const auto w0 = std::chrono::steady_clock::now();
+        std::unique_lock<std::mutex> g(m);
+        cv.wait(g, [&] { return S[s].ready; });
+        wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+      }
+      if (S[s].err) std::rethrow_exception(S[s].err);
+      Stage& g = st[s & 1];
+      SlabTables& T = S[s];
+      const size_t nb = T.blob.size();
+      if (s >= 2) cuda_check(cudaEventSynchronize(g.h2d), "gk_bem_dense H2D");
+      const size_t nb16 = (nb + 15) & ~size_t(15);
+      if (g.host_bytes < nb16) {
+        cuda_check(cudaStreamSynchronize(ks), "gk_bem_dense");  // the fetch kernels read the old staging
+        if (g.host) cudaFreeHost(g.host);
+        g.host = nullptr;
+        g.host_bytes = 0;
+        const size_t want = std::max<size_t>(nb16 + nb16 / 2, 1 << 20);
+        cuda_check(cudaHostAlloc(&g.host, want, cudaHostAllocMapped | cudaHostAllocPortable),
+                   "cudaHostAlloc staging");
+        g.host_bytes = want;
+        cuda_check(cudaHostGetDevicePointer(&g.host_dev, g.host, 0), "cudaHostGetDevicePointer");
+      }
+      if (g.dev_bytes < nb16) {
+        if (g.dev) cuda_check(cudaFreeAsync(g.dev, ks), "cudaFreeAsync");
+        g.dev = nullptr;
+        g.dev_bytes = 0;
+        const size_t want = std::max<size_t>(nb16 + nb16 / 2, 1 << 20);
+        cuda_check(cudaMallocAsync(&g.dev, want, ks), "cudaMallocAsync tables");
+        g.dev_bytes = want;
+      }
+      std::memcpy(g.host, T.blob.data(), nb);
+      std::vector<char>().swap(T.blob);
+      launch_fetch_tables(g.dev, g.host_dev, nb, ks);
+      cuda_check(cudaEventRecord(g.h2d, ks), "cudaEventRecord");
+      {
+        std::lock_guard<std::mutex> lk(m);
+        consumed = s + 1;
+      }
+      cv.notify_all();
+      if (s >= 2) cuda_check(cudaStreamWaitEvent(ks, g.d2h, 0), "cudaStreamWaitEvent");
+      a.tiles = reinterpret_cast<const TileDesc*>(static_cast<char*>(g.dev) + T.o_desc);
+      a.yrec = reinterpret_cast<const YRec*>(static_cast<char*>(g.dev) + T.o_yrec);
+      a.yperm = reinterpret_cast<const int32_t*>(static_cast<char*>(g.dev) + T.o_yperm);
+      a.A = R.slab[s & 1].p;
+      launch_assemble(a, T.ntiles, helm, T.slots, ks);
+      cuda_check(cudaEventRecord(g.kern, ks), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(cs, g.kern, 0), "cudaStreamWaitEvent");
+      const int64_t c0 = s * w, nc = std::min(cols, c0 + w) - c0;
+      if (pinned_dst) {
+        cuda_check(cudaMemcpy2DAsync(A_host + c0 * lda, sizeof(gk_cplx) * lda, R.slab[s & 1].p,
+                                     sizeof(gk_cplx) * rows, sizeof(gk_cplx) * rows, nc, cudaMemcpyDeviceToHost, cs),
+                   "cudaMemcpy2DAsync D2H");
+      } else {
+        if (s >= 2) drain(s - 2);  // bounce buffer s & 1 is free once slab s-2 is on the host
+        cuda_check(cudaMemcpyAsync(g.bounce, R.slab[s & 1].p, sizeof(gk_cplx) * rows * nc,
+                                   cudaMemcpyDeviceToHost, cs),
+                   "cudaMemcpyAsync D2H");
+      }
+      cuda_check(cudaEventRecord(g.d2h, cs), "cudaEventRecord");
+    }
+    if (!pinned_dst)
+      for (int64_t s = std::max<int64_t>(0, nslab - 2); s < nslab; ++s) drain(s);
+    lap("slabs issued");
+    if (timing) std::fprintf(stderr, "[gk_stream] %lld slabs of %lld cols, %d workers, waited %.2f ms for tables\n",
+                             (long long)nslab, (long long)w, nworkers, wait_ms);
+    cuda_check(cudaStreamSynchronize(cs), "gk_bem_dense");
+    cuda_check(cudaStreamSynchronize(ks), "gk_bem_dense");
+    lap("slabs drained");
+    if (timing) std::fprintf(stderr, "[gk_stream] slab tables: %.2f ms of worker time\n", build_us.load() * 1e-3);
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
 }
 
 }  // namespace
@@ -382,6 +712,21 @@ gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kerne
                    std::chrono::duration<double, std::milli>(t1 - t0).count());
       t0 = t1;
     };
+    if (test && trial && kernel && A_host && test->nfree > 0 && trial->nfree > 0 && lda >= test->nfree) {
+      const int64_t w = stream_slab_cols(test->nfree, trial->nfree);
+      if (w > 0) {
+        check_kernel(kernel);
+        gk_options o;
+        gk_options_default(&o);
+        if (opts) o = *opts;
+        memory_cap(*test, *trial, o);
+        require_device();
+        if (o.symmetric == 1 && !sides_identical(*test, *trial))
+          throw std::invalid_argument("bem_dense: symmetric=1 requires identical test and trial sides");
+        bem_dense_streamed(test, trial, kernel, o, A_host, lda, w);
+        return;
+      }
+    }
     auto P = make_plan(test, trial, kernel, opts);
     lap("plan");
     if (P->rows == 0 || P->cols == 0) return;

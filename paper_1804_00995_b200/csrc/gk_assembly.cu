@@ -258,7 +258,24 @@ void launch_slots(const AsmArgs& a, int64_t ntiles, int slots, cudaStream_t s) {
     launch_one<HELM, 2>(a, ntiles, s);
 }
 
+// Tile tables from mapped pinned host memory into device memory by SM loads:
+// the copy engines stay free for the matrix slabs streaming the other way (a
+// cudaMemcpyAsync of the tables would queue behind the previous slab's D2H).
+__global__ void __launch_bounds__(256) k_fetch_tables(int4* __restrict__ dst, const int4* __restrict__ src,
+                                                      int64_t n16) {
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n16; i += (int64_t)gridDim.x * 256) dst[i] = src[i];
+}
+
 }  // namespace
+
+void launch_fetch_tables(void* dst, const void* src_mapped, size_t bytes, void* stream) {
+  const int64_t n16 = (int64_t)((bytes + 15) / 16);
+  if (n16 == 0) return;
+  const int blocks = (int)std::min<int64_t>(148, (n16 + 255) / 256);
+  k_fetch_tables<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<int4*>(dst), static_cast<const int4*>(src_mapped), n16);
+  cuda_check(cudaGetLastError(), "k_fetch_tables launch");
+}
 
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream) {
   if (ntiles <= 0) return;

@@ -208,6 +208,26 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
 // tiles (natural preferred within 10%: coalesced writes); GK_ORDER=natural|rcb
 // overrides.  Y may be null (symmetric: Y = X).
 TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps);
+// The pieces, for planners that tile one side once and the other in slabs.
+struct OrderChoice {
+  bool natural = true;
+  BlockLayout B;
+  Coincidence C;
+};
+OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps);
+void layout_x_blocks(const Locations& X, BlockLayout& B);
+void layout_y_blocks(const Locations& Y, BlockLayout& B);
+void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, std::vector<int32_t>& xl_id);
+void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std::vector<int64_t>& yb_start,
+                    std::vector<int32_t>& yb_list);
+void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
+                     const std::vector<int32_t>& xl_id, const std::vector<int64_t>& yb_start,
+                     const std::vector<int32_t>& yb_list);
+// Trial locations restricted to dofs [c0, c1) (renumbered from 0, natural
+// order not yet set); slab_of_full maps full location ids to slab ids or -1.
+Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, std::vector<int32_t>& slab_of_full);
+// Run this thread's planner loops serially (slab workers run one slab per thread).
+void planner_serial(bool on);
 
 struct TileDesc {  // everything a k_assemble CTA needs to stage its tile
   int32_t i0, nI;      // x block: first permuted row, rows
@@ -239,6 +259,9 @@ struct AsmArgs {
 };
 // slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream);
+// Copy ceil(bytes/16) 16-byte words from mapped pinned host memory (device
+// view) to device memory with SM loads (both 16-byte aligned and padded).
+void launch_fetch_tables(void* dst, const void* src_mapped, size_t bytes, void* stream);
 
 // ---- matvec ---------------------------------------------------------------------------
 void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,

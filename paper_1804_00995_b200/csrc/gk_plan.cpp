@@ -10,6 +10,7 @@
 #include <numeric>
 #include <cstdlib>
 #include <exception>
+#include <future>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
@@ -264,9 +265,10 @@ int64_t cut(const Locations& L, int64_t start, int64_t end_max) {
 }
 }  // namespace
 
-BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric) {
-  BlockLayout B;
-  const int64_t nrows = X.nfree, ncols = Y.nfree;
+void layout_x_blocks(const Locations& X, BlockLayout& B) {
+  const int64_t nrows = X.nfree;
+  B.xb.clear();
+  B.xloc.clear();
   // ---- x blocks: consecutive permuted rows while their locations fit kUCap,
   // cut back to the strongest order boundary
   std::vector<int64_t> owner(X.size(), -1);
@@ -302,6 +304,12 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
     B.xloc.push_back((int32_t)nloc);
     p = end;
   }
+}
+
+void layout_y_blocks(const Locations& Y, BlockLayout& B) {
+  const int64_t ncols = Y.nfree;
+  B.yb.clear();
+  B.yrec.clear();
   // ---- y blocks: up to kJCap consecutive permuted cols (fewer if their
   // records would exceed kRCap), cut back to the strongest order boundary
   std::vector<int64_t> ystamp(Y.size(), -1);
@@ -343,6 +351,10 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
     B.yrec.push_back((int32_t)nrec);
     q0 = q1;
   }
+}
+
+int64_t layout_pairs(const BlockLayout& B, bool symmetric) {
+  int64_t pairs = 0;
   // ---- evaluated pairs: symmetric plans keep tiles whose last column >= first row
   const int64_t nJb = (int64_t)B.yrec.size();
   std::vector<int64_t> suffix(nJb + 1, 0);
@@ -351,12 +363,21 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
     int64_t first = 0;
     if (symmetric)  // first y block with yb[bj+1] - 1 >= xb[bi]
       first = std::upper_bound(B.yb.begin() + 1, B.yb.end(), B.xb[bi]) - (B.yb.begin() + 1);
-    B.pairs += (int64_t)B.xloc[bi] * suffix[first];
+    pairs += (int64_t)B.xloc[bi] * suffix[first];
   }
+  return pairs;
+}
+
+BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric) {
+  BlockLayout B;
+  layout_x_blocks(X, B);
+  layout_y_blocks(Y, B);
+  B.pairs = layout_pairs(B, symmetric);
   return B;
 }
 
 namespace {
+thread_local bool t_serial = false;  // set by callers that already run one task per thread
 // Static-partition parallel loop over [0, n) on up to GK_THREADS (default:
 // hardware threads, capped at 16) host threads; fn(begin, end) per chunk.
 template <class F>
@@ -366,7 +387,7 @@ void parallel_for(int64_t n, F&& fn) {
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
     return std::max(1, e ? std::atoi(e) : std::min(hw, 16));
   }();
-  const int nt = (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, n / 8));
+  const int nt = t_serial ? 1 : (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, n / 8));
   if (nt <= 1) {
     fn((int64_t)0, n);
     return;
@@ -399,11 +420,9 @@ struct YBlock {  // one y block's records, in descending first-slot order
 };
 }  // namespace
 
-TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
-                       const BlockLayout& B) {
-  TileTables T;
+void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, std::vector<int32_t>& xl_id) {
   const int64_t nrows = X.nfree;
-  const int64_t nIb = (int64_t)B.xb.size() - 1, nJb = (int64_t)B.yb.size() - 1;
+  const int64_t nIb = (int64_t)B.xb.size() - 1;
   // ---- x blocks (boundaries from the layout), built in parallel
   std::vector<XBlock> xb(nIb);
   parallel_for(nIb, [&](int64_t b0, int64_t b1) {
@@ -426,7 +445,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
       }
     }
   });
-  std::vector<int32_t> xl_id;  // global x location id of every block entry (parallel to xl_x)
+  xl_id.clear();  // global x location id of every block entry (parallel to xl_x)
   {
     size_t nl = 0, ns = 0;
     for (const XBlock& XB : xb) {
@@ -463,6 +482,11 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
       T.xb_loc_start.push_back((int32_t)T.xl_x.size());
     }
   }
+}
+
+void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std::vector<int64_t>& yb_start,
+                    std::vector<int32_t>& yb_list) {
+  const int64_t nJb = (int64_t)B.yb.size() - 1;
   // ---- y blocks (boundaries from the layout): records = incident locations,
   // each carrying <= 2 (slot, coef) pairs.  Descending first slot: second
   // slots are larger than first slots, so every second-slot update of a row
@@ -528,8 +552,9 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
     }
   });
   // y location -> y blocks holding it (CSR; a location is listed once per block)
-  std::vector<int64_t> yb_start(Y.size() + 1, 0);
-  std::vector<int32_t> yb_list, last(Y.size(), -1);
+  yb_start.assign(Y.size() + 1, 0);
+  yb_list.clear();
+  std::vector<int32_t> last(Y.size(), -1);
   for (int64_t b = 0; b < nJb; ++b)
     for (int32_t v : yb[b].loc)
       if (last[v] != (int32_t)b) {
@@ -565,9 +590,17 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
     T.yb_dof_start.push_back((int32_t)B.yb[b + 1]);
     T.yb_rec_start.push_back((int32_t)T.yrec.size());
   }
-  T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
-  T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
+}
 
+void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
+                     const std::vector<int32_t>& xl_id, const std::vector<int64_t>& yb_start,
+                     const std::vector<int32_t>& yb_list) {
+  const int64_t nIb = (int64_t)TX.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
+  T.tile_i.clear();
+  T.tile_j.clear();
+  T.mtile_i.clear();
+  T.mtile_j.clear();
+  T.pairs_evaluated = 0;
   // ---- which tiles can hold a coincident (masked) pair?  With only exact
   // coincidences (find_coincidences), a tile needs the mask iff one of its x
   // locations coincides with one of its y records' locations.
@@ -576,7 +609,7 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
   if (!unsafe)
     parallel_for(nIb, [&](int64_t b0, int64_t b1) {
       for (int64_t bi = b0; bi < b1; ++bi) {
-        for (int32_t e = T.xb_loc_start[bi]; e < T.xb_loc_start[bi + 1]; ++e) {
+        for (int32_t e = TX.xb_loc_start[bi]; e < TX.xb_loc_start[bi + 1]; ++e) {
           const int32_t v = C.y_of_x[xl_id[e]];
           if (v >= 0)
             masked_j[bi].insert(masked_j[bi].end(), yb_list.begin() + yb_start[v], yb_list.begin() + yb_start[v + 1]);
@@ -588,16 +621,29 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
   for (int64_t bi = 0; bi < nIb; ++bi) {
     int64_t first = 0;
     if (symmetric)
-      first = std::upper_bound(T.yb_dof_start.begin() + 1, T.yb_dof_start.end(), T.xb_dof_start[bi]) -
+      first = std::upper_bound(T.yb_dof_start.begin() + 1, T.yb_dof_start.end(), TX.xb_dof_start[bi]) -
               (T.yb_dof_start.begin() + 1);
     for (int64_t bj = first; bj < nJb; ++bj) {
       const bool m = unsafe || std::binary_search(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)bj);
       (m ? T.mtile_i : T.tile_i).push_back((int32_t)bi);
       (m ? T.mtile_j : T.tile_j).push_back((int32_t)bj);
-      T.pairs_evaluated += (int64_t)(T.xb_loc_start[bi + 1] - T.xb_loc_start[bi]) *
+      T.pairs_evaluated += (int64_t)(TX.xb_loc_start[bi + 1] - TX.xb_loc_start[bi]) *
                            (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
     }
   }
+}
+
+TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
+                       const BlockLayout& B) {
+  TileTables T;
+  std::vector<int32_t> xl_id;
+  std::vector<int64_t> yb_start;
+  std::vector<int32_t> yb_list;
+  build_x_tables(X, B, T, xl_id);
+  build_y_tables(Y, B, T, yb_start, yb_list);
+  T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
+  T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
+  build_tile_list(T, T, symmetric, C, xl_id, yb_start, yb_list);
   return T;
 }
 
@@ -651,7 +697,9 @@ Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same,
   return C;
 }
 
-TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps) {
+void planner_serial(bool on) { t_serial = on; }
+
+OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps) {
   const char* force = std::getenv("GK_ORDER");
   const std::string f = force ? force : "";
   const bool timing = std::getenv("GK_TIMING") != nullptr;
@@ -663,37 +711,98 @@ TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, dou
                  std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  const Coincidence C = find_coincidences(X, Y ? *Y : X, Y == nullptr, eps);
-  lap("coincidences");
-  auto order = [&](bool natural) {
-    set_order(X, natural);
-    if (Y) set_order(*Y, natural);
-    lap(natural ? "order natural" : "order rcb");
-    BlockLayout B = layout_blocks(X, Y ? *Y : X, symmetric);
-    lap("layout");
-    return B;
-  };
+  // The coincidence sweep and the two candidate orders are independent (the
+  // sweep reads coordinates only; RCB works on copies), so they run
+  // concurrently; build_locations left X and Y in natural order.
+  auto sweep = std::async(std::launch::async, [&] { return find_coincidences(X, Y ? *Y : X, Y == nullptr, eps); });
+  auto layout_of = [&](Locations& Lx, Locations* Ly) { return layout_blocks(Lx, Ly ? *Ly : Lx, symmetric); };
   bool natural;
   BlockLayout B;
-  if (f == "natural" || f == "rcb") {
-    natural = f == "natural";
-    B = order(natural);
+  if (f == "natural") {
+    natural = true;
+    B = layout_of(X, Y);
+  } else if (f == "rcb") {
+    natural = false;
+    set_order(X, false);
+    if (Y) set_order(*Y, false);
+    B = layout_of(X, Y);
   } else {
     // Natural order keeps the rows of every tile contiguous in A (full-sector,
     // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
     // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
-    BlockLayout rcb = order(false);
-    B = order(true);
-    natural = (double)B.pairs <= 1.10 * (double)rcb.pairs;
+    Locations Xr = X, Yr;
+    if (Y) Yr = *Y;
+    auto rcb = std::async(std::launch::async, [&] {
+      set_order(Xr, false);
+      if (Y) set_order(Yr, false);
+      return layout_of(Xr, Y ? &Yr : nullptr);
+    });
+    B = layout_of(X, Y);
+    BlockLayout Br = rcb.get();
+    natural = (double)B.pairs <= 1.10 * (double)Br.pairs;
     if (!natural) {
-      set_order(X, false);  // restore the RCB numbering the layout refers to
-      if (Y) set_order(*Y, false);
-      B = std::move(rcb);
+      X = std::move(Xr);
+      if (Y) *Y = std::move(Yr);
+      B = std::move(Br);
     }
   }
-  TileTables T = build_tiles(X, Y ? *Y : X, symmetric, C, B);
-  lap("tiles");
+  OrderChoice O;
+  O.C = sweep.get();
+  O.natural = natural;
+  O.B = std::move(B);
+  lap(natural ? "coincidences+orders (natural)" : "coincidences+orders (rcb)");
+  return O;
+}
+
+TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps) {
+  const OrderChoice O = choose_order(X, Y, symmetric, eps);
+  const auto t0 = std::chrono::steady_clock::now();
+  TileTables T = build_tiles(X, Y ? *Y : X, symmetric, O.C, O.B);
+  if (std::getenv("GK_TIMING"))
+    std::fprintf(stderr, "[gk_plan]   %-20s %8.2f ms\n", "tiles",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   return T;
+}
+
+Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, std::vector<int32_t>& slab_of_full) {
+  // the trial locations supporting dofs [c0, c1), in increasing location id,
+  // with only those dofs' contributions (renumbered from 0)
+  Locations S;
+  S.nfree = c1 - c0;
+  slab_of_full.assign(Y.size(), -1);
+  std::vector<int32_t> locs;
+  for (int64_t d = c0; d < c1; ++d) {
+    const int64_t q = Y.iperm[d];
+    for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
+      const int32_t v = Y.dloc[s];
+      if (slab_of_full[v] < 0) {
+        slab_of_full[v] = 0;
+        locs.push_back(v);
+      }
+    }
+  }
+  std::sort(locs.begin(), locs.end());
+  const size_t n = locs.size();
+  S.x.resize(n);
+  S.y.resize(n);
+  S.z.resize(n);
+  S.cstart.assign(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const int32_t v = locs[i];
+    slab_of_full[v] = (int32_t)i;
+    S.x[i] = Y.x[v];
+    S.y[i] = Y.y[v];
+    S.z[i] = Y.z[v];
+    for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
+      const int64_t d = Y.cdof[c];
+      if (d >= c0 && d < c1) {
+        S.cdof.push_back((int32_t)(d - c0));
+        S.ccoef.push_back(Y.ccoef[c]);
+      }
+    }
+    S.cstart[i + 1] = (int64_t)S.cdof.size();
+  }
+  return S;
 }
 
 }  // namespace gk

@@ -4,8 +4,11 @@
 // the reference algorithm; all pair/contraction work goes to the device.
 #include "galerk.hpp"
 
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -450,6 +453,24 @@ MatrixXcd product(const SideTables& tst, const Kernel& kernel, const SideTables&
   return A;
 }
 }  // namespace
+
+MatrixXcd::MatrixXcd(int64_t r, int64_t c) : rows_(r), cols_(c) {
+  const size_t bytes = sizeof(cplx) * (size_t)r * (size_t)c;
+  if (bytes == 0) return;
+  constexpr size_t kHuge = size_t(2) << 20;
+  void* p = nullptr;
+  if (bytes >= kHuge) {
+    const size_t padded = (bytes + kHuge - 1) / kHuge * kHuge;
+    p = std::aligned_alloc(kHuge, padded);
+    if (p) madvise(p, padded, MADV_HUGEPAGE);
+  } else {
+    p = std::malloc(bytes);
+  }
+  if (!p) throw std::bad_alloc();
+  data_.reset(static_cast<cplx*>(p));
+}
+
+void MatrixXcd::Free::operator()(cplx* p) const { std::free(p); }
 
 MatrixXcd bem_dense(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const Kernel& kernel,
                     const FemSpace& trial, const BemOptions& opts) {

@@ -131,20 +131,26 @@ struct BemOptions {
 };
 
 // Column-major complex128 matrix, storage identical to Eigen::MatrixXcd.
+// Storage is left uninitialised (every producer writes all entries) and large
+// matrices are 2 MB aligned and advised for transparent huge pages, so the
+// first touch of a 1.7 GB matrix takes ~800 page faults instead of ~400k.
 class MatrixXcd {
  public:
   MatrixXcd() = default;
-  MatrixXcd(int64_t r, int64_t c) : rows_(r), cols_(c), data_((size_t)(r * c)) {}
+  MatrixXcd(int64_t r, int64_t c);
   int64_t rows() const { return rows_; }
   int64_t cols() const { return cols_; }
   cplx& operator()(int64_t i, int64_t j) { return data_[(size_t)(i + j * rows_)]; }
   const cplx& operator()(int64_t i, int64_t j) const { return data_[(size_t)(i + j * rows_)]; }
-  cplx* data() { return data_.data(); }
-  const cplx* data() const { return data_.data(); }
+  cplx* data() { return data_.get(); }
+  const cplx* data() const { return data_.get(); }
 
  private:
+  struct Free {
+    void operator()(cplx* p) const;
+  };
   int64_t rows_ = 0, cols_ = 0;
-  std::vector<cplx> data_;
+  std::unique_ptr<cplx[], Free> data_;
 };
 
 // CSC sparse matrix with setFromTriplets semantics (duplicates summed in order).

@@ -21,6 +21,11 @@ for it in range(int(os.environ.get("CALLS", "3"))):
     t = time.perf_counter()
     g.bem_dense_into(dom, dom, sp, kern, sp, g.BemOptions(), host.data_ptr(), n)
     print(f"call {it}: {1e3 * (time.perf_counter() - t):.2f} ms", flush=True)
+for it in range(int(os.environ.get("PAGEABLE_CALLS", "2"))):
+    t = time.perf_counter()
+    A = g.bem_dense(dom, dom, sp, kern, sp)
+    print(f"pageable call {it} (bem_dense -> new numpy matrix): {1e3 * (time.perf_counter() - t):.2f} ms", flush=True)
+    del A
 dev = torch.empty(n * n, dtype=torch.complex128, device="cuda")
 for it in range(3):
     torch.cuda.synchronize()
