@@ -396,7 +396,7 @@ def e2e_dense(g, torch, dom, space, kern, opts, n, pairs_ref, steps):
     t = float(np.median(ts))
     return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 16 * n * n, "s_per_step": t,
-            "path": "gk_bem_dense (C-ABI, host sides -> pinned host matrix)"}
+            "path": "gk_bem_dense (C-ABI, host sides -> pinned host matrix; column slabs streamed: tables built ahead, D2H overlapped)"}
 
 
 def cpu_baseline(spec, mesh, k, name, gpu_ms_step):
