@@ -136,7 +136,35 @@ struct YTri {
   double len[3];
   double r0min[3];  // 1e-28 len^2 (the log guard, kernels.cpp:184); +inf for an empty edge
   V3 g_bary[3];  // P1 tangential barycentric gradients (femspace.cpp:254-277)
+  // in-plane frame for the batched kernel: origin v[0], axes e1 = s_hat[0],
+  // e2 = n x e1, e3 = n; the triangle is P0 = 0, P1 = (len0, 0), P2
+  V3 e1, e2;
+  double p2x, p2y;
+  double s2x[3], s2y[3];   // edge unit vectors in the plane; m_hat = (s2y, -s2x)
+  double area2;            // |(B - A) x (C - A)|
+  double g2x[3], g2y[3];   // in-plane barycentric gradients (P1)
 };
+
+struct V2 {
+  double x, y;
+};
+
+// Fill the in-plane frame of T (after v, n, s_hat, len, g_bary).
+__device__ __forceinline__ void frame2(YTri& T, double area2, bool p1) {
+  T.e1 = T.s_hat[0];
+  T.e2 = cross(T.n, T.e1);
+  const V3 c = T.v[2] - T.v[0];
+  T.p2x = dot(c, T.e1);
+  T.p2y = dot(c, T.e2);
+  T.area2 = area2;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    T.s2x[i] = dot(T.s_hat[i], T.e1);
+    T.s2y[i] = dot(T.s_hat[i], T.e2);
+    T.g2x[i] = p1 ? dot(T.g_bary[i], T.e1) : 0.0;
+    T.g2y[i] = p1 ? dot(T.g_bary[i], T.e2) : 0.0;
+  }
+}
 
 struct NfArgs {
   int64_t npairs;
@@ -213,6 +241,75 @@ __device__ __forceinline__ void analytic(const YTri& T, V3 x, double& newton, V3
     for (int i = 0; i < 3; ++i)
       if (T.len[i] > 1e-300) mom = mom + mo[i] * (0.5 * T.m_hat[i]);
     moment = mom;
+  }
+}
+
+// analytic() in the y triangle's in-plane frame: x = (u, v, w) local.  With
+// A_i = v_i - x = (a_i, b_i, -w): every edge dot product is a 2D one, the
+// normal offset w0 is w, and the triple product of the solid angle is the
+// constant -w |(B-A) x (C-A)|.  The moment is returned in-plane.
+template <bool MOMENT>
+__device__ __forceinline__ void analytic2(const YTri& T, double u, double v, double w, double& newton, V2& moment) {
+  const double a[3] = {-u, T.len[0] - u, T.p2x - u};
+  const double b[3] = {-v, -v, T.p2y - v};
+  const double w2 = w * w;
+  double rv[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double r2 = fma(a[i], a[i], fma(b[i], b[i], w2));
+    rv[i] = r2 > 0.0 ? r2 * gk::rsqrt_refined(r2) : 0.0;
+  }
+  const double d01 = fma(a[0], a[1], fma(b[0], b[1], w2));
+  const double d02 = fma(a[0], a[2], fma(b[0], b[2], w2));
+  const double d12 = fma(a[1], a[2], fma(b[1], b[2], w2));
+  const double trip = -w * T.area2;
+  const double vden = fma(rv[0] * rv[1], rv[2], fma(d01, rv[2], fma(d02, rv[1], d12 * rv[0])));
+  const double omega = 2.0 * atan2_fast(trip, vden);
+  double f[3], t[3], mo[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int ip = i == 2 ? 0 : i + 1;
+    const double sx = T.s2x[i], sy = T.s2y[i];
+    const double ti = fma(a[i], sy, -b[i] * sx);  // (a, b) . m, m = (sy, -sx)
+    const double sm = fma(a[i], sx, b[i] * sy);
+    const double sp = fma(a[ip], sx, b[ip] * sy);
+    const double rm = rv[i], rp = rv[ip];
+    const double r0sq = fma(ti, ti, w2);
+    const bool ca = sm >= 0.0, cb = sp <= 0.0;
+    const double num = ca ? rp + sp : (cb ? rm - sm : (rp + sp) * (rm - sm));
+    const double den = ca ? rm + sm : (cb ? rp - sp : r0sq);
+    const bool ok = r0sq > T.r0min[i];
+    f[i] = ok ? log_ratio(num, den) : 0.0;
+    t[i] = T.len[i] > 1e-300 ? ti : 0.0;
+    if (MOMENT) mo[i] = r0sq * f[i] + sp * rp - sm * rm;
+  }
+  newton = (t[0] * f[0] + t[1] * f[1] + t[2] * f[2]) + w * omega;
+  if (MOMENT) {
+    V2 m = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (T.len[i] > 1e-300) {
+        const double h = 0.5 * mo[i];
+        m.x = fma(h, T.s2y[i], m.x);
+        m.y = fma(-h, T.s2x[i], m.y);
+      }
+    moment = m;
+  }
+}
+
+// exact_values() from analytic2: lam at rho = (u, v) is affine in the plane
+// (lam_0 = 1 + g_0.(u,v), lam_j = g_j.(u,v)), the moment term a 2D dot.
+template <int NT, int NTR>
+__device__ __forceinline__ void exact_values2(const YTri& T, double newton, V2 mom, double u, double v,
+                                              double d[NTR]) {
+  if (NTR == 1) {
+    d[0] = newton;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NTR; ++j) {
+      const double lam = (j == 0 ? 1.0 : 0.0) + fma(T.g2x[j], u, T.g2y[j] * v);
+      d[j] = fma(lam, newton, fma(T.g2x[j], mom.x, T.g2y[j] * mom.y));
+    }
   }
 }
 
@@ -324,6 +421,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
         T.g_bary[2] = mk(e1.x * i01 + e2.x * i11, e1.y * i01 + e2.y * i11, e1.z * i01 + e2.z * i11);
         T.g_bary[0] = mk(0, 0, 0) - T.g_bary[1] - T.g_bary[2];
       }
+      frame2(T, area2, NTR == 3);
     }
     __syncwarp();
     const YTri& T = S.tri;
@@ -333,6 +431,16 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
       xv[c] = mk(a.xv[3 * vi], a.xv[3 * vi + 1], a.xv[3 * vi + 2]);
     }
     const double measure_x = 0.5 * nrm(cross(xv[1] - xv[0], xv[2] - xv[0]));
+    // x-triangle vertices in the y triangle's frame: every rule point is then
+    // (u, v, w) = sum b_c X_c and the analytic integral works in 2D
+    double Xu[3], Xv[3], Xw[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const V3 d = xv[c] - T.v[0];
+      Xu[c] = dot(d, T.e1);
+      Xv[c] = dot(d, T.e2);
+      Xw[c] = dot(d, T.n);
+    }
 
     // ---- Gauss x Gauss part (assembly.cpp:659-674, YContext::gauss :504-543)
     if (lane < a.gx) {
@@ -374,13 +482,15 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
     {
       if (lane < 7) {
         const double* b = c_r7_bary[lane];
-        const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
+        const double u = b[0] * Xu[0] + b[1] * Xu[1] + b[2] * Xu[2];
+        const double v = b[0] * Xv[0] + b[1] * Xv[1] + b[2] * Xv[2];
+        const double wn = b[0] * Xw[0] + b[1] * Xw[1] + b[2] * Xw[2];
         const double w = c_r7_w[lane] * (measure_x * 1.0);
         double nw;
-        V3 mo, rho;
-        analytic<NTR == 3>(T, x, nw, mo, rho);
+        V2 mo;
+        analytic2<NTR == 3>(T, u, v, wn, nw, mo);
         double d[NTR];
-        exact_values<NT, NTR>(T, nw, mo, rho, d);
+        exact_values2<NT, NTR>(T, nw, mo, u, v, d);
 #pragma unroll
         for (int i = 0; i < NT; ++i)
 #pragma unroll
@@ -454,13 +564,15 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
 #pragma unroll
           for (int c = 0; c < 3; ++c)
             b[c] = c_r7_bary[q][0] * cr[c] + c_r7_bary[q][1] * cr[3 + c] + c_r7_bary[q][2] * cr[6 + c];
-          const V3 x = b[0] * xv[0] + b[1] * xv[1] + b[2] * xv[2];
+          const double u = b[0] * Xu[0] + b[1] * Xu[1] + b[2] * Xu[2];
+          const double v = b[0] * Xv[0] + b[1] * Xv[1] + b[2] * Xv[2];
+          const double wn = b[0] * Xw[0] + b[1] * Xw[1] + b[2] * Xw[2];
           const double w = c_r7_w[q] * (measure_x * frac);
           double nw;
-          V3 mo, rho;
-          analytic<NTR == 3>(T, x, nw, mo, rho);
+          V2 mo;
+          analytic2<NTR == 3>(T, u, v, wn, nw, mo);
           double d[NTR];
-          exact_values<NT, NTR>(T, nw, mo, rho, d);
+          exact_values2<NT, NTR>(T, nw, mo, u, v, d);
 #pragma unroll
           for (int i = 0; i < NT; ++i)
 #pragma unroll
