@@ -203,8 +203,13 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   double2* A = reinterpret_cast<double2*>(a.A);
   const long long lda = a.lda;
   const int items = nI * ((nJ + kGC - 1) / kGC);
-  for (int e = t; e < items; e += kAsmThreads) {
-    const int ii = e % nI, jb = (e / nI) * kGC;
+  // item e = (row e % nI, column group e / nI), advanced incrementally: one
+  // integer division per thread instead of two per item
+  const int nIs = max(nI, 1);  // items = 0 when nI = 0
+  const int di = kAsmThreads % nIs, dg = kAsmThreads / nIs;
+  int ii = t % nIs, jb = (t / nIs) * kGC;
+  for (int e = t; e < items; e += kAsmThreads, ii += di, jb += dg * kGC) {
+    if (ii >= nI) ii -= nI, jb += kGC;
     const int pi = i0 + ii;
     if (a.symmetric && pi > j0 + min(jb + kGC, nJ) - 1) continue;  // whole group below the diagonal
     double re[kGC], im[kGC];

@@ -66,9 +66,9 @@ __device__ __forceinline__ double div_fast(double d, double sg) {
 // atan2(y, x) without special-value branches: t = min/max(|x|,|y|) in [0,1]
 // is shifted to the nearest of the angles 0, pi/8, pi/4 (atan t = theta +
 // atan((t - c)/(1 + t c)), c = tan theta, evaluated from min and max so there
-// is one division), leaving |s| <= tan(pi/16); atan s = s + s z P(z) with the
-// Taylor coefficients (-1)^k/(2k+1), k = 1..11 (truncation < 2e-17 relative).
-// <= 1 ulp against a 40-digit reference on 3e4 random arguments.  atan2(0,0) = 0.
+// is one division), leaving |s| <= tan(pi/16); atan s = s + s z P(z) with P
+// the degree-7 Chebyshev interpolant in z (tools/derive_logatan.py: 0.51 ulp,
+// as the 11-term Taylor series it replaces).  atan2(0,0) = 0.
 __device__ __forceinline__ double atan2_fast(double y, double x) {
   const double ax = fabs(x), ay = fabs(y);
   const double mx = fmax(ax, ay), mn = fmin(ax, ay);
@@ -77,17 +77,14 @@ __device__ __forceinline__ double atan2_fast(double y, double x) {
   const double th = hi ? 0.7853981633974483 : (mid ? 0.39269908169872414 : 0.0);
   const double s = div_fast(fma(-c, mx, mn), fma(c, mn, mx));
   const double z = s * s;
-  double p = -1.0 / 23.0;
-  p = fma(p, z, 1.0 / 21.0);
-  p = fma(p, z, -1.0 / 19.0);
-  p = fma(p, z, 1.0 / 17.0);
-  p = fma(p, z, -1.0 / 15.0);
-  p = fma(p, z, 1.0 / 13.0);
-  p = fma(p, z, -1.0 / 11.0);
-  p = fma(p, z, 1.0 / 9.0);
-  p = fma(p, z, -1.0 / 7.0);
-  p = fma(p, z, 1.0 / 5.0);
-  p = fma(p, z, -1.0 / 3.0);
+  double p = 0.05115745967981171;
+  p = fma(p, z, -0.06618732486766733);
+  p = fma(p, z, 0.07690724472468718);
+  p = fma(p, z, -0.0909087995193466);
+  p = fma(p, z, 0.11111110818998077);
+  p = fma(p, z, -0.1428571428427355);
+  p = fma(p, z, 0.1999999999999729);
+  p = fma(p, z, -0.3333333333333333);
   double a = th + fma(s * z, p, s);
   a = ay > ax ? 1.5707963267948966 - a : a;
   a = x < 0.0 ? 3.141592653589793 - a : a;
@@ -100,7 +97,9 @@ __device__ __forceinline__ double atan2_fast(double y, double x) {
 // so that mn / md lies in [1/sqrt2, sqrt2), then
 //   log(num/den) = k ln2 + log((1+s)/(1-s)),  s = (mn - md) / (mn + md),
 // |s| <= 0.1716, and log((1+s)/(1-s)) = 2s + s z R(z), z = s^2, with R the
-// atanh series 2/3 + 2z/5 + ... + 2z^8/19 (truncation < 1e-17 relative).
+// degree-6 Chebyshev interpolant in z of (log((1+s)/(1-s)) - 2s)/(s z)
+// (tools/derive_logatan.py: 0.52 ulp, against 0.63 for the 9-term atanh
+// series it replaces).
 // mn - md is exact (Sterbenz).  ~1-2 ulp; one division instead of a division
 // plus the library log's own reduction.
 __device__ __forceinline__ double log_ratio(double num, double den) {
@@ -114,15 +113,13 @@ __device__ __forceinline__ double log_ratio(double num, double den) {
   k += up ? 1 : (dn ? -1 : 0);
   const double s = div_fast(mn - md, mn + md);  // mn + md in [1.7, 6)
   const double z = s * s;
-  double r = 2.0 / 19.0;
-  r = fma(r, z, 2.0 / 17.0);
-  r = fma(r, z, 2.0 / 15.0);
-  r = fma(r, z, 2.0 / 13.0);
-  r = fma(r, z, 2.0 / 11.0);
-  r = fma(r, z, 2.0 / 9.0);
-  r = fma(r, z, 2.0 / 7.0);
-  r = fma(r, z, 2.0 / 5.0);
-  r = fma(r, z, 2.0 / 3.0);
+  double r = 0.14616449685043406;
+  r = fma(r, z, 0.15331721600556042);
+  r = fma(r, z, 0.18182889125261723);
+  r = fma(r, z, 0.2222221113479508);
+  r = fma(r, z, 0.28571428625975487);
+  r = fma(r, z, 0.39999999999899505);
+  r = fma(r, z, 0.666666666666667);
   const double kd = (double)k;
   const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
   return fma(kd, ln2_hi, 2.0 * s + fma(s * z, r, kd * ln2_lo));

@@ -63,8 +63,9 @@ def check(P, Q, n=20001):
 
 
 if __name__ == "__main__":
-    P = cheb_fit(p_fun, 7)
-    Q = cheb_fit(q_fun, 8)
+    # degrees used by gk_math.cuh: P degree 6 (7 terms), Q degree 6 (7 terms)
+    P = cheb_fit(p_fun, 6)
+    Q = cheb_fit(q_fun, 6)
     ws, wc = check(P, Q, 4001)
     print("max abs err sin %.3e cos %.3e" % (ws, wc))
     for name, cs in (("P", P), ("Q", Q)):
