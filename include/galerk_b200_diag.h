@@ -31,6 +31,17 @@ gk_status gk_diag_probe_pairs(int64_t n, const double* x, const double* y, const
 gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const double* z, double k,
                              double eps, gk_cplx* out, gk_stream stream);
 
+/* Device math accuracy probe: out[i] = f(a[i], b[i]) for one scalar helper of
+ * the kernels (gk_math.cuh), on device arrays; b may be NULL for unary f.
+ *   GK_MATH_LOG_RATIO   log(a / b)            (near-field edge logs, K3)
+ *   GK_MATH_ATAN2       atan2(a, b)           (solid angle, K3)
+ *   GK_MATH_DIV         a / b, b > 0          (K3 reductions)
+ *   GK_MATH_SIN_QUARTER sin(pi a / 2)         (phase of the pair kernel)
+ *   GK_MATH_COS_QUARTER cos(pi a / 2)
+ *   GK_MATH_RSQRT       1 / sqrt(a)           (1/r of every kernel) */
+enum { GK_MATH_LOG_RATIO = 0, GK_MATH_ATAN2, GK_MATH_DIV, GK_MATH_SIN_QUARTER, GK_MATH_COS_QUARTER, GK_MATH_RSQRT };
+gk_status gk_diag_math(int32_t fn, int64_t n, const double* a, const double* b, double* out, gk_stream stream);
+
 /* Host-only dry run of gk_plan_create (no device needed): fills the plan
  * statistics (locations, tiles, evaluated vs unique pairs) so the tiling can
  * be inspected and tested on a CPU-only machine. */

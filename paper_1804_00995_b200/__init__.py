@@ -70,6 +70,7 @@ bem_dense_into = _native.bem_dense_into
 diag_fp64_peak = _native.diag_fp64_peak
 plan_info_dry = _native.plan_info_dry
 diag_probe_pairs = _native.diag_probe_pairs
+diag_math = _native.diag_math
 last_error = _native.last_error
 version = _native.version
 FP64 = _native.FP64

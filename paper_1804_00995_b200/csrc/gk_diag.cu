@@ -67,6 +67,26 @@ __global__ void __launch_bounds__(256) k_fast(long long n, const double* __restr
   out[i] = make_double2(re, im);
 }
 
+
+// Device math accuracy probe: one scalar helper of gk_math.cuh per element.
+__global__ void __launch_bounds__(256) k_math(int fn, long long n, const double* __restrict__ a,
+                                              const double* __restrict__ b, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = a[i], y = b ? b[i] : 0.0;
+  double r = 0.0, s, c;
+  switch (fn) {
+    case GK_MATH_LOG_RATIO: r = log_ratio(x, y); break;
+    case GK_MATH_ATAN2: r = atan2_fast(x, y); break;
+    case GK_MATH_DIV: r = div_fast(x, y); break;
+    case GK_MATH_SIN_QUARTER: sincos_quarter(x, s, c); r = s; break;
+    case GK_MATH_COS_QUARTER: sincos_quarter(x, s, c); r = c; break;
+    case GK_MATH_RSQRT: r = rsqrt_refined(x); break;
+    default: break;
+  }
+  out[i] = r;
+}
+
 }  // namespace
 }  // namespace gk
 
@@ -119,6 +139,16 @@ gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const 
     k_fast<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         n, x, y, z, 2.0 * k / M_PI, eps * eps, reinterpret_cast<double2*>(out));
     cuda_check(cudaGetLastError(), "k_fast");
+  });
+}
+
+gk_status gk_diag_math(int32_t fn, int64_t n, const double* a, const double* b, double* out, gk_stream stream) {
+  return guard([&] {
+    require_device();
+    if (fn < GK_MATH_LOG_RATIO || fn > GK_MATH_RSQRT) throw std::invalid_argument("gk_diag_math: unknown function");
+    if (n <= 0) return;
+    k_math<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(fn, n, a, b, out);
+    cuda_check(cudaGetLastError(), "k_math");
   });
 }
 

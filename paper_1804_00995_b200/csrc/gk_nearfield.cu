@@ -52,78 +52,8 @@ __device__ __forceinline__ double nrm_fast(V3 a) {
   return r2 > 0.0 ? r2 * gk::rsqrt_refined(r2) : 0.0;
 }
 
-// q = d / sg for sg > 0 in the normal range: MUFU.RCP64H + two Newton steps +
-// one residual correction of the quotient (~0.5 ulp, no slow path).
-__device__ __forceinline__ double div_fast(double d, double sg) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(sg));
-  y = fma(y, fma(-sg, y, 1.0), y);
-  y = fma(y, fma(-sg, y, 1.0), y);
-  const double q0 = d * y;
-  return fma(fma(-sg, q0, d), y, q0);
-}
-
-// atan2(y, x) without special-value branches: t = min/max(|x|,|y|) in [0,1]
-// is shifted to the nearest of the angles 0, pi/8, pi/4 (atan t = theta +
-// atan((t - c)/(1 + t c)), c = tan theta, evaluated from min and max so there
-// is one division), leaving |s| <= tan(pi/16); atan s = s + s z P(z) with P
-// the degree-7 Chebyshev interpolant in z (tools/derive_logatan.py: 0.51 ulp,
-// as the 11-term Taylor series it replaces).  atan2(0,0) = 0.
-__device__ __forceinline__ double atan2_fast(double y, double x) {
-  const double ax = fabs(x), ay = fabs(y);
-  const double mx = fmax(ax, ay), mn = fmin(ax, ay);
-  const bool hi = mn > 0.6681786379192989 * mx, mid = !hi && mn > 0.198912367379658 * mx;
-  const double c = hi ? 1.0 : (mid ? 0.41421356237309503 : 0.0);
-  const double th = hi ? 0.7853981633974483 : (mid ? 0.39269908169872414 : 0.0);
-  const double s = div_fast(fma(-c, mx, mn), fma(c, mn, mx));
-  const double z = s * s;
-  double p = 0.05115745967981171;
-  p = fma(p, z, -0.06618732486766733);
-  p = fma(p, z, 0.07690724472468718);
-  p = fma(p, z, -0.0909087995193466);
-  p = fma(p, z, 0.11111110818998077);
-  p = fma(p, z, -0.1428571428427355);
-  p = fma(p, z, 0.1999999999999729);
-  p = fma(p, z, -0.3333333333333333);
-  double a = th + fma(s * z, p, s);
-  a = ay > ax ? 1.5707963267948966 - a : a;
-  a = x < 0.0 ? 3.141592653589793 - a : a;
-  a = mx > 0.0 ? a : 0.0;
-  return y < 0.0 ? -a : a;
-}
-
-// log(num / den) for positive normal num, den without forming the quotient:
-// num = mn 2^en, den = md 2^ed with mn, md in [1, 2); one of them is doubled
-// so that mn / md lies in [1/sqrt2, sqrt2), then
-//   log(num/den) = k ln2 + log((1+s)/(1-s)),  s = (mn - md) / (mn + md),
-// |s| <= 0.1716, and log((1+s)/(1-s)) = 2s + s z R(z), z = s^2, with R the
-// degree-6 Chebyshev interpolant in z of (log((1+s)/(1-s)) - 2s)/(s z)
-// (tools/derive_logatan.py: 0.52 ulp, against 0.63 for the 9-term atanh
-// series it replaces).
-// mn - md is exact (Sterbenz).  ~1-2 ulp; one division instead of a division
-// plus the library log's own reduction.
-__device__ __forceinline__ double log_ratio(double num, double den) {
-  const int hn = __double2hiint(num), hd = __double2hiint(den);
-  int k = ((hn >> 20) & 0x7ff) - ((hd >> 20) & 0x7ff);
-  double mn = __hiloint2double((hn & 0x800fffff) | 0x3ff00000, __double2loint(num));
-  double md = __hiloint2double((hd & 0x800fffff) | 0x3ff00000, __double2loint(den));
-  const bool up = mn > 1.4142135623730951 * md, dn = mn < 0.7071067811865476 * md;
-  md = up ? 2.0 * md : md;
-  mn = dn ? 2.0 * mn : mn;
-  k += up ? 1 : (dn ? -1 : 0);
-  const double s = div_fast(mn - md, mn + md);  // mn + md in [1.7, 6)
-  const double z = s * s;
-  double r = 0.14616449685043406;
-  r = fma(r, z, 0.15331721600556042);
-  r = fma(r, z, 0.18182889125261723);
-  r = fma(r, z, 0.2222221113479508);
-  r = fma(r, z, 0.28571428625975487);
-  r = fma(r, z, 0.39999999999899505);
-  r = fma(r, z, 0.666666666666667);
-  const double kd = (double)k;
-  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
-  return fma(kd, ln2_hi, 2.0 * s + fma(s * z, r, kd * ln2_lo));
-}
+// div_fast, atan2_fast and log_ratio live in gk_math.cuh (shared with the
+// device math accuracy probe, gk_diag_math).
 
 // y-triangle frame shared by all analytic calls of a pair
 struct YTri {
@@ -552,18 +482,30 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
           cr[3 * i + 2] = (kUnit - cc[2 * i] - cc[2 * i + 1]) * inv;
         }
         const double frac = ldexp(1.0, -2 * (depth + 1));  // 0.25^(depth+1), as repeated quartering
+        // the sub-cell's corners in the y frame: a rule point's frame
+        // coordinates are affine in its barycentrics, so each point costs
+        // three 3-term sums instead of barycentrics + frame sums
+        double Cu[3], Cv[3], Cw[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          Cu[i] = cr[3 * i] * Xu[0] + cr[3 * i + 1] * Xu[1] + cr[3 * i + 2] * Xu[2];
+          Cv[i] = cr[3 * i] * Xv[0] + cr[3 * i + 1] * Xv[1] + cr[3 * i + 2] * Xv[2];
+          Cw[i] = cr[3 * i] * Xw[0] + cr[3 * i + 1] * Xw[1] + cr[3 * i + 2] * Xw[2];
+        }
 #pragma unroll 2
         for (int q = 0; q < 7; ++q) {
           // re-read the y-triangle frame from shared memory every point instead
           // of keeping ~60 registers of it live across the loop
           asm volatile("" ::: "memory");
+          const double r0 = c_r7_bary[q][0], r1 = c_r7_bary[q][1], r2 = c_r7_bary[q][2];
           double b[3];
+          if (NT == 3) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
-            b[c] = c_r7_bary[q][0] * cr[c] + c_r7_bary[q][1] * cr[3 + c] + c_r7_bary[q][2] * cr[6 + c];
-          const double u = b[0] * Xu[0] + b[1] * Xu[1] + b[2] * Xu[2];
-          const double v = b[0] * Xv[0] + b[1] * Xv[1] + b[2] * Xv[2];
-          const double wn = b[0] * Xw[0] + b[1] * Xw[1] + b[2] * Xw[2];
+            for (int c = 0; c < 3; ++c) b[c] = r0 * cr[c] + r1 * cr[3 + c] + r2 * cr[6 + c];
+          }
+          const double u = r0 * Cu[0] + r1 * Cu[1] + r2 * Cu[2];
+          const double v = r0 * Cv[0] + r1 * Cv[1] + r2 * Cv[2];
+          const double wn = r0 * Cw[0] + r1 * Cw[1] + r2 * Cw[2];
           const double w = c_r7_w[q] * (measure_x * frac);
           double nw;
           V2 mo;

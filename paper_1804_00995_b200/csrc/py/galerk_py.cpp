@@ -483,6 +483,10 @@ PYBIND11_MODULE(_galerk, m) {
     throw_status(f(n, reinterpret_cast<const double*>(x), reinterpret_cast<const double*>(y),
                    reinterpret_cast<const double*>(z), k, eps, reinterpret_cast<gk_cplx*>(out), as_stream(stream)));
   });
+  m.def("diag_math", [](int fn, int64_t n, uintptr_t a, uintptr_t b, uintptr_t out, uintptr_t stream) {
+    throw_status(gk_diag_math(fn, n, reinterpret_cast<const double*>(a), reinterpret_cast<const double*>(b),
+                              reinterpret_cast<double*>(out), as_stream(stream)));
+  });
   m.def("last_error", []() { return std::string(gk_last_error()); });
   m.def("version", []() { return std::string(gk_version()); });
   m.attr("FP64") = GK_FP64;
