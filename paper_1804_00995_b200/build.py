@@ -22,6 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gk_abi.cu", "gk_assembly.cu", "gk_matvec.cu", "gk_green.cu", "gk_nearfield.cu", "gk_blockeval.cu", "gk_solve.cu",
               "gk_diag.cu"]
 CXX_SOURCES = ["gk_plan.cpp", "host/galerk.cpp"]
+# tuning experiments only (e.g. GK_NVCC_EXTRA="-DGK_NF_MINB=3"); empty by default
+EXTRA = os.environ.get("GK_NVCC_EXTRA", "").split()
 HEADERS = ["gk_internal.hpp", "gk_math.cuh", "host/galerk.hpp", "../../include/galerk_b200_diag.h"]
 
 
@@ -57,7 +59,7 @@ def build(force=False, verbose=False):
                 # per-source register/spill report of the latest compile (+ the running log)
                 with open(o + ".ptxas", "w") as one:
                     res = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-ccbin", CXX, "-Xcompiler",
-                                "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", s, "-o", o], log)
+                                "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", *EXTRA, "-c", s, "-o", o], log)
                     one.write(res.stdout + res.stderr)
         for src in CXX_SOURCES:
             s = os.path.join(CSRC, src)

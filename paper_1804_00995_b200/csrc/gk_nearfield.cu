@@ -32,6 +32,16 @@ namespace gk {
 namespace {
 
 constexpr int kNfWarps = 4;       // warps per CTA
+// Resident CTAs per SM the register budget is sized for, and rule points
+// evaluated in lockstep per lane.  P0 x P0 (cfg 3), measured on cfg 3:
+// (CTAs, unroll) = (4, 2) 48.9 ms, (5, 1) 47.7, (6, 1) 47.4, (7, 1) 47.8,
+// (8, 1) 48.3, (3, 2) 54.1, (2, 4) 64.1: more resident warps beat more ILP per
+// lane.  The P1 variants carry up to 9 local values and keep (4, 2).
+template <int NL>
+struct NfTune {
+  static constexpr int minb = NL == 1 ? 6 : 4;
+  static constexpr int qunroll = NL == 1 ? 1 : 2;
+};
 constexpr int kMaxLoc = 9;        // local matrix entries (P1 x P1)
 
 struct V3 {
@@ -305,7 +315,7 @@ struct WarpSmemB {
 };
 
 template <int NT, int NTR>
-__global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a) {
+__global__ void __launch_bounds__(32 * kNfWarps, NfTune<NT * NTR>::minb) k_nearfield_b(const NfArgs a) {
   constexpr int NL = NT * NTR;
   extern __shared__ unsigned char smem_raw[];
   WarpSmemB<NL>& S = reinterpret_cast<WarpSmemB<NL>*>(smem_raw)[threadIdx.x / 32];
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, 4) k_nearfield_b(const NfArgs a
           Cv[i] = cr[3 * i] * Xv[0] + cr[3 * i + 1] * Xv[1] + cr[3 * i + 2] * Xv[2];
           Cw[i] = cr[3 * i] * Xw[0] + cr[3 * i + 1] * Xw[1] + cr[3 * i + 2] * Xw[2];
         }
-#pragma unroll 2
+#pragma unroll NfTune<NL>::qunroll
         for (int q = 0; q < 7; ++q) {
           // re-read the y-triangle frame from shared memory every point instead
           // of keeping ~60 registers of it live across the loop
