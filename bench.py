@@ -36,11 +36,11 @@ HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json i
 #    libdevice sqrt/sin/cos/division + one complex x real accumulate:
 #    43 DFMA + 13 DMUL + 7 DADD = 106 flops/pair (DFMA = 2 flops);
 #  - production formula: SASS count of k_assemble's pair loop (cuobjdump, P1
-#    cfg 2, y-side accumulation included): 24 DFMA + 7 DMUL + 4 DADD = 59
-#    flops/pair; Laplace: 5 DFMA + 4 DMUL + 5 DADD = 19.
+#    cfg 2, y-side accumulation included): 23 DFMA + 7 DMUL + 4 DADD = 57
+#    flops/pair (59 before the degree-6 cos polynomial); Laplace: 5 DFMA + 4 DMUL + 5 DADD = 19.
 # Laplace ("[1/r]", cfg 1) probe: 11 FP64 instructions + accumulate = 23 flops.
 F_PAIR_PROBE_FLOPS = {True: 106.0, False: 23.0}
-F_PAIR_PROD_FLOPS = {True: 59.0, False: 19.0}
+F_PAIR_PROD_FLOPS = {True: 57.0, False: 19.0}
 
 
 def parse():
