@@ -35,7 +35,10 @@ namespace gk {
 
 namespace {
 
-constexpr int kRecUnroll = 4;  // records per group = independent evaluations per thread
+#ifndef GK_ASM_UNROLL
+#define GK_ASM_UNROLL 6  // measured (cfg 2 / cfg 3 ms): 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56
+#endif
+constexpr int kRecUnroll = GK_ASM_UNROLL;  // records per group = independent evaluations per thread
 constexpr int kGC = 2;         // gather: columns per work item (divides kJCap)
 static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
 
