@@ -111,7 +111,7 @@ void DevArena::upload() {
       cuda_check(cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
     }
   }
-  std::vector<char>().swap(host);
+  hvec<char>().swap(host);
 }
 
 void DevArena::release() {
@@ -182,9 +182,9 @@ void memory_cap(const gk_side& test, const gk_side& trial, const gk_options& o) 
 // run in one launch; the flag selects the masked pair loop per CTA.
 // TX holds the x-block tables, T the y-block tables and the tile lists (the
 // same object for whole-matrix plans).
-std::vector<TileDesc> make_tile_descs(const TileTables& TX, const TileTables& T) {
+hvec<TileDesc> make_tile_descs(const TileTables& TX, const TileTables& T) {
   const size_t nu = T.tile_i.size(), nm = T.mtile_i.size();
-  std::vector<TileDesc> d(nu + nm);
+  hvec<TileDesc> d(nu + nm);
   auto fill = [&](TileDesc& D, int32_t bi, int32_t bj, bool masked) {
     D.i0 = TX.xb_dof_start[bi];
     D.nI = TX.xb_dof_start[bi + 1] - D.i0;
@@ -266,7 +266,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
   if (dry_run) return P;
   DevArena& Ar = P->arena;
-  const std::vector<TileDesc> descs = make_tile_descs(T, T);
+  const hvec<TileDesc> descs = make_tile_descs(T, T);
   lap("tile descriptors");
   Ar.host.reserve(descs.size() * sizeof(TileDesc) + (T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
                   (T.xsup_start.size() + T.xsup_u.size() + X.perm.size() + Yr.perm.size()) * sizeof(int32_t) +
@@ -324,7 +324,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
 // and the copy engine drains slab s-1.  Pageable destinations go through
 // pinned bounce buffers and a threaded host copy.
 struct SlabTables {
-  std::vector<char> blob;  // descs | yrec | yperm, 256-byte aligned sections
+  hvec<char> blob;  // descs | yrec | yperm, 256-byte aligned sections
   size_t o_desc = 0, o_yrec = 0, o_yperm = 0;
   int64_t ntiles = 0;
   int slots = 0;
@@ -332,8 +332,9 @@ struct SlabTables {
   std::exception_ptr err;
 };
 
-template <class T>
-size_t blob_add(std::vector<char>& b, const std::vector<T>& v) {
+template <class V>
+size_t blob_add(hvec<char>& b, const V& v) {
+  using T = typename V::value_type;
   const size_t off = (b.size() + 255) & ~size_t(255);
   b.resize(off + v.size() * sizeof(T));
   if (!v.empty()) std::memcpy(b.data() + off, v.data(), v.size() * sizeof(T));
@@ -380,21 +381,15 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
   Locations Y;
   if (!same) Y = build_locations(*trial, "bem_dense(trial)");
   lap("locations");
-  const OrderChoice O = choose_order(X, same ? nullptr : &Y, false, eps);
+  // the slabs are PCIe-bound (the kernel takes ~1/5 of a slab's copy), so a
+  // natural order within 3x of the unique pair count is taken without
+  // building the RCB candidate (saves ~3 ms of host time per call on cfg 2)
+  const OrderChoice O = choose_order(X, same ? nullptr : &Y, false, eps, 3.0);
   const Locations& Yf = same ? X : Y;
   lap("order");
   TileTables TX;
-  std::vector<int32_t> xl_id;
-  build_x_tables(X, O.B, TX, xl_id);
-  lap("x tables");
-  DevArena AX;
-  AX.host.reserve((TX.xl_x.size() * 3 + TX.xsup_c.size()) * sizeof(double) +
-                  (TX.xsup_start.size() + TX.xsup_u.size() + X.perm.size()) * sizeof(int32_t) + 8 * 256);
-  const size_t o_xl_x = AX.add(TX.xl_x), o_xl_y = AX.add(TX.xl_y), o_xl_z = AX.add(TX.xl_z),
-               o_xsup_start = AX.add(TX.xsup_start), o_xsup_u = AX.add(TX.xsup_u), o_xsup_c = AX.add(TX.xsup_c),
-               o_xperm = AX.add(X.perm);
-  AX.upload();
-  lap("x upload");
+  hvec<int32_t> xl_id;
+  bool x_ready = false;  // TX / xl_id built (workers prepare their y side before that)
 
   // ---- slab table builders (look-ahead bounded to keep host memory flat)
   const int64_t nslab = (cols + w - 1) / w;
@@ -410,14 +405,14 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     const auto b0 = std::chrono::steady_clock::now();
     SlabTables& T = S[s];
     const int64_t c0 = s * w, c1 = std::min(cols, c0 + w);
-    std::vector<int32_t> slab_of_full;
+    hvec<int32_t> slab_of_full;
     Locations Ys = restrict_cols(Yf, c0, c1, slab_of_full);
     set_order(Ys, O.natural);
     BlockLayout Bs;
     layout_y_blocks(Ys, Bs);
     TileTables TY;
-    std::vector<int64_t> yb_start;
-    std::vector<int32_t> yb_list;
+    hvec<int64_t> yb_start;
+    hvec<int32_t> yb_list;
     build_y_tables(Ys, Bs, TY, yb_start, yb_list);
     Coincidence Cs;
     Cs.unsafe = O.C.unsafe;
@@ -428,8 +423,13 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
         Cs.y_of_x[u] = v >= 0 ? slab_of_full[v] : -1;
       }
     }
+    {
+      std::unique_lock<std::mutex> g(m);
+      cv.wait(g, [&] { return stop || x_ready; });
+      if (!x_ready) return;  // stopping: the slab is never consumed
+    }
     build_tile_list(TX, TY, false, Cs, xl_id, yb_start, yb_list);
-    const std::vector<TileDesc> descs = make_tile_descs(TX, TY);
+    const hvec<TileDesc> descs = make_tile_descs(TX, TY);
     T.blob.reserve(descs.size() * sizeof(TileDesc) + TY.yrec.size() * sizeof(YRec) + Ys.perm.size() * 4 + 768);
     T.o_desc = blob_add(T.blob, descs);
     T.o_yrec = blob_add(T.blob, TY.yrec);
@@ -473,6 +473,33 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
         cv.notify_all();
       }
     });
+
+  // ---- x tables, built while the workers prepare the first slabs' y sides
+  DevArena AX;
+  size_t o_xl_x = 0, o_xl_y = 0, o_xl_z = 0, o_xsup_start = 0, o_xsup_u = 0, o_xsup_c = 0, o_xperm = 0;
+  try {
+    build_x_tables(X, O.B, TX, xl_id);
+    {
+      std::lock_guard<std::mutex> g(m);
+      x_ready = true;
+    }
+    cv.notify_all();
+    lap("x tables");
+    AX.host.reserve((TX.xl_x.size() * 3 + TX.xsup_c.size()) * sizeof(double) +
+                    (TX.xsup_start.size() + TX.xsup_u.size() + X.perm.size()) * sizeof(int32_t) + 8 * 256);
+    o_xl_x = AX.add(TX.xl_x);
+    o_xl_y = AX.add(TX.xl_y);
+    o_xl_z = AX.add(TX.xl_z);
+    o_xsup_start = AX.add(TX.xsup_start);
+    o_xsup_u = AX.add(TX.xsup_u);
+    o_xsup_c = AX.add(TX.xsup_c);
+    o_xperm = AX.add(X.perm);
+    AX.upload();
+    lap("x upload");
+  } catch (...) {
+    stop_workers();
+    throw;
+  }
 
   // ---- device pipeline: tables H2D + kernel on ks, matrix D2H on cs
   // Streams, events, table staging and slab buffers persist between calls
@@ -591,7 +618,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
         g.dev_bytes = want;
       }
       std::memcpy(g.host, T.blob.data(), nb);
-      std::vector<char>().swap(T.blob);
+      hvec<char>().swap(T.blob);
       launch_fetch_tables(g.dev, g.host_dev, nb, ks);
       cuda_check(cudaEventRecord(g.h2d, ks), "cudaEventRecord");
       {
@@ -802,10 +829,10 @@ gk_status gk_green_plan_create(int64_t nt, const double* tx, const double* ty, c
       for (int64_t i = 0; i < n; ++i) dofs[i] = (int32_t)i;
       gk_side s{n, x, y, z, w.data(), 1, n, 1, dofs.data(), basis.data(), n};
       Locations L = build_locations(s, "green_matvec");
-      ux = L.x;
-      uy = L.y;
-      uz = L.z;
-      loc = L.point_loc;
+      ux.assign(L.x.begin(), L.x.end());
+      uy.assign(L.y.begin(), L.y.end());
+      uz.assign(L.z.begin(), L.z.end());
+      loc.assign(L.point_loc.begin(), L.point_loc.end());
     };
     std::vector<double> ux, uy, uz, vx, vy, vz;
     std::vector<int64_t> tloc, sloc;

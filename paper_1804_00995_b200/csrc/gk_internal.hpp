@@ -43,6 +43,32 @@ gk_status guard(F&& f) {
   }
 }
 
+// ---- host allocator of the planner ------------------------------------------------
+// The one-shot path plans on every call, and its large temporaries (hash
+// tables, location and tile tables: tens of MB per cfg-2 plan) would otherwise
+// come fresh from mmap each time and be page-faulted in again (~30% of the
+// plan time measured).  Blocks of >= 64 KB are kept in a process-wide cache
+// of size classes (up to 512 MB retained) and reused by later plans; smaller
+// ones go straight to malloc.  Thread-safe.
+void* plan_alloc(size_t bytes);
+void plan_free(void* p, size_t bytes) noexcept;
+size_t plan_cache_bytes();  // bytes currently retained by the cache
+template <class T>
+struct PlanAlloc {
+  using value_type = T;
+  PlanAlloc() = default;
+  template <class U>
+  PlanAlloc(const PlanAlloc<U>&) noexcept {}
+  T* allocate(size_t n) { return static_cast<T*>(plan_alloc(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) noexcept { plan_free(p, n * sizeof(T)); }
+  template <class U>
+  bool operator==(const PlanAlloc<U>&) const noexcept { return true; }
+  template <class U>
+  bool operator!=(const PlanAlloc<U>&) const noexcept { return false; }
+};
+template <class T>
+using hvec = std::vector<T, PlanAlloc<T>>;
+
 void cuda_check(int err, const char* what);  // err is a cudaError_t
 void require_device();
 
@@ -66,8 +92,8 @@ struct DevBuf {
   void alloc(size_t n);
   void release();
   void upload(const void* src, size_t n);
-  template <class T>
-  void upload(const std::vector<T>& v) {
+  template <class T, class A>
+  void upload(const std::vector<T, A>& v) {
     upload(v.data(), v.size() * sizeof(T));
   }
   template <class T>
@@ -83,7 +109,7 @@ struct DevBuf {
 struct DevArena {
   void* p = nullptr;
   size_t bytes = 0;
-  std::vector<char> host;
+  hvec<char> host;
   DevArena() = default;
   DevArena(const DevArena&) = delete;
   DevArena& operator=(const DevArena&) = delete;
@@ -95,8 +121,8 @@ struct DevArena {
     if (n) std::memcpy(host.data() + off, data, n * sizeof(T));
     return off;
   }
-  template <class T>
-  size_t add(const std::vector<T>& v) {
+  template <class V>
+  size_t add(const V& v) {
     return add(v.data(), v.size());
   }
   void upload();  // allocate + copy; releases the host staging
@@ -115,17 +141,17 @@ void ensure_pool();  // default memory pool keeps up to 256 MB cached
 // values, so merging only reorders the additions.
 struct Locations {
   int64_t npts = 0, nfree = 0;
-  std::vector<double> x, y, z;           // [U]
-  std::vector<int64_t> cstart;           // [U+1]
-  std::vector<int32_t> cdof;             // contributing dof (original index)
-  std::vector<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
-  std::vector<int32_t> perm, iperm;      // locality order: perm[p] = dof
+  hvec<double> x, y, z;           // [U]
+  hvec<int64_t> cstart;           // [U+1]
+  hvec<int32_t> cdof;             // contributing dof (original index)
+  hvec<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
+  hvec<int32_t> perm, iperm;      // locality order: perm[p] = dof
   bool natural = false;                  // perm is the identity
-  std::vector<int8_t> strength;          // [nfree+1] boundary strength of each cut position
-  std::vector<int64_t> dstart;           // [nfree+1] by permuted dof
-  std::vector<int32_t> dloc;             // location id
-  std::vector<double> dcoef;
-  std::vector<int64_t> point_loc;        // [npts] location of each point
+  hvec<int8_t> strength;          // [nfree+1] boundary strength of each cut position
+  hvec<int64_t> dstart;           // [nfree+1] by permuted dof
+  hvec<int32_t> dloc;             // location id
+  hvec<double> dcoef;
+  hvec<int64_t> point_loc;        // [npts] location of each point
   int64_t size() const { return (int64_t)x.size(); }
 };
 Locations build_locations(const gk_side& s, const char* who);
@@ -166,22 +192,22 @@ void set_order(Locations& L, bool natural);
 
 struct TileTables {
   // x blocks
-  std::vector<int32_t> xb_dof_start;  // [nIb+1] permuted row ranges
-  std::vector<int32_t> xb_loc_start;  // [nIb+1]
-  std::vector<double> xl_x, xl_y, xl_z;
-  std::vector<int32_t> xsup_start;    // [nrows+1] by permuted row (global offsets)
-  std::vector<int32_t> xsup_u;        // local location index in its block
-  std::vector<double> xsup_c;
+  hvec<int32_t> xb_dof_start;  // [nIb+1] permuted row ranges
+  hvec<int32_t> xb_loc_start;  // [nIb+1]
+  hvec<double> xl_x, xl_y, xl_z;
+  hvec<int32_t> xsup_start;    // [nrows+1] by permuted row (global offsets)
+  hvec<int32_t> xsup_u;        // local location index in its block
+  hvec<double> xsup_c;
   // y blocks
-  std::vector<int32_t> yb_dof_start;  // [nJb+1]
-  std::vector<int32_t> yb_rec_start;  // [nJb+1]
-  std::vector<YRec> yrec;
-  std::vector<uint32_t> yb_zero;      // [nJb] bitmask of H rows with no run (need zero fill)
+  hvec<int32_t> yb_dof_start;  // [nJb+1]
+  hvec<int32_t> yb_rec_start;  // [nJb+1]
+  hvec<YRec> yrec;
+  hvec<uint32_t> yb_zero;      // [nJb] bitmask of H rows with no run (need zero fill)
   // tiles: `masked` tiles may contain coincident location pairs and apply the
   // r^2 <= eps^2 mask; the others provably cannot (exact coincidences only,
   // checked on the host) and skip it.
-  std::vector<int32_t> tile_i, tile_j;          // unmasked tiles
-  std::vector<int32_t> mtile_i, mtile_j;        // masked tiles
+  hvec<int32_t> tile_i, tile_j;          // unmasked tiles
+  hvec<int32_t> mtile_i, mtile_j;        // masked tiles
   bool has_second_slot = false;                 // any record with off1 >= 0
   bool equal_coefs = true;                      // every such record has c1 == c0 (bitwise)
   int64_t pairs_evaluated = 0;
@@ -190,15 +216,15 @@ struct TileTables {
 // Exact x/y location coincidences (the only pairs the r^2 <= eps^2 mask can
 // hit when `unsafe` is false: no two points closer than 8 eps are distinct).
 struct Coincidence {
-  std::vector<int32_t> y_of_x;  // y location with the same coordinates, or -1
+  hvec<int32_t> y_of_x;  // y location with the same coordinates, or -1
   bool unsafe = false;          // some near-coincidence is not exact: mask every tile
 };
 Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same, double eps);
 // Block boundaries for the current dof orders and the pairs they evaluate
 // (count-only: cheap enough to compare orders).
 struct BlockLayout {
-  std::vector<int32_t> xb, xloc;  // x block dof starts [nIb+1], locations per block
-  std::vector<int32_t> yb, yrec;  // y block dof starts [nJb+1], records per block
+  hvec<int32_t> xb, xloc;  // x block dof starts [nIb+1], locations per block
+  hvec<int32_t> yb, yrec;  // y block dof starts [nJb+1], records per block
   int64_t pairs = 0;
 };
 BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric);
@@ -214,18 +240,18 @@ struct OrderChoice {
   BlockLayout B;
   Coincidence C;
 };
-OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps);
+OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps, double accept_natural = 0.0);
 void layout_x_blocks(const Locations& X, BlockLayout& B);
 void layout_y_blocks(const Locations& Y, BlockLayout& B);
-void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, std::vector<int32_t>& xl_id);
-void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std::vector<int64_t>& yb_start,
-                    std::vector<int32_t>& yb_list);
+void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, hvec<int32_t>& xl_id);
+void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hvec<int64_t>& yb_start,
+                    hvec<int32_t>& yb_list);
 void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
-                     const std::vector<int32_t>& xl_id, const std::vector<int64_t>& yb_start,
-                     const std::vector<int32_t>& yb_list);
+                     const hvec<int32_t>& xl_id, const hvec<int64_t>& yb_start,
+                     const hvec<int32_t>& yb_list);
 // Trial locations restricted to dofs [c0, c1) (renumbered from 0, natural
 // order not yet set); slab_of_full maps full location ids to slab ids or -1.
-Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, std::vector<int32_t>& slab_of_full);
+Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, hvec<int32_t>& slab_of_full);
 // Run this thread's planner loops serially (slab workers run one slab per thread).
 void planner_serial(bool on);
 

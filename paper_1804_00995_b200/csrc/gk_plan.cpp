@@ -19,6 +19,83 @@
 
 namespace gk {
 
+// ---- planner allocator (gk_internal.hpp) ----------------------------------------
+namespace {
+constexpr size_t kPoolMin = size_t(64) << 10;       // smaller blocks: plain malloc
+constexpr size_t kPoolCap = size_t(512) << 20;      // retained bytes at most
+// size class: the request rounded up to 1/8 of its power-of-two range (<= 12.5% waste)
+size_t pool_class_bytes(size_t bytes) {
+  size_t p = 1;
+  while (p < bytes) p <<= 1;
+  const size_t step = std::max<size_t>(p >> 3, 4096);
+  return (bytes + step - 1) / step * step;
+}
+struct PlanPool {
+  std::mutex m;
+  std::unordered_map<size_t, std::vector<void*>> free;  // class bytes -> cached blocks
+  size_t retained = 0;
+  ~PlanPool() {
+    for (auto& kv : free)
+      for (void* p : kv.second) std::free(p);
+  }
+};
+PlanPool& plan_pool() {
+  static PlanPool* pool = new PlanPool();  // never destroyed: deallocations may run at exit
+  return *pool;
+}
+}  // namespace
+
+void* plan_alloc(size_t bytes) {
+  if (bytes < kPoolMin) {
+    void* p = std::malloc(bytes ? bytes : 1);
+    if (!p) throw std::bad_alloc();
+    return p;
+  }
+  const size_t c = pool_class_bytes(bytes);
+  PlanPool& P = plan_pool();
+  {
+    std::lock_guard<std::mutex> g(P.m);
+    auto it = P.free.find(c);
+    if (it != P.free.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      P.retained -= c;
+      return p;
+    }
+  }
+  void* p = std::malloc(c);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+
+void plan_free(void* p, size_t bytes) noexcept {
+  if (!p) return;
+  if (bytes < kPoolMin) {
+    std::free(p);
+    return;
+  }
+  const size_t c = pool_class_bytes(bytes);
+  PlanPool& P = plan_pool();
+  {
+    std::lock_guard<std::mutex> g(P.m);
+    if (P.retained + c <= kPoolCap) {
+      try {
+        P.free[c].push_back(p);
+        P.retained += c;
+        return;
+      } catch (...) {  // bookkeeping allocation failed: release the block instead
+      }
+    }
+  }
+  std::free(p);
+}
+
+size_t plan_cache_bytes() {
+  PlanPool& P = plan_pool();
+  std::lock_guard<std::mutex> g(P.m);
+  return P.retained;
+}
+
 namespace {
 struct Key {
   uint64_t a, b, c;
@@ -95,8 +172,8 @@ Locations build_locations(const gk_side& s, const char* who) {
   // patterns (linear probing, load <= 1/2); ids in first-seen point order
   size_t cap = 16;
   while (cap < 2 * (size_t)s.npts) cap <<= 1;
-  std::vector<int64_t> slot(cap, -1);
-  std::vector<Key> keys;
+  hvec<int64_t> slot(cap, -1);
+  hvec<Key> keys;
   keys.reserve((size_t)s.npts);
   L.x.reserve((size_t)s.npts);
   L.y.reserve((size_t)s.npts);
@@ -122,12 +199,12 @@ Locations build_locations(const gk_side& s, const char* who) {
   // contributions: (dof, w_k * phi) for nonzero basis values of free dofs
   // (femspace.cpp:476-484 skips exact zeros and constrained dofs), merged per
   // (location, dof) in point order.
-  std::vector<int64_t> cnt(U + 1, 0);
+  hvec<int64_t> cnt(U + 1, 0);
   for (int64_t k = 0; k < s.npts; ++k) cnt[L.point_loc[k] + 1] += s.nloc;
   for (int64_t u = 0; u < U; ++u) cnt[u + 1] += cnt[u];
-  std::vector<int32_t> tdof(cnt[U]);
-  std::vector<double> tcoef(cnt[U]);
-  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1), used(U, 0);
+  hvec<int32_t> tdof(cnt[U]);
+  hvec<double> tcoef(cnt[U]);
+  hvec<int64_t> fill(cnt.begin(), cnt.end() - 1), used(U, 0);
   for (int64_t k = 0; k < s.npts; ++k) {
     const int64_t e = k / s.g;
     const int q = (int)(k % s.g);
@@ -175,7 +252,7 @@ void finalize_perm(Locations& L) {
   for (int64_t d = 0; d < n; ++d) L.dstart[d + 1] += L.dstart[d];
   L.dloc.resize(L.cstart[U]);
   L.dcoef.resize(L.cstart[U]);
-  std::vector<int64_t> f(L.dstart.begin(), L.dstart.end() - 1);
+  hvec<int64_t> f(L.dstart.begin(), L.dstart.end() - 1);
   for (int64_t u = 0; u < U; ++u)
     for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
       const int32_t pd = L.iperm[L.cdof[p]];
@@ -190,7 +267,7 @@ struct RcbPoint {
   int32_t dof;
 };
 
-void rcb(std::vector<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf, int depth, std::vector<int8_t>& strength) {
+void rcb(hvec<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf, int depth, hvec<int8_t>& strength) {
   if (hi - lo <= leaf) return;
   double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
   for (int64_t i = lo; i < hi; ++i)
@@ -227,8 +304,8 @@ void set_order(Locations& L, bool natural) {
   } else {
     // recursive coordinate bisection of the dof locations (mean of their
     // supporting quadrature locations); unsupported dofs go last.
-    std::vector<double> sx(n, 0.0), sy(n, 0.0), sz(n, 0.0);
-    std::vector<int64_t> cnt(n, 0);
+    hvec<double> sx(n, 0.0), sy(n, 0.0), sz(n, 0.0);
+    hvec<int64_t> cnt(n, 0);
     for (int64_t u = 0; u < U; ++u)
       for (int64_t p = L.cstart[u]; p < L.cstart[u + 1]; ++p) {
         const int32_t d = L.cdof[p];
@@ -237,7 +314,7 @@ void set_order(Locations& L, bool natural) {
         sz[d] += L.z[u];
         cnt[d]++;
       }
-    std::vector<RcbPoint> pts;
+    hvec<RcbPoint> pts;
     pts.reserve(n);
     for (int64_t d = 0; d < n; ++d)
       if (cnt[d]) pts.push_back({{sx[d] / cnt[d], sy[d] / cnt[d], sz[d] / cnt[d]}, (int32_t)d});
@@ -271,7 +348,7 @@ void layout_x_blocks(const Locations& X, BlockLayout& B) {
   B.xloc.clear();
   // ---- x blocks: consecutive permuted rows while their locations fit kUCap,
   // cut back to the strongest order boundary
-  std::vector<int64_t> owner(X.size(), -1);
+  hvec<int64_t> owner(X.size(), -1);
   int64_t p = 0, trial_id = 0;
   B.xb.push_back(0);
   while (p < nrows) {
@@ -312,7 +389,7 @@ void layout_y_blocks(const Locations& Y, BlockLayout& B) {
   B.yrec.clear();
   // ---- y blocks: up to kJCap consecutive permuted cols (fewer if their
   // records would exceed kRCap), cut back to the strongest order boundary
-  std::vector<int64_t> ystamp(Y.size(), -1);
+  hvec<int64_t> ystamp(Y.size(), -1);
   int64_t sid = 0;
   auto count_records = [&](int64_t q0, int64_t q1) {
     ++sid;
@@ -357,7 +434,7 @@ int64_t layout_pairs(const BlockLayout& B, bool symmetric) {
   int64_t pairs = 0;
   // ---- evaluated pairs: symmetric plans keep tiles whose last column >= first row
   const int64_t nJb = (int64_t)B.yrec.size();
-  std::vector<int64_t> suffix(nJb + 1, 0);
+  hvec<int64_t> suffix(nJb + 1, 0);
   for (int64_t bj = nJb - 1; bj >= 0; --bj) suffix[bj] = suffix[bj + 1] + B.yrec[bj];
   for (size_t bi = 0; bi < B.xloc.size(); ++bi) {
     int64_t first = 0;
@@ -392,7 +469,7 @@ void parallel_for(int64_t n, F&& fn) {
     fn((int64_t)0, n);
     return;
   }
-  std::vector<std::thread> pool;
+  hvec<std::thread> pool;
   std::exception_ptr err;
   std::mutex m;
   for (int t = 0; t < nt; ++t)
@@ -409,25 +486,25 @@ void parallel_for(int64_t n, F&& fn) {
 }
 
 struct XBlock {  // one x block's tables (block-local location indices)
-  std::vector<int32_t> locs, sup_u, sup_n;  // locations; per-entry local index; entries per row
-  std::vector<double> sup_c;
+  hvec<int32_t> locs, sup_u, sup_n;  // locations; per-entry local index; entries per row
+  hvec<double> sup_c;
 };
 struct YBlock {  // one y block's records, in descending first-slot order
-  std::vector<YRec> recs;
-  std::vector<int32_t> loc;
+  hvec<YRec> recs;
+  hvec<int32_t> loc;
   uint32_t zero = 0;
   bool second = false, equal = true;
 };
 }  // namespace
 
-void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, std::vector<int32_t>& xl_id) {
+void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, hvec<int32_t>& xl_id) {
   const int64_t nrows = X.nfree;
   const int64_t nIb = (int64_t)B.xb.size() - 1;
   // ---- x blocks (boundaries from the layout), built in parallel
-  std::vector<XBlock> xb(nIb);
+  hvec<XBlock> xb(nIb);
   parallel_for(nIb, [&](int64_t b0, int64_t b1) {
-    std::vector<int64_t> owner(X.size(), -1);
-    std::vector<int32_t> local(X.size(), 0);
+    hvec<int64_t> owner(X.size(), -1);
+    hvec<int32_t> local(X.size(), 0);
     for (int64_t blk = b0; blk < b1; ++blk) {
       XBlock& XB = xb[blk];
       for (int64_t p = B.xb[blk]; p < B.xb[blk + 1]; ++p) {
@@ -484,8 +561,8 @@ void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, std
   }
 }
 
-void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std::vector<int64_t>& yb_start,
-                    std::vector<int32_t>& yb_list) {
+void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hvec<int64_t>& yb_start,
+                    hvec<int32_t>& yb_list) {
   const int64_t nJb = (int64_t)B.yb.size() - 1;
   // ---- y blocks (boundaries from the layout): records = incident locations,
   // each carrying <= 2 (slot, coef) pairs.  Descending first slot: second
@@ -493,12 +570,12 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std
   // comes after that row's own run has been flushed — the run flush is the
   // row's first touch and can be a plain store; rows without a run of their
   // own are only ever read-modify-written and get zero-filled (bitmask).
-  std::vector<YBlock> yb(nJb);
+  hvec<YBlock> yb(nJb);
   parallel_for(nJb, [&](int64_t b0, int64_t b1) {
-    std::vector<int64_t> ystamp(Y.size(), -1);
-    std::vector<std::pair<int32_t, double>> sl;  // slots of one location inside the block
-    std::vector<YRec> recs;
-    std::vector<int32_t> rec_loc, order;
+    hvec<int64_t> ystamp(Y.size(), -1);
+    hvec<std::pair<int32_t, double>> sl;  // slots of one location inside the block
+    hvec<YRec> recs;
+    hvec<int32_t> rec_loc, order;
     for (int64_t b = b0; b < b1; ++b) {
       const int64_t q0 = B.yb[b], q1 = B.yb[b + 1];
       recs.clear();
@@ -554,7 +631,7 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std
   // y location -> y blocks holding it (CSR; a location is listed once per block)
   yb_start.assign(Y.size() + 1, 0);
   yb_list.clear();
-  std::vector<int32_t> last(Y.size(), -1);
+  hvec<int32_t> last(Y.size(), -1);
   for (int64_t b = 0; b < nJb; ++b)
     for (int32_t v : yb[b].loc)
       if (last[v] != (int32_t)b) {
@@ -564,7 +641,7 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std
   for (int64_t v = 0; v < Y.size(); ++v) yb_start[v + 1] += yb_start[v];
   yb_list.resize(yb_start[Y.size()]);
   {
-    std::vector<int64_t> fill(yb_start.begin(), yb_start.end() - 1);
+    hvec<int64_t> fill(yb_start.begin(), yb_start.end() - 1);
     std::fill(last.begin(), last.end(), -1);
     for (int64_t b = 0; b < nJb; ++b)
       for (int32_t v : yb[b].loc)
@@ -593,8 +670,8 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, std
 }
 
 void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
-                     const std::vector<int32_t>& xl_id, const std::vector<int64_t>& yb_start,
-                     const std::vector<int32_t>& yb_list) {
+                     const hvec<int32_t>& xl_id, const hvec<int64_t>& yb_start,
+                     const hvec<int32_t>& yb_list) {
   const int64_t nIb = (int64_t)TX.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
   T.tile_i.clear();
   T.tile_j.clear();
@@ -605,7 +682,7 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
   // coincidences (find_coincidences), a tile needs the mask iff one of its x
   // locations coincides with one of its y records' locations.
   const bool unsafe = C.unsafe;
-  std::vector<std::vector<int32_t>> masked_j(nIb);
+  hvec<hvec<int32_t>> masked_j(nIb);
   if (!unsafe)
     parallel_for(nIb, [&](int64_t b0, int64_t b1) {
       for (int64_t bi = b0; bi < b1; ++bi) {
@@ -636,9 +713,9 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
                        const BlockLayout& B) {
   TileTables T;
-  std::vector<int32_t> xl_id;
-  std::vector<int64_t> yb_start;
-  std::vector<int32_t> yb_list;
+  hvec<int32_t> xl_id;
+  hvec<int64_t> yb_start;
+  hvec<int32_t> yb_list;
   build_x_tables(X, B, T, xl_id);
   build_y_tables(Y, B, T, yb_start, yb_list);
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
@@ -663,7 +740,7 @@ Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same,
     int32_t id;
     int8_t side;
   };
-  std::vector<P> pts;
+  hvec<P> pts;
   pts.reserve(X.size() + (same ? 0 : Y.size()));
   for (int64_t u = 0; u < X.size(); ++u) pts.push_back({X.x[u], (int32_t)u, 0});
   if (!same)
@@ -699,7 +776,7 @@ Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same,
 
 void planner_serial(bool on) { t_serial = on; }
 
-OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps) {
+OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps, double accept_natural) {
   const char* force = std::getenv("GK_ORDER");
   const std::string f = force ? force : "";
   const bool timing = std::getenv("GK_TIMING") != nullptr;
@@ -730,6 +807,21 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps)
     // Natural order keeps the rows of every tile contiguous in A (full-sector,
     // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
     // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
+    // accept_natural > 0: take natural order without building RCB when it
+    // evaluates at most that many pairs per unique pair (callers whose kernel
+    // time hides under a larger cost, like the PCIe-bound streamed path).
+    if (accept_natural > 0.0) {
+      B = layout_of(X, Y);
+      const double unique = (double)X.size() * (double)(Y ? Y->size() : X.size()) * (symmetric ? 0.5 : 1.0);
+      if ((double)B.pairs <= accept_natural * unique) {
+        OrderChoice O;
+        O.C = sweep.get();
+        O.natural = true;
+        O.B = std::move(B);
+        lap("coincidences+orders (natural accepted)");
+        return O;
+      }
+    }
     Locations Xr = X, Yr;
     if (Y) Yr = *Y;
     auto rcb = std::async(std::launch::async, [&] {
@@ -764,13 +856,13 @@ TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, dou
   return T;
 }
 
-Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, std::vector<int32_t>& slab_of_full) {
+Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, hvec<int32_t>& slab_of_full) {
   // the trial locations supporting dofs [c0, c1), in increasing location id,
   // with only those dofs' contributions (renumbered from 0)
   Locations S;
   S.nfree = c1 - c0;
   slab_of_full.assign(Y.size(), -1);
-  std::vector<int32_t> locs;
+  hvec<int32_t> locs;
   for (int64_t d = c0; d < c1; ++d) {
     const int64_t q = Y.iperm[d];
     for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
