@@ -68,7 +68,7 @@ def build(force=False, verbose=False):
             if force or _newer(o, [s] + hdrs):
                 changed = True
                 _run([CXX, "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
-                      "-I/usr/local/cuda/include", "-c", s, "-o", o], log)
+                      "-I/usr/local/cuda/include", *EXTRA, "-c", s, "-o", o], log)
     lib = os.path.join(OUT, "libgalerk_b200.so")
     if changed or not os.path.exists(lib):
         _run([NVCC, *ARCH, "-shared", "-ccbin", CXX, "-o", lib, *objs, "-cudart", "static"])
