@@ -69,6 +69,7 @@ complex_normal = _native.complex_normal
 bem_dense_into = _native.bem_dense_into
 diag_fp64_peak = _native.diag_fp64_peak
 plan_info_dry = _native.plan_info_dry
+plan_info_dry_rows = _native.plan_info_dry_rows
 diag_probe_pairs = _native.diag_probe_pairs
 diag_math = _native.diag_math
 last_error = _native.last_error

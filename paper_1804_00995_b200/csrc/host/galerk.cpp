@@ -410,6 +410,37 @@ SideTables make_side_tables(const Domain& dom, const FemSpace& space) {
   return t;
 }
 
+SideTables row_slab(const SideTables& t, int64_t r0, int64_t r1) {
+  if (r0 < 0 || r1 < r0 || r1 > t.nfree) throw std::invalid_argument("row_slab: rows out of range");
+  SideTables s;
+  s.g = t.g;
+  s.nloc = t.nloc;
+  s.basis = t.basis;
+  s.nfree = r1 - r0;
+  for (int64_t e = 0; e < t.nelem; ++e) {
+    bool touches = false;
+    for (int l = 0; l < t.nloc; ++l) {
+      const int32_t d = t.elem_dofs[e * t.nloc + l];
+      touches |= d >= r0 && d < r1;
+    }
+    if (!touches) continue;
+    for (int l = 0; l < t.nloc; ++l) {
+      const int32_t d = t.elem_dofs[e * t.nloc + l];
+      s.elem_dofs.push_back(d >= r0 && d < r1 ? (int32_t)(d - r0) : -1);
+    }
+    for (int q = 0; q < t.g; ++q) {  // point e*g+q keeps its order within the element
+      const int64_t k = e * t.g + q;
+      s.qs.x.push_back(t.qs.x[k]);
+      s.qs.y.push_back(t.qs.y[k]);
+      s.qs.z.push_back(t.qs.z[k]);
+      s.qs.weights.push_back(t.qs.weights[k]);
+      s.qs.element_of.push_back((int32_t)s.nelem);
+    }
+    ++s.nelem;
+  }
+  return s;
+}
+
 SideTables make_point_side_tables(const std::vector<Vec3>& points) {
   SideTables t;
   const int64_t n = (int64_t)points.size();
@@ -549,9 +580,16 @@ SpMat regularize_radiation(const std::vector<Vec3>& points, const Domain& dom_y,
 
 // ---------------------------------------------------------------------------------
 AssemblyPlan::AssemblyPlan(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const Kernel& kernel,
-                           const FemSpace& trial, const BemOptions& opts, int symmetric) {
-  const SideTables tst = make_side_tables(dom_x, test);
+                           const FemSpace& trial, const BemOptions& opts, int symmetric, int64_t row_begin,
+                           int64_t row_end) {
+  SideTables tst = make_side_tables(dom_x, test);
   const SideTables tri = make_side_tables(dom_y, trial);
+  const bool slab = row_begin != 0 || (row_end >= 0 && row_end != tst.nfree);
+  if (slab) {
+    tst = row_slab(tst, row_begin, row_end < 0 ? tst.nfree : row_end);
+    if (symmetric == 1) throw std::invalid_argument("AssemblyPlan: a row slab is not symmetric");
+    symmetric = 0;
+  }
   const gk_side a = tst.abi(), b = tri.abi();
   const gk_kernel k = kernel.abi();
   const gk_options o = abi_options(opts, symmetric);

@@ -184,11 +184,20 @@ struct SideTables {
 };
 SideTables make_side_tables(const Domain& dom, const FemSpace& space);  // make_side, assembly.cpp:144-171
 SideTables make_point_side_tables(const std::vector<Vec3>& points);      // make_point_side, :173-190
+// Row slab [r0, r1) of a test side (SURVEY 8e, row-slab sharding): the elements
+// touching those dofs, their dofs renumbered to d - r0 and every other dof
+// constrained (-1, skipped like femspace.cpp:476-484).  A plan on it assembles
+// rows r0..r1-1 of the operator; with the trial side replicated, row slabs on
+// different GPUs need no exchange.
+SideTables row_slab(const SideTables& t, int64_t r0, int64_t r1);
 
 class AssemblyPlan {
  public:
+  // row_begin/row_end: assemble only rows [row_begin, row_end) of A into an
+  // (row_end - row_begin) x cols matrix (row_end < 0: all rows)
   AssemblyPlan(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const Kernel& kernel,
-               const FemSpace& trial, const BemOptions& opts = {}, int symmetric = -1);
+               const FemSpace& trial, const BemOptions& opts = {}, int symmetric = -1, int64_t row_begin = 0,
+               int64_t row_end = -1);
   ~AssemblyPlan();
   AssemblyPlan(const AssemblyPlan&) = delete;
   AssemblyPlan& operator=(const AssemblyPlan&) = delete;

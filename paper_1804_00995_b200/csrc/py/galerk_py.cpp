@@ -285,9 +285,10 @@ PYBIND11_MODULE(_galerk, m) {
 
   py::class_<AssemblyPlan>(m, "AssemblyPlan")
       .def(py::init<const Domain&, const Domain&, const FemSpace&, const Kernel&, const FemSpace&,
-                    const BemOptions&, int>(),
+                    const BemOptions&, int, int64_t, int64_t>(),
            py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
-           py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1)
+           py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1, py::arg("row_begin") = 0,
+           py::arg("row_end") = -1)
       .def(
           "assemble",
           [](AssemblyPlan& p, uintptr_t A, int64_t lda, uintptr_t stream) {
@@ -472,6 +473,24 @@ PYBIND11_MODULE(_galerk, m) {
       },
       py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
       py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1);
+  m.def(
+      "plan_info_dry_rows",
+      [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
+         const BemOptions& o, int64_t r0, int64_t r1) {
+        const SideTables a = row_slab(make_side_tables(dx, t), r0, r1), b = make_side_tables(dy, u);
+        const gk_side sa = a.abi(), sb = b.abi();
+        const gk_kernel kk = k.abi();
+        gk_options go;
+        gk_options_default(&go);
+        go.memory_cap_bytes = o.memory_cap_bytes;
+        go.chunk = o.chunk;
+        go.symmetric = 0;
+        gk_plan_info info;
+        throw_status(gk_diag_plan_info(&sa, &sb, &kk, &go, &info));
+        return info_dict(info);
+      },
+      py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
+      py::arg("opts"), py::arg("row_begin"), py::arg("row_end"));
   m.def("diag_fp64_peak", [](int64_t iters, uintptr_t stream) {
     double g = 0;
     throw_status(gk_diag_fp64_peak(iters, &g, as_stream(stream)));
