@@ -73,3 +73,34 @@ def test_sharded_operator_single_rank(galerk):
     ref = np.asarray(A) @ x.cpu().numpy()
     assert y.shape == (n,)
     assert np.linalg.norm(y.cpu().numpy() - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_matrix_free_target_slabs(galerk):
+    """Matrix-free matvec sharded by targets (sources replicated, no reduction):
+    each target slab's plan reproduces its rows of the whole plan's product."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1804_00995_b200.shard import row_partition
+
+    m = galerk.build_sphere(2562, 1.0)
+    d = galerk.make_domain(m, 3)
+    pts, w, _ = galerk.quadrature(d)
+    pts = np.asarray(pts)
+    k = 2 * math.pi / (10 * galerk.edge_stats(m).mean_len)
+    kern = galerk.green_kernel("[exp(ikr)/r]", k)
+    q = torch.tensor(np.asarray(w) * galerk.complex_normal(4, len(w)), device="cuda")
+    whole = galerk.GreenPlan(pts, pts, kern)
+    y = torch.empty(len(w), dtype=torch.complex128, device="cuda")
+    whole.matvec(q.data_ptr(), y.data_ptr(), galerk.FP64, 0)
+    torch.cuda.synchronize()
+    yn = y.cpu().numpy()
+    for r0, r1 in row_partition(len(w), 3):
+        plan = galerk.GreenPlan(np.ascontiguousarray(pts[r0:r1]), pts, kern)
+        assert plan.info()["eps"] == whole.info()["eps"]  # the guard radius sees every source
+        ys = torch.empty(r1 - r0, dtype=torch.complex128, device="cuda")
+        plan.matvec(q.data_ptr(), ys.data_ptr(), galerk.FP64, 0)
+        torch.cuda.synchronize()
+        ref = yn[r0:r1]
+        assert np.linalg.norm(ys.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
