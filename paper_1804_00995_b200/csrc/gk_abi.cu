@@ -341,11 +341,6 @@ size_t blob_add(hvec<char>& b, const V& v) {
   return off;
 }
 
-int host_threads() {
-  const char* e = std::getenv("GK_THREADS");
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  return std::max(1, e ? std::atoi(e) : std::min(hw, 16));
-}
 
 // Column-slab width for a streamed one-shot call, or 0 for the whole-matrix path.
 int64_t stream_slab_cols(int64_t rows, int64_t cols) {

@@ -254,6 +254,9 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
 Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, hvec<int32_t>& slab_of_full);
 // Run this thread's planner loops serially (slab workers run one slab per thread).
 void planner_serial(bool on);
+// Host threads the planner and the streamed path use: GK_THREADS, else the
+// hardware threads divided among the node's ranks (LOCAL_WORLD_SIZE), <= 16.
+int host_threads();
 
 struct TileDesc {  // everything a k_assemble CTA needs to stage its tile
   int32_t i0, nI;      // x block: first permuted row, rows

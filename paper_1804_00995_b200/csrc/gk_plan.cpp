@@ -453,17 +453,26 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
   return B;
 }
 
+int host_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("GK_THREADS");
+    if (e) return std::max(1, std::atoi(e));
+    int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    // one process per GPU (torchrun exports LOCAL_WORLD_SIZE): share the node's cores
+    const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+    if (lw && std::atoi(lw) > 1) hw = std::max(1, hw / std::atoi(lw));
+    return std::min(hw, 16);
+  }();
+  return n;
+}
+
 namespace {
 thread_local bool t_serial = false;  // set by callers that already run one task per thread
-// Static-partition parallel loop over [0, n) on up to GK_THREADS (default:
-// hardware threads, capped at 16) host threads; fn(begin, end) per chunk.
+// Static-partition parallel loop over [0, n) on up to host_threads() threads;
+// fn(begin, end) per chunk.
 template <class F>
 void parallel_for(int64_t n, F&& fn) {
-  static const int nthreads = [] {
-    const char* e = std::getenv("GK_THREADS");
-    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    return std::max(1, e ? std::atoi(e) : std::min(hw, 16));
-  }();
+  const int nthreads = host_threads();
   const int nt = t_serial ? 1 : (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, n / 8));
   if (nt <= 1) {
     fn((int64_t)0, n);
