@@ -72,3 +72,16 @@ def test_gather_rows_two_ranks(n):
     out = mgr.dict()
     mp.spawn(_worker, args=(2, port, n, out), nprocs=2, join=True)
     assert out[0] and out[1]
+
+
+def test_empty_and_out_of_range_slabs(galerk):
+    """More ranks than rows leave empty slabs (a valid, empty plan); a range
+    outside the test side is rejected like the reference's bad arguments."""
+    m = galerk.build_sphere(12, 1.0)
+    d = galerk.make_domain(m, 3)
+    sp = galerk.make_fem(m, "P1")
+    kern = galerk.green_kernel("[1/r]", 0.0)
+    info = galerk.plan_info_dry_rows(d, d, sp, kern, sp, galerk.BemOptions(), 5, 5)
+    assert info["rows"] == 0 and info["pairs_evaluated"] == 0 and info["tiles"] == 0
+    with pytest.raises(ValueError):
+        galerk.plan_info_dry_rows(d, d, sp, kern, sp, galerk.BemOptions(), 3, 13)
