@@ -39,7 +39,10 @@ namespace {
 #define GK_ASM_UNROLL 6  // measured (cfg 2 / cfg 3 ms): 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56
 #endif
 constexpr int kRecUnroll = GK_ASM_UNROLL;  // records per group = independent evaluations per thread
-constexpr int kGC = 2;         // gather: columns per work item (divides kJCap)
+#ifndef GK_ASM_GC
+#define GK_ASM_GC 2  // measured (cfg 2 / cfg 3 ms): 1: 2.54 / 19.09, 2: 2.53 / 19.20, 11: 2.50 / 19.45
+#endif
+constexpr int kGC = GK_ASM_GC;  // gather: columns per work item (divides kJCap)
 static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
 
 struct AsmSmem {
