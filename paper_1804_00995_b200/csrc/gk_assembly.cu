@@ -39,11 +39,15 @@ namespace {
 #define GK_ASM_UNROLL 6  // measured (cfg 2 / cfg 3 ms): 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56
 #endif
 constexpr int kRecUnroll = GK_ASM_UNROLL;  // records per group = independent evaluations per thread
-#ifndef GK_ASM_GC
-#define GK_ASM_GC 2  // measured (cfg 2 / cfg 3 ms): 1: 2.54 / 19.09, 2: 2.53 / 19.20, 11: 2.50 / 19.45
-#endif
-constexpr int kGC = GK_ASM_GC;  // gather: columns per work item (divides kJCap)
-static_assert(kJCap % kGC == 0, "gather column groups must tile the H rows");
+// gather: columns per work item (divides kJCap).  Measured (cfg 2 P1 / cfg 3 P0
+// ms): 1: 2.54 / 19.09, 2: 2.53 / 19.20, 11: 2.50 / 19.45 -> 11 for the P1
+// edge-midpoint specialisation (SLOTS = 2), 2 otherwise.
+template <int SLOTS>
+constexpr int gather_cols() {
+  return SLOTS == 2 ? 11 : 2;
+}
+static_assert(kJCap % gather_cols<2>() == 0 && kJCap % gather_cols<0>() == 0,
+              "gather column groups must tile the H rows");
 
 struct AsmSmem {
   double2 H[kJCap * kUCap];
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   cp_async_wait<0>();
   __syncthreads();
 
+  constexpr int kGC = gather_cols<SLOTS>();
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
   // the row's support entries are read once per item and feed kGC independent
   // H loads; lanes run along rows (coalesced columns for the natural order).
