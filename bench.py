@@ -1,17 +1,27 @@
 #!/usr/bin/env python
 """bench.py — driver-contract benchmark for the B200 dense BEM hot path.
 
-Default workload (BASELINE.json configs[1], "cfg2"): unit-sphere icosphere L5
-(10242 vertices, 20480 triangles), P1 Lagrange, 3-point (edge-midpoint) rule,
-Helmholtz single layer with k = 2 pi / (10 hbar); one step = dense assembly of
-the 10242 x 10242 complex128 matrix (K1+K2, device-resident tables) followed
-by one stored matvec y = A x (K4, x complex N(0,1) from seed 1).
+Default workload (BASELINE.json configs[3], "cfg4", the largest configuration
+that fits one GPU): unit-sphere icosphere L6 (40962 vertices, 81920
+triangles), P0, 3-point (edge-midpoint) rule, Helmholtz single layer with
+k = 2 pi / (10 hbar).  One step = dense assembly of the 81920 x 81920
+complex128 matrix (107 GB, resident in HBM; K1+K2) followed by 10 stored
+matvecs y = A x (K4) with seeded complex N(0,1) vectors (seed 3).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config 1|2|3|4|5]
+                  [--config 1|2|3|4|5] [--extras 2,3,5|none]
 
 Metric: reference-equivalent quadrature-pair kernel evaluations per second
-(M_x * M_y per assembly / step time), plus matrix entries/s and matvec GB/s.
+(M_x * M_y per step / step time).  `roofline` is the assembly kernel against
+the FP64 pipe (sustained DFMA peak measured in the same run); `roofline_matvec`
+the stored matvec against HBM.  With the default config the cfg 2 / cfg 3 /
+cfg 5 lines (smaller workloads, BASELINE configs[1], [2], [4]) are measured
+first and nested under "other_configs".
+
+--impl reference: the reference's CPU path (the oracle restatement of
+bem_product / regularize / zgemv / the matrix-free loop, oracle/; the
+reference itself cannot be built here) on all host cores, on
+the same config, metric and unit; it imports nothing from the product.
 Multi-GPU: replicas only — every rank runs the full step; value
 is the whole-job aggregate over ranks with the max-over-ranks device time.
 """
@@ -31,16 +41,24 @@ sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
 # FP64 work per unique location pair (DESIGN.md §4 "F_pair"), frozen from ncu
-# counters (profiles/r01_fpair_probe.txt):
-#  - canonical probe: the reference formula kernels.cpp:94-114 with
-#    libdevice sqrt/sin/cos/division + one complex x real accumulate:
-#    43 DFMA + 13 DMUL + 7 DADD = 106 flops/pair (DFMA = 2 flops);
-#  - production formula: SASS count of k_assemble's pair loop (cuobjdump, P1
-#    cfg 2, y-side accumulation included): 23 DFMA + 7 DMUL + 4 DADD = 57
-#    flops/pair (59 before the degree-6 cos polynomial); Laplace: 5 DFMA + 4 DMUL + 5 DADD = 19.
-# Laplace ("[1/r]", cfg 1) probe: 11 FP64 instructions + accumulate = 23 flops.
+# counters (profiles/r01_fpair_probe.txt): the canonical probe —
+# the reference formula kernels.cpp:94-114 with libdevice sqrt/sin/cos/division
+# plus one complex x real accumulate — 43 DFMA + 13 DMUL + 7 DADD = 106
+# flops/pair (DFMA = 2 flops); Laplace ("[1/r]") 23 flops.
 F_PAIR_PROBE_FLOPS = {True: 106.0, False: 23.0}
+# the production pair loop (SASS count incl. the y-side accumulation), for
+# the executed-work fraction: P1 cfg 2 23 DFMA + 7 DMUL + 4 DADD = 57 flops/pair
 F_PAIR_PROD_FLOPS = {True: 57.0, False: 19.0}
+METRIC = "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per step, fp64)"
+METRIC_GREEN = "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)"
+
+SPECS = {
+    1: dict(n=642, gauss=3, fam="P1", helm=False, perturb=None, seed=0, real_x=True, nmv=1),
+    2: dict(n=10242, gauss=3, fam="P1", helm=True, perturb=None, seed=1, real_x=False, nmv=1),
+    3: dict(n=10242, gauss=6, fam="P0", helm=True, perturb=2, seed=1, real_x=False, nmv=1),
+    4: dict(n=40962, gauss=3, fam="P0", helm=True, perturb=None, seed=3, real_x=False, nmv=10),
+    5: dict(n=163842, gauss=3, fam="points", helm=True, perturb=None, seed=4, real_x=False, nmv=1),
+}
 
 
 def parse():
@@ -49,42 +67,41 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--extras", default=None,
+                   help="comma list of extra configs measured first (default: 2,3,5 with --config 4 at N=1)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-chunks", type=int, default=8, help="1024-point x chunks of the 1-thread CPU baseline")
     return p.parse_args()
 
 
 # ---------------------------------------------------------------------------------
-def config_problem(g, cfg):
-    """Mesh/space/kernel of a BASELINE config."""
-    spec = {
-        1: dict(n=642, gauss=3, fam="P1", helm=False, perturb=None, seed=0, real_x=True),
-        2: dict(n=10242, gauss=3, fam="P1", helm=True, perturb=None, seed=1, real_x=False),
-        3: dict(n=10242, gauss=6, fam="P0", helm=True, perturb=2, seed=1, real_x=False),
-        4: dict(n=40962, gauss=3, fam="P0", helm=True, perturb=None, seed=3, real_x=False),
-        5: dict(n=163842, gauss=3, fam="points", helm=True, perturb=None, seed=4, real_x=False),
-    }[cfg]
-    mesh = g.build_sphere(spec["n"], 1.0)
-    if spec["perturb"] is not None:
-        mesh = g.perturb_radial(mesh, spec["perturb"], 0.02)
-    hbar = g.edge_stats(mesh).mean_len
-    k = 2 * math.pi / (10 * hbar) if spec["helm"] else 0.0
-    name = "[exp(ikr)/r]" if spec["helm"] else "[1/r]"
-    dom = g.make_domain(mesh, spec["gauss"])
-    space = g.make_fem(mesh, spec["fam"]) if spec["fam"] != "points" else None
-    return spec, mesh, dom, space, g.green_kernel(name, k), k, hbar, name
-
-
-def workload_name(cfg, spec, mesh):
-    nv, ne = mesh.vertex_count(), mesh.element_count()
+def workload_name(cfg, nv, ne):
     return {
         1: f"cfg1: Laplace single layer, P1, 3-pt, icosphere L3 ({nv} v/{ne} t), 642^2 real-valued complex128 + matvec",
         2: f"cfg2: Helmholtz single layer, P1, 3-pt, icosphere L5 ({nv} v/{ne} t), 10242^2 complex128 + matvec",
-        3: f"cfg3: Helmholtz single layer, P0, 6-pt, perturbed L5 ({ne} t), 20480^2 complex128 + matvec (dense part)",
-        4: f"cfg4: Helmholtz single layer, P0, 3-pt, icosphere L6 ({ne} t), 81920^2 complex128 (107 GB) + 10 matvecs",
-        5: f"cfg5: matrix-free Helmholtz Green matvec, 983040 points of L7 ({ne} t)",
+        3: f"cfg3: Helmholtz single layer, P0, 6-pt, perturbed L5 ({ne} t), 20480^2 complex128 incl. near-field "
+           f"correction + matvec",
+        4: f"cfg4: Helmholtz single layer, P0, 3-pt, icosphere L6 ({ne} t), 81920^2 complex128 (107 GB in HBM) "
+           f"+ 10 stored matvecs",
+        5: f"cfg5: matrix-free Helmholtz Green matvec, 983040 points = 3-pt Gauss nodes of icosphere L7 ({ne} t), "
+           f"self-interaction masked",
     }[cfg]
+
+
+def config_dict(cfg, nv, ne, N, M, k, hbar):
+    """The `config` object — identical on both arms (built from their own, bitwise
+    identical, mesh statistics)."""
+    s = SPECS[cfg]
+    d = {"workload": workload_name(cfg, nv, ne), "N": int(N), "M": int(M), "k": float(k), "hbar": float(hbar),
+         "space": s["fam"], "rule_points": s["gauss"], "matvecs_per_step": s["nmv"] if cfg != 5 else 0}
+    if cfg == 5:
+        d["l2"] = "matrix-free: sources (15.7 MB fp64) re-streamed from L2 per tile"
+    else:
+        d["l2"] = "inputs larger than L2 for cfg 2-4: A = %.2f GB written and read every step (no flush needed)" % (
+            16.0 * N * N / 1e9)
+    return d
 
 
 # ---------------------------------------------------------------------------------
@@ -178,41 +195,433 @@ def measured_peaks():
 
 def profile_summary(cfg):
     """The committed ncu capture of the dominant kernel (profiles/ncu_summary.json)."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             return json.load(f).get(f"cfg{cfg}", {})
     except Exception:
         return {}
 
 
-def profile_traffic(cfg):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    return profile_summary(cfg).get("k_assemble_dram_bytes_per_launch")
+# ---------------------------------------------------------------------------------
+# CPU side (oracle = test infrastructure: only the cpu_baseline leg and the
+# reference arm run it).  Chunks follow SURVEY §8(d): S uniformly spaced
+# 1024-point chunks of the x quadrature points (the reference's
+# BemOptions::chunk, assembly.cpp:212-220); the oracle computes the complete
+# rows of the test dofs those points support (bitwise the full computation's
+# rows) and the time extrapolates linearly in the x points processed.
+def load_oracle():
+    from tests._support import load_oracle as _lo
+
+    return _lo()
+
+
+def oracle_problem(o, cfg):
+    """Mesh statistics and side tables from the oracle alone (reference arm: no
+    product code is imported)."""
+    s = SPECS[cfg]
+    v, e = o.build_sphere(s["n"], 1.0)
+    if s["perturb"] is not None:
+        v, e = o.perturb_radial(v, e, s["perturb"], 0.02)
+    v, e = np.asarray(v), np.asarray(e)
+    hbar = o.edge_stats(v, e)[2]
+    k = 2 * math.pi / (10 * hbar) if s["helm"] else 0.0
+    name = "[exp(ikr)/r]" if s["helm"] else "[1/r]"
+    fam = {"P1": 1, "P0": 0, "points": 0}[s["fam"]]
+    ne, nv = len(e), len(v)
+    N = nv if s["fam"] == "P1" else ne
+    return dict(v=v, e=e, hbar=hbar, k=k, name=name, fam=fam, ne=ne, nv=nv, N=N, M=ne * s["gauss"], g=s["gauss"])
+
+
+def chunk_rows(o, P, nchunks, chunk=1024, first=0):
+    """Test dofs supported by `nchunks` uniformly spaced 1024-point x chunks."""
+    start, dof, _ = o.eval_rows(P["v"], P["e"], P["fam"], P["g"])
+    start, dof = np.asarray(start), np.asarray(dof)
+    M = P["M"]
+    los = np.linspace(0, max(0, M - chunk), max(1, nchunks)).astype(np.int64)
+    out = []
+    for lo in los[first:]:
+        hi = min(M, lo + chunk)
+        out.append(sorted(set(dof[start[lo]:start[hi]].tolist())))
+    # x points the complete rows touch (what the oracle's row restriction processes)
+    pt_of = np.repeat(np.arange(M), np.diff(start))
+    npts = [int(len(np.unique(pt_of[np.isin(dof, r)]))) for r in out]
+    return out, npts
+
+
+def complex_normal_np(o, seed, n):
+    """n complex N(0,1) values from the SplitMix64 stream `seed` (re then im,
+    Box-Muller cos branch first): the product's complex_normal
+    (host/galerk.cpp:690-707) drawn from the oracle's stream (numpy libm)."""
+    m = 2 * n
+    u = np.asarray(o.uniform01_stream(seed, 2 * ((m + 1) // 2)))
+    r = np.sqrt(-2.0 * np.log(1.0 - u[0::2]))
+    t = 2.0 * np.pi * u[1::2]
+    z = np.empty(2 * len(r))
+    z[0::2] = r * np.cos(t)
+    z[1::2] = r * np.sin(t)
+    z = z[:m]
+    return z[0::2] + 1j * z[1::2]
+
+
+def cpu_dense_step(o, P, cfg, rows, npts, threads, xs):
+    """Extrapolated seconds of one reference step (assembly [+ regularize] + nmv
+    zgemv) from the complete rows of one chunk."""
+    s = SPECS[cfg]
+    t0 = time.perf_counter()
+    Ar = o.bem_dense(P["v"], P["e"], P["g"], P["fam"], P["v"], P["e"], P["g"], P["fam"], P["name"], P["k"],
+                     rows=rows, threads=threads, cap=1e15)
+    t_asm = time.perf_counter() - t0
+    t_reg = 0.0
+    if cfg == 3:  # the step includes regularize (assembly.cpp:609-697) of those test elements
+        t0 = time.perf_counter()
+        o.regularize(P["v"], P["e"], P["g"], 0, P["v"], P["e"], P["g"], 0, "[1/r]", 0, 0.0, list(rows), threads)
+        t_reg = time.perf_counter() - t0
+    Ar = np.asfortranarray(Ar)
+    t0 = time.perf_counter()
+    for i in range(s["nmv"]):
+        o.matvec(Ar, xs[i], threads)
+    t_mv = time.perf_counter() - t0
+    nr = len(rows)
+    est = t_asm * P["M"] / npts + (t_reg + t_mv) * P["N"] / nr
+    return est, dict(t_asm=t_asm, t_reg=t_reg, t_mv=t_mv, rows=nr, npts=npts)
+
+
+def cpu_green_step(o, P, threads, ids, eps, q):
+    pts, _, _ = o.quadrature(P["v"], P["e"], P["g"])
+    pts = np.asarray(pts)
+    t0 = time.perf_counter()
+    o.green_matvec(P["name"], P["k"], pts, pts, q, eps, list(ids), threads)
+    t = time.perf_counter() - t0
+    return t * P["M"] / len(ids), t
+
+
+def cpu_baseline(o, cfg, nchunks, threads=1):
+    """The reference's CPU path on `nchunks` chunks, `threads` threads (1 = the
+    reference's own concurrency), extrapolated to a full step."""
+    P = oracle_problem(o, cfg)
+    s = SPECS[cfg]
+    if cfg == 5:
+        pts, w, _ = o.quadrature(P["v"], P["e"], P["g"])
+        pts, w = np.asarray(pts), np.asarray(w)
+        q = w * complex_normal_np(o, s["seed"], len(w))
+        lo, hi = pts.min(axis=0), pts.max(axis=0)
+        eps = 1e-12 * float(np.linalg.norm(hi - lo))  # singular_guard_radius (kernels.cpp:14-19)
+        M = P["M"]
+        ids = np.concatenate([np.arange(b, b + 16) for b in np.linspace(0, M - 16, max(1, nchunks)).astype(np.int64)])
+        est, t = cpu_green_step(o, P, threads, ids, eps, q)
+        return {"value": P["M"] ** 2 / est, "unit": "pairs/s", "cores": threads, "kind": "port",
+                "sample": f"oracle matrix-free Green matvec (evaluate_blocks mask=true x weighted charges), "
+                          f"{len(ids)} targets in {nchunks} uniformly spaced blocks x {M} sources in {t:.1f} s, "
+                          f"{threads} thread(s); extrapolated x{M / len(ids):.0f}"}
+    xs = [complex_normal_np(o, s["seed"], P["N"] * s["nmv"])[i * P["N"]:(i + 1) * P["N"]] for i in range(s["nmv"])]
+    chunks, npts = chunk_rows(o, P, nchunks)
+    ests, det = [], []
+    for r, n in zip(chunks, npts):
+        e, d = cpu_dense_step(o, P, cfg, r, n, threads, xs)
+        ests.append(e)
+        det.append(d)
+    est = float(np.sum([d["t_asm"] for d in det]) * P["M"] / np.sum(npts)
+                + np.sum([d["t_reg"] + d["t_mv"] for d in det]) * P["N"] / np.sum([d["rows"] for d in det]))
+    tot = sum(d["t_asm"] + d["t_reg"] + d["t_mv"] for d in det)
+    return {"value": P["M"] ** 2 / est, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "step_s_extrapolated": est,
+            "sample": f"oracle bem_product restatement (+ regularize for cfg 3) + {s['nmv']} zgemv on the complete "
+                      f"rows of {len(chunks)} uniformly spaced 1024-point x chunks ({sum(d['rows'] for d in det)} rows, "
+                      f"{sum(npts)} x points x {P['M']} y points) in {tot:.1f} s, {threads} thread(s); "
+                      f"extrapolated linearly in x points (assembly) and rows (matvec)"}
 
 
 # ---------------------------------------------------------------------------------
-def cpu_sample_rows(oracle, mesh, gauss, fam, target_points):
-    """Evenly spaced test dofs whose supporting x points total ~target_points."""
-    start, dof, _ = oracle.eval_rows(mesh.vertices, mesh.elements, fam, gauss)
-    start = np.asarray(start)
-    dof = np.asarray(dof)
-    ndof = mesh.vertex_count() if fam == 1 else mesh.element_count()
-    per_dof = np.bincount(dof, minlength=ndof)
-    count = max(1, int(target_points / max(1.0, per_dof.mean())))
-    rows = sorted(set(np.linspace(0, ndof - 1, count).astype(int).tolist()))
-    sel = np.isin(dof, rows)
-    pt_of = np.repeat(np.arange(len(start) - 1), np.diff(start))
-    npts = len(np.unique(pt_of[sel]))
-    return rows, npts
+def product_problem(g, cfg):
+    """Mesh/space/kernel of a BASELINE config through the product's host API."""
+    s = SPECS[cfg]
+    mesh = g.build_sphere(s["n"], 1.0)
+    if s["perturb"] is not None:
+        mesh = g.perturb_radial(mesh, s["perturb"], 0.02)
+    hbar = g.edge_stats(mesh).mean_len
+    k = 2 * math.pi / (10 * hbar) if s["helm"] else 0.0
+    name = "[exp(ikr)/r]" if s["helm"] else "[1/r]"
+    dom = g.make_domain(mesh, s["gauss"])
+    space = g.make_fem(mesh, s["fam"]) if s["fam"] != "points" else None
+    return dict(mesh=mesh, dom=dom, space=space, kern=g.green_kernel(name, k), k=k, hbar=hbar, name=name,
+                nv=mesh.vertex_count(), ne=mesh.element_count())
 
 
-def run_cpu(oracle, mesh, spec, k, name, rows, threads, cap=1e13):
-    fam = 1 if spec["fam"] == "P1" else 0
-    t = time.perf_counter()
-    oracle.bem_dense(mesh.vertices, mesh.elements, spec["gauss"], fam, mesh.vertices, mesh.elements, spec["gauss"],
-                     fam, name, k, rows=rows, threads=threads, cap=cap)
-    return time.perf_counter() - t
+def fp64_peaks(g, torch, dev, stream, seconds=2.0):
+    """Burst (one short DFMA launch) and sustained (DFMA + 0.125 B/flop of HBM
+    stores, back to back for `seconds`) FP64 peaks, measured now."""
+    burst = g.diag_fp64_peak(20000, stream.cuda_stream) / 1e3
+    scratch = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
+    with ClockSampler(dev.index or 0) as clk:
+        gf, ms = g.diag_fp64_sustained(seconds, scratch.data_ptr(), scratch.numel(), stream.cuda_stream)
+    del scratch
+    torch.cuda.empty_cache()
+    return burst, gf / 1e3, clk.summary(), ms
+
+
+def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_fp64, with_cpu, with_e2e):
+    s = SPECS[cfg]
+    pp = product_problem(g, cfg)
+    opts = g.BemOptions()
+    opts.memory_cap_bytes = 10 ** 15  # the reference's 8e9 cap refuses cfg 3/4 (SURVEY trap 5)
+    space, dom, kern = pp["space"], pp["dom"], pp["kern"]
+    plan = g.AssemblyPlan(dom, dom, space, kern, space, opts)
+    info = plan.info()
+    n = info["rows"]
+    nmv = s["nmv"]
+    A = torch.empty(n * n, dtype=torch.complex128, device=dev)
+    xs = g.normal(s["seed"], n) if s["real_x"] else g.complex_normal(s["seed"], nmv * n)
+    X = torch.tensor(np.asarray(xs, dtype=np.complex128).reshape(nmv, n), device=dev)
+    y = torch.empty(n, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    nf = g.NearField(dom, dom, space, "[1/r]", space) if cfg == 3 else None
+    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n) + (3 if nf else 0)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        plan.assemble(A.data_ptr(), n, sp)
+        if ev:
+            ev[3].record(stream)
+        if nf:
+            nf.compute(sp)
+            nf.apply(A.data_ptr(), n, sp)
+        if ev:
+            ev[1].record(stream)
+        for i in range(nmv):
+            g.matvec(A.data_ptr(), n, n, n, X[i].data_ptr(), y.data_ptr(), sp)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(max(3, warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index or 0) as clk:
+        t0.record(stream)
+        for i in range(steps):
+            step(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    total_ms = max_over_ranks(t0.elapsed_time(t1), dist, dev)
+    asm_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in evs]))
+    nf_ms = float(np.mean([e[3].elapsed_time(e[1]) for e in evs])) if nf else None
+    mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
+    ms_step = total_ms / steps
+    pairs_ref = info["pairs_reference"]
+    value = aggregate_value(pairs_ref, world, ms_step)
+    nf_2h = None
+    if nf and rank == 0:
+        # BASELINE words cfg 3's near field as "pairs closer than 2 hbar"; the
+        # reference's rule (used in the step) is 3 max circumradius (SURVEY trap 3).
+        nf2 = g.NearField(dom, dom, space, "[1/r]", space, g.NEAR_2HBAR, pp["hbar"])
+        nf2.compute(sp)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nf2.compute(sp)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        nf_2h = {"ms": e0.elapsed_time(e1), "pairs": nf2.info()[0], "analytic_calls": nf2.stats()[0]}
+        del nf2
+    out = None
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+        helm = pp["k"] != 0.0
+        burst, sustained, sus_clk, sus_ms = peaks_fp64
+        achieved = info["pairs_unique"] * F_PAIR_PROBE_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
+        exec_prod = info["pairs_evaluated"] * F_PAIR_PROD_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
+        mv_bytes = 16.0 * n * n + 32.0 * n
+        prof = profile_summary(cfg)
+        out = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": steps, "warmup": warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (complex128)",
+            "data": "synthetic (seeded icosphere mesh per BASELINE config, SplitMix64/Box-Muller vectors)",
+            "config": config_dict(cfg, pp["nv"], pp["ne"], n, math.isqrt(pairs_ref), pp["k"], pp["hbar"])
+            | {"parallelism": f"replicas x{world}"},
+            "entries_per_s": world * n * n / (ms_step * 1e-3),
+            "assembly_ms": asm_ms, "nearfield_ms": nf_ms,
+            "nearfield": (dict(zip(("pairs", "entries"), nf.info())) | {"analytic_calls": nf.stats()[0], "rule": "ref"})
+            if nf else None,
+            "nearfield_2hbar": nf_2h,
+            "matvec_ms": mv_ms, "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
+            "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
+            "pairs_evaluated_per_unique": info["pairs_evaluated"] / info["pairs_unique"],
+            "plan": {k_: info[k_] for k_ in ("tiles", "x_halo", "y_halo", "natural_order", "device_bytes")},
+            "roofline": {"bound": "fp64", "kernel": "k_assemble (K1+K2)", "achieved": achieved, "peak": sustained,
+                         "unit": "TFLOP/s", "frac": achieved / sustained,
+                         "traffic": prof.get("k_assemble_dram_bytes_per_launch"),
+                         "algorithmic_write_bytes": 16.0 * n * n,
+                         "peak_source": "sustained FP64 peak measured in this run: DFMA chains + 0.125 B/flop HBM "
+                                        "stores, back to back for %.1f s (gk_diag_fp64_sustained; MEASURED_PEAKS.json "
+                                        "has no FP64 figure)" % (sus_ms / 1e3),
+                         "peak_clocks": sus_clk,
+                         "peak_burst": burst, "frac_of_burst": achieved / burst,
+                         "work": "pairs_unique (twins merged, symmetric half) x %.0f flops/pair = canonical libdevice "
+                                 "probe F_pair (SURVEY 8d)" % F_PAIR_PROBE_FLOPS[helm],
+                         "frac_executed_pairs_production_formula": exec_prod / sustained,
+                         "ncu_fp64_pipe_pct": prof.get("fp64_pipe_pct"),
+                         "ncu_sfu_xu_pipe_pct": prof.get("xu_pipe_pct")},
+            "roofline_matvec": {"bound": "hbm", "kernel": "k_matvec_partial + k_matvec_reduce (K4)",
+                                "achieved": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak": hbm,
+                                "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
+                                "traffic": prof.get("k_matvec_dram_bytes_per_call"),
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "step_share": {"assembly": asm_ms / ms_step, "nearfield": (nf_ms or 0.0) / ms_step,
+                           "matvecs": mv_ms * nmv / ms_step},
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * steps,
+        }
+    if with_e2e and rank == 0:
+        del A  # the e2e leg allocates its own device matrix
+        torch.cuda.empty_cache()
+        out["e2e"] = e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup)
+    if with_cpu and rank == 0 and world == 1:
+        out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
+    return out
+
+
+def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup):
+    """The same step through the public host API with HOST buffers: host side
+    tables -> AssemblyPlan (gk_plan_create: host planning + table upload) ->
+    gk_plan_assemble into the device-resident matrix [-> NearField] -> per
+    vector: pinned x host->device, gk_matvec, y device->host.  Wall clock per
+    step, everything inside; the matrix buffer is allocated once (the device
+    memory the caller keeps A in)."""
+    s = SPECS[cfg]
+    space, dom, kern = pp["space"], pp["dom"], pp["kern"]
+    A = torch.empty(n * n, dtype=torch.complex128, device=dev)
+    xh = torch.tensor(np.asarray(xs, dtype=np.complex128).reshape(nmv, n)).pin_memory()
+    yh = torch.empty((nmv, n), dtype=torch.complex128).pin_memory()
+    xd = torch.empty(n, dtype=torch.complex128, device=dev)
+    yd = torch.empty(n, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    h2d_tables = [0]
+
+    def one():
+        plan = g.AssemblyPlan(dom, dom, space, kern, space, opts)
+        h2d_tables[0] = plan.info()["device_bytes"]
+        plan.assemble(A.data_ptr(), n, sp)
+        if cfg == 3:
+            nf = g.NearField(dom, dom, space, "[1/r]", space)
+            nf.compute(sp)
+            nf.apply(A.data_ptr(), n, sp)
+        for i in range(nmv):
+            xd.copy_(xh[i], non_blocking=True)
+            g.matvec(A.data_ptr(), n, n, n, xd.data_ptr(), yd.data_ptr(), sp)
+            yh[i].copy_(yd, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(1, min(3, warmup))):
+        one()
+    ts = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        one()
+        ts.append(time.perf_counter() - t)
+    del A
+    torch.cuda.empty_cache()
+    t = float(np.mean(ts))
+    return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d_tables[0] + 16 * n * nmv),
+            "d2h_bytes_per_step": int(16 * n * nmv), "s_per_step": t, "s_per_step_median": float(np.median(ts)),
+            "steps": steps,
+            "path": "C-ABI through the host API: host mesh tables -> gk_plan_create (host plan + table upload) -> "
+                    "gk_plan_assemble (device-resident A)%s -> %d x (x pinned H2D, gk_matvec, y D2H); wall clock"
+                    % (" -> gk_nearfield_create/compute/apply" if cfg == 3 else "", nmv)}
+
+
+def run_green(args, g, torch, dev, rank, world, dist, steps, warmup, peaks_fp64, with_cpu, with_e2e):
+    """cfg 5: matrix-free Green matvec (K5).  A step is one fp64 matvec of the
+    983,040 Gauss points against themselves; the fp32 variant is timed beside it."""
+    s = SPECS[5]
+    pp = product_problem(g, 5)
+    pts, w, _ = g.quadrature(pp["dom"])
+    pts = np.asarray(pts)
+    q = np.asarray(w) * g.complex_normal(s["seed"], len(w))
+    plan = g.GreenPlan(pts, pts, pp["kern"])
+    info = plan.info()
+    qd = torch.tensor(q, device=dev)
+    y = torch.empty(len(w), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    res, clocks = {}, None
+    for prec, label in ((g.FP64, "fp64"), (g.FP32, "fp32")):
+        for _ in range(max(3, warmup)):
+            plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index or 0) as clk:
+            e0.record(stream)
+            for _ in range(steps):
+                plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist, dev)
+        if label == "fp64":
+            clocks = clk.summary()
+        U = info["unique_targets"]
+        res[label] = {"ms": ms, "pairs_per_s": world * len(w) ** 2 / (ms * 1e-3),
+                      "unique_pairs_per_s": world * U * U / (ms * 1e-3)}
+    if rank != 0:
+        return None
+    U = info["unique_targets"]
+    helm = pp["k"] != 0.0
+    evaluated = U * (U + 1) / 2 if info.get("symmetric") else U * U
+    t = res["fp64"]["ms"] * 1e-3
+    burst, sustained, sus_clk, _ = peaks_fp64
+    achieved = evaluated * F_PAIR_PROBE_FLOPS[helm] / t / 1e12
+    M = len(w)
+    out = {
+        "metric": METRIC_GREEN, "value": res["fp64"]["pairs_per_s"], "unit": "pairs/s", "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": res["fp64"]["ms"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128); fp32 variant in detail",
+        "data": "synthetic (seeded icosphere L7 Gauss nodes, SplitMix64/Box-Muller charges)",
+        "config": config_dict(5, pp["nv"], pp["ne"], 0, M, pp["k"], pp["hbar"]) | {"unique": U,
+                                                                                  "parallelism": f"replicas x{world}"},
+        "detail": res, "info": info,
+        "roofline": {"bound": "fp64", "kernel": "k_green64_sym (K5)", "achieved": achieved, "peak": sustained,
+                     "unit": "TFLOP/s", "frac": achieved / sustained, "traffic": None,
+                     "peak_source": "sustained DFMA+store FP64 peak measured in this run",
+                     "peak_burst": burst, "frac_of_burst": achieved / burst,
+                     "work": "evaluated unique pairs (%s) x %.0f flops/pair (probe F_pair)"
+                             % ("symmetric: U(U+1)/2" if info.get("symmetric") else "U^2", F_PAIR_PROBE_FLOPS[helm])},
+        "clocks": clocks,
+        "gpu_launches": plan.launches(g.FP64) * steps,
+    }
+    if with_e2e:
+        # host charges in, host potentials out, plan (host twin merge + upload) inside
+        qh = torch.tensor(q).pin_memory()
+        yh = torch.empty(M, dtype=torch.complex128).pin_memory()
+        ts = []
+        for it in range(max(2, min(steps, 5)) + 1):
+            t0 = time.perf_counter()
+            p2 = g.GreenPlan(pts, pts, pp["kern"])
+            qd.copy_(qh, non_blocking=True)
+            p2.matvec(qd.data_ptr(), y.data_ptr(), g.FP64, stream.cuda_stream)
+            yh.copy_(y, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            if it:
+                ts.append(time.perf_counter() - t0)
+            del p2
+        tm = float(np.mean(ts))
+        out["e2e"] = {"value": M * M / tm, "unit": "pairs/s", "h2d_bytes_per_step": int(16 * M + 24 * M),
+                      "d2h_bytes_per_step": int(16 * M), "s_per_step": tm, "steps": len(ts),
+                      "path": "GreenPlan(host points) + pinned charges H2D + gk_green_matvec + D2H; wall clock"}
+    if with_cpu and world == 1:
+        out["cpu_baseline"] = cpu_baseline(load_oracle(), 5, 8, threads=1)
+    return out
 
 
 # ---------------------------------------------------------------------------------
@@ -235,332 +644,99 @@ def main():
 
     import paper_1804_00995_b200 as g
 
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    spec, mesh, dom, space, kern, k, hbar, kname = config_problem(g, args.config)
-    if args.config == 5:
-        return bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k, hbar)
-
-    opts = g.BemOptions()
-    opts.memory_cap_bytes = 10 ** 15  # the reference's 8e9 cap refuses cfg 3/4 (SURVEY trap 5)
-    plan = g.AssemblyPlan(dom, dom, space, kern, space, opts)
-    info = plan.info()
-    n = info["rows"]
-    A = torch.empty(n * n, dtype=torch.complex128, device=dev)
-    nmv = 10 if args.config == 4 else 1
-    # cfg 4: ten vectors drawn consecutively from the seed-3 stream
-    xs = g.normal(spec["seed"], n) if spec["real_x"] else g.complex_normal(spec["seed"], nmv * n)
-    X = torch.tensor(np.asarray(xs, dtype=np.complex128).reshape(nmv, n), device=dev)
-    y = torch.empty(n, dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sp = stream.cuda_stream
-    # cfg 3: "including the near-field singular correction" -> K3 inside the step
-    nf = g.NearField(dom, dom, space, "[1/r]", space) if args.config == 3 else None
-    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n) + (3 if nf else 0)
-
-    def step(ev=None):
-        if ev:
-            ev[0].record(stream)
-        plan.assemble(A.data_ptr(), n, sp)
-        if nf:
-            if ev:
-                ev[3].record(stream)
-            nf.compute(sp)
-            nf.apply(A.data_ptr(), n, sp)
-        if ev:
-            ev[1].record(stream)
-        for i in range(nmv):
-            g.matvec(A.data_ptr(), n, n, n, X[i].data_ptr(), y.data_ptr(), sp)
-        if ev:
-            ev[2].record(stream)
-
-    fp64_peak_gflops = g.diag_fp64_peak(20000, sp)  # DFMA microbenchmark, this run
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    total_ms = t0.elapsed_time(t1)
-    if nf:
-        nf_ms = float(np.mean([e[3].elapsed_time(e[1]) for e in evs]))
-        asm_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in evs]))
+    peaks_fp64 = fp64_peaks(g, torch, dev, stream)
+    if args.extras is None:
+        extras = [2, 3, 5] if (args.config == 4 and world == 1) else []
     else:
-        nf_ms = None
-        asm_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
-    mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
-    nf_2h = None
-    if nf:
-        # BASELINE words cfg 3's near field as "pairs closer than 2 hbar"; the
-        # reference's rule (used in the step) is 3 max circumradius (SURVEY trap 3).
-        # The 2-hbar mode is timed beside it, outside the step.
-        nf2 = g.NearField(dom, dom, space, "[1/r]", space, g.NEAR_2HBAR, hbar)
-        nf2.compute(sp)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        nf2.compute(sp)
-        e1.record(stream)
+        extras = [int(c) for c in args.extras.split(",") if c.strip() and c.strip() != "none"]
+    others = {}
+    for c in extras:
+        if c == args.config:
+            continue
+        try:
+            st = min(args.steps, 10)
+            if c == 5:
+                others[f"cfg{c}"] = run_green(args, g, torch, dev, rank, world, dist, st, 3, peaks_fp64,
+                                              not args.no_cpu_baseline, not args.no_e2e)
+            else:
+                others[f"cfg{c}"] = run_dense(args, g, torch, dev, rank, world, dist, c, st, 3, peaks_fp64,
+                                              not args.no_cpu_baseline, not args.no_e2e)
+        except Exception as e:  # an extra line never takes the headline down
+            others[f"cfg{c}"] = {"error": repr(e)}
         torch.cuda.synchronize(dev)
-        nf_2h = {"ms": e0.elapsed_time(e1), "pairs": nf2.info()[0], "analytic_calls": nf2.stats()[0]}
-    total_ms = max_over_ranks(total_ms, dist, dev)
-    ms_step = total_ms / args.steps
-    pairs_ref = info["pairs_reference"]
-    value = aggregate_value(pairs_ref, world, ms_step)
-
-    out = None
+        torch.cuda.empty_cache()
+    if args.config == 5:
+        out = run_green(args, g, torch, dev, rank, world, dist, args.steps, args.warmup, peaks_fp64,
+                        not args.no_cpu_baseline, not args.no_e2e)
+    else:
+        out = run_dense(args, g, torch, dev, rank, world, dist, args.config, args.steps, args.warmup, peaks_fp64,
+                        not args.no_cpu_baseline, not args.no_e2e)
     if rank == 0:
-        peaks = measured_peaks()
-        hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-        helm = k != 0.0
-        alg_flops = info["pairs_unique"] * F_PAIR_PROBE_FLOPS[helm]
-        achieved = alg_flops / (asm_ms * 1e-3) / 1e12
-        achieved_prod = info["pairs_unique"] * F_PAIR_PROD_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
-        exec_prod = info["pairs_evaluated"] * F_PAIR_PROD_FLOPS[helm] / (asm_ms * 1e-3) / 1e12
-        peak = fp64_peak_gflops / 1e3
-        mv_bytes = 16.0 * n * n + 32.0 * n
-        clocks = clk.summary()
-        out = {
-            "metric": "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per assembly, fp64)",
-            "value": value,
-            "unit": "pairs/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_step,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64 (complex128)",
-            "data": "synthetic (seeded icosphere mesh, SplitMix64/Box-Muller vectors)",
-            "config": {"workload": workload_name(args.config, spec, mesh), "N": n, "M": int(math.isqrt(pairs_ref)),
-                       "k": k, "hbar": hbar, "parallelism": f"replicas x{world}",
-                       "l2": "inputs larger than L2: A = %.2f GB written+read per step; plan tables %.1f MB"
-                             % (16 * n * n / 1e9, info["device_bytes"] / 1e6)},
-            "entries_per_s": world * n * n / (ms_step * 1e-3),
-            "assembly_ms": asm_ms,
-            "nearfield_ms": nf_ms,
-            "nearfield": (dict(zip(("pairs", "entries"), nf.info())) | {"analytic_calls": nf.stats()[0], "rule": "ref"})
-                         if nf else None,
-            "nearfield_2hbar": nf_2h,
-            "matvec_ms": mv_ms,
-            "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
-            "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
-            "pairs_evaluated_per_unique": info["pairs_evaluated"] / info["pairs_unique"],
-            "roofline": {"bound": "fp64", "kernel": "k_assemble (K1+K2)", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": profile_traffic(args.config),
-                         "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no FP64)",
-                         "work": "pairs_unique (twins merged, symmetric half) x %.0f flops/pair = canonical "
-                                 "libdevice probe F_pair (SURVEY 8d)" % F_PAIR_PROBE_FLOPS[helm],
-                         "frac_production_formula": achieved_prod / peak,
-                         "frac_executed_pairs_production_formula": exec_prod / peak,
-                         "ncu_fp64_pipe_pct": profile_summary(args.config).get("fp64_pipe_pct"),
-                         "ncu_sfu_xu_pipe_pct": profile_summary(args.config).get("xu_pipe_pct")},
-            "roofline_matvec": {"bound": "hbm", "achieved": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak": hbm,
-                                "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
-                                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
-            "clocks": clocks,
-            "gpu_launches": launches_per_step * args.steps,
-        }
-        if not args.no_e2e and args.config in (1, 2):
-            out["e2e"] = e2e_dense(g, torch, dom, space, kern, opts, n, pairs_ref, steps=max(2, min(args.steps, 3)))
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(spec, mesh, k, kname, ms_step)
-    if rank == 0:
+        if others:
+            out["other_configs"] = others
         print(json.dumps(out))
     if dist:
         dist.destroy_process_group()
 
 
-def e2e_dense(g, torch, dom, space, kern, opts, n, pairs_ref, steps):
-    """Same metric through the public drop-in (gk_bem_dense): host mesh tables in,
-    host (pinned) matrix out, every copy inside the timed region."""
-    host = torch.empty(n * n, dtype=torch.complex128, pin_memory=True)
-    g.bem_dense_into(dom, dom, space, kern, space, opts, host.data_ptr(), n)  # warm-up
-    ts = []
-    h2d = 0
-    for _ in range(steps):
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        h2d = g.bem_dense_into(dom, dom, space, kern, space, opts, host.data_ptr(), n)
-        ts.append(time.perf_counter() - t)
-    t = float(np.median(ts))
-    return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": 16 * n * n, "s_per_step": t,
-            "path": "gk_bem_dense (C-ABI, host sides -> pinned host matrix; column slabs streamed: tables built ahead, D2H overlapped)"}
-
-
-def cpu_baseline(spec, mesh, k, name, gpu_ms_step):
-    from tests._support import load_oracle
-
-    oracle = load_oracle()
-    fam = 1 if spec["fam"] == "P1" else 0
-    M = mesh.element_count() * spec["gauss"]
-    rows, npts = cpu_sample_rows(oracle, mesh, spec["gauss"], fam, target_points=min(M, 1536))
-    secs = run_cpu(oracle, mesh, spec, k, name, rows, threads=1)
-    extra = ""
-    if spec["fam"] == "P0" and spec["perturb"] is not None:  # cfg 3: the step includes regularize
-        t0 = time.perf_counter()
-        oracle.regularize(mesh.vertices, mesh.elements, spec["gauss"], 0, mesh.vertices, mesh.elements,
-                          spec["gauss"], 0, "[1/r]", 0, 0.0, list(rows), 1)
-        secs += time.perf_counter() - t0
-        extra = " + regularize of those test elements"
-    pairs = npts * M
-    return {"value": pairs / secs, "unit": "pairs/s", "cores": 1, "kind": "port",
-            "sample": f"oracle bem_product restatement, {len(rows)} complete test rows ({npts} x-points x {M} "
-                      f"y-points = {pairs:.3g} pairs){extra} in {secs:.1f} s, 1 thread (reference concurrency)"}
-
-
 def reference_arm(args, rank, world, dist):
-    """The reference's CPU path timed on the host cores: the oracle (C++
-    restatement, the reference cannot be built here) with all host threads."""
+    """The reference's CPU path on the host cores: the oracle (C++ restatement
+    of bem_product / regularize / zgemv / the matrix-free loop; the reference
+    cannot be built here) with all host threads.  Nothing from the product is
+    imported.  Each step is one 1024-point x chunk (cycling over 8 uniformly
+    spaced chunks) + the step's matvecs on its rows, extrapolated to the full
+    step; cfg 5: one block of 96 targets."""
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    import paper_1804_00995_b200 as g
-    from tests._support import load_oracle
-
-    oracle = load_oracle()
-    spec, mesh, dom, space, kern, k, hbar, kname = config_problem(g, args.config)
+    o = load_oracle()
+    cfg = args.config
+    s = SPECS[cfg]
+    P = oracle_problem(o, cfg)
     threads = os.cpu_count() or 1
-    if args.config == 5:
-        return reference_arm_green(args, g, oracle, spec, mesh, dom, k, kname, threads, world, dist)
-    fam = 1 if spec["fam"] == "P1" else 0
-    M = mesh.element_count() * spec["gauss"]
-    rows, npts = cpu_sample_rows(oracle, mesh, spec["gauss"], fam, target_points=min(M, 2048))
-    for _ in range(max(1, args.warmup)):
-        run_cpu(oracle, mesh, spec, k, kname, rows[:8], threads)
-    ts = [run_cpu(oracle, mesh, spec, k, kname, rows, threads) for _ in range(args.steps)]
-    t = float(np.mean(ts))
-    if args.config == 3:
-        # cfg 3's step includes the near-field correction: the reference's
-        # regularize (assembly.cpp:609-697) for the same test elements (P0: row = element)
-        nt = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            oracle.regularize(mesh.vertices, mesh.elements, spec["gauss"], 0, mesh.vertices, mesh.elements,
-                              spec["gauss"], 0, "[1/r]", 0, 0.0, list(rows), threads)
-            nt.append(time.perf_counter() - t0)
-        t += float(np.mean(nt))
-    value = npts * M / t
-    out = {"impl": "reference", "metric": "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per assembly, fp64)",
-           "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64 (complex128)", "data": "synthetic",
-           "config": {"workload": workload_name(args.config, spec, mesh), "N": space.free_count() if space else None},
-           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
-                            "sample": f"oracle bem_product restatement (OpenMP over trial columns), {len(rows)} "
-                                      f"complete test rows = {npts} x-points x {M} y-points per step"
-                                      + (" + regularize of those test elements" if args.config == 3 else "")},
+    if cfg == 5:
+        pts, w, _ = o.quadrature(P["v"], P["e"], P["g"])
+        pts, w = np.asarray(pts), np.asarray(w)
+        q = w * complex_normal_np(o, s["seed"], len(w))
+        lo, hi = pts.min(axis=0), pts.max(axis=0)
+        eps = 1e-12 * float(np.linalg.norm(hi - lo))
+        blocks = np.linspace(0, P["M"] - 96, 8).astype(np.int64)
+        cpu_green_step(o, P, threads, np.arange(4), eps, q)  # warm-up
+        ests = []
+        for i in range(args.steps):
+            ids = np.arange(blocks[i % 8], blocks[i % 8] + 96)
+            ests.append(cpu_green_step(o, P, threads, ids, eps, q)[0])
+        est = float(np.mean(ests))
+        sample = f"oracle matrix-free Green matvec, 96 targets x {P['M']} sources per step (8 uniformly spaced blocks)"
+        metric = METRIC_GREEN
+        N = 0
+    else:
+        xs = [complex_normal_np(o, s["seed"], P["N"] * s["nmv"])[i * P["N"]:(i + 1) * P["N"]] for i in range(s["nmv"])]
+        chunks, npts = chunk_rows(o, P, 8)
+        o.bem_dense(P["v"], P["e"], P["g"], P["fam"], P["v"], P["e"], P["g"], P["fam"], P["name"], P["k"],
+                    rows=chunks[0][:4], threads=threads, cap=1e15)  # warm-up
+        ests = []
+        for i in range(args.steps):
+            ests.append(cpu_dense_step(o, P, cfg, chunks[i % 8], npts[i % 8], threads, xs)[0])
+        est = float(np.mean(ests))
+        sample = (f"oracle bem_product restatement{' + regularize' if cfg == 3 else ''} + {s['nmv']} zgemv on the "
+                  f"complete rows of one 1024-point x chunk per step (8 uniformly spaced chunks, cycled), "
+                  f"extrapolated to the full step")
+        metric = METRIC
+        N = P["N"]
+    value = P["M"] ** 2 / est
+    cfgd = config_dict(cfg, P["nv"], P["ne"], N, P["M"], P["k"], P["hbar"]) | {"parallelism": f"replicas x{world}"}
+    out = {"impl": "reference", "metric": metric, "value": value, "unit": "pairs/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)",
+           "data": "synthetic (seeded icosphere mesh per BASELINE config, SplitMix64/Box-Muller vectors)",
+           "config": cfgd,
+           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port", "sample": sample},
            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
-    if dist:
-        dist.destroy_process_group()
-
-
-def reference_arm_green(args, g, oracle, spec, mesh, dom, k, kname, threads, world, dist):
-    """cfg 5 reference arm: the oracle's matrix-free Green matvec (the reference's
-    evaluate_blocks(mask=true) x weighted charges) on a sample of targets."""
-    pts, w, _ = g.quadrature(dom)
-    q = np.asarray(w) * g.complex_normal(spec["seed"], len(w))
-    M = len(w)
-    ids = list(range(0, M, M // 96))[:96]
-    lo, hi = np.asarray(pts).min(axis=0), np.asarray(pts).max(axis=0)
-    eps = 1e-12 * float(np.linalg.norm(hi - lo))  # singular_guard_radius (kernels.cpp:14-19)
-    oracle.green_matvec(kname, k, pts, pts, q, eps, ids[:4], threads)  # warm-up
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.green_matvec(kname, k, pts, pts, q, eps, ids, threads)
-        ts.append(time.perf_counter() - t0)
-    t = float(np.mean(ts))
-    value = len(ids) * M / t
-    out = {"impl": "reference", "metric": "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)",
-           "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64 (complex128)", "data": "synthetic",
-           "config": {"workload": "cfg5: matrix-free Helmholtz Green matvec, 983040 targets = sources", "M": M},
-           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
-                            "sample": f"oracle Green matvec, {len(ids)} targets x {M} sources per step"},
-           "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
-    if dist:
-        dist.destroy_process_group()
-
-
-def bench_green(args, g, torch, dev, rank, world, dist, spec, mesh, dom, kern, k, hbar):
-    """cfg 5: matrix-free Green matvec (K5).  A step is one fp64 matvec of the
-    983,040 Gauss points against themselves; the fp32 variant is timed beside it."""
-    pts, w, _ = g.quadrature(dom)
-    q = np.asarray(w) * g.complex_normal(spec["seed"], len(w))
-    plan = g.GreenPlan(pts, pts, kern)
-    info = plan.info()
-    qd = torch.tensor(q, device=dev)
-    y = torch.empty(len(w), dtype=torch.complex128, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    fp64_peak_gflops = g.diag_fp64_peak(20000, stream.cuda_stream)
-    res = {}
-    clocks = None
-    for prec, label in ((g.FP64, "fp64"), (g.FP32, "fp32")):
-        for _ in range(max(3, args.warmup)):
-            plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
-            e0.record(stream)
-            for _ in range(args.steps):
-                plan.matvec(qd.data_ptr(), y.data_ptr(), prec, stream.cuda_stream)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
-        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, dev)
-        if label == "fp64":
-            clocks = clk.summary()
-        U = info["unique_targets"]
-        res[label] = {"ms": ms, "pairs_per_s": world * len(w) ** 2 / (ms * 1e-3),
-                      "unique_pairs_per_s": world * U * U / (ms * 1e-3)}
-    if rank == 0:
-        U = info["unique_targets"]
-        helm = k != 0.0
-        # evaluated pairs: the symmetric path evaluates each unordered unique pair once
-        evaluated = U * (U + 1) / 2 if info.get("symmetric") else U * U
-        t = res["fp64"]["ms"] * 1e-3
-        peak = fp64_peak_gflops / 1e3
-        achieved = evaluated * F_PAIR_PROBE_FLOPS[helm] / t / 1e12
-        out = {
-            "metric": "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)",
-            "value": res["fp64"]["pairs_per_s"], "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["fp64"]["ms"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64 (complex128); fp32 variant in detail",
-            "data": "synthetic (seeded icosphere L7 Gauss nodes, SplitMix64/Box-Muller charges)",
-            "config": {"workload": "cfg5: matrix-free Helmholtz Green matvec, 983040 targets = sources (icosphere L7, "
-                                   "3-pt), self-interaction masked", "M": len(w), "unique": U, "k": k, "hbar": hbar,
-                       "parallelism": f"replicas x{world}",
-                       "l2": "sources re-streamed from L2 per tile; no matrix (matrix-free)"},
-            "detail": res, "info": info,
-            "roofline": {"bound": "fp64", "kernel": "k_green64_sym (K5)", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "peak_source": "DFMA microbenchmark measured in this run",
-                         "work": "evaluated unique pairs (%s) x %.0f flops/pair (probe F_pair)"
-                                 % ("symmetric: U(U+1)/2" if info.get("symmetric") else "U^2",
-                                    F_PAIR_PROBE_FLOPS[helm])},
-            "clocks": clocks,
-            "gpu_launches": plan.launches(g.FP64) * args.steps,
-        }
-        print(json.dumps(out))
     if dist:
         dist.destroy_process_group()
 

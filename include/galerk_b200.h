@@ -121,6 +121,7 @@ typedef struct gk_plan_info {
   double x_halo;                /* sum over x blocks of their locations / U_x    */
   double y_halo;                /* sum over y blocks of their records / U_y      */
   int32_t natural_order;        /* 1 if the dof order kept the input numbering   */
+  int64_t x_blocks, y_blocks;   /* tile rows / columns of blocks                 */
 } gk_plan_info;
 
 /* Builds the location/dof tables (host) and uploads them (device).  Applies

@@ -18,6 +18,14 @@ extern "C" {
  * timed with CUDA events on `stream`. */
 gk_status gk_diag_fp64_peak(int64_t iters, double* gflops, gk_stream stream);
 
+/* Sustained FP64 peak: the DFMA chains of gk_diag_fp64_peak plus a streaming
+ * 16-byte store per 64 flops into `scratch` (device, >= 1 MB; sized above L2
+ * so the stores reach HBM), launched back to back for about `seconds`.  This
+ * is the clock the power cap allows under a DFMA + HBM-write load such as the
+ * 107 GB cfg-4 assembly; gflops = DFMA flops / elapsed. */
+gk_status gk_diag_fp64_sustained(double seconds, void* scratch, uint64_t scratch_bytes, double* gflops,
+                                 double* elapsed_ms, gk_stream stream);
+
 /* The canonical F_pair probe: the reference formula of
  * kernels.cpp:94-114 compiled with libdevice (sqrt, sin, cos, complex / real
  * division, r*r <= eps^2 mask) plus one complex x real accumulate, evaluated

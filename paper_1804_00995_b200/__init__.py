@@ -68,6 +68,7 @@ normal = _native.normal
 complex_normal = _native.complex_normal
 bem_dense_into = _native.bem_dense_into
 diag_fp64_peak = _native.diag_fp64_peak
+diag_fp64_sustained = _native.diag_fp64_sustained
 plan_info_dry = _native.plan_info_dry
 plan_info_dry_rows = _native.plan_info_dry_rows
 diag_probe_pairs = _native.diag_probe_pairs

@@ -134,12 +134,13 @@ struct gk_plan {
   int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0, nmtiles = 0;
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false;
-  int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0)
+  int64_t xblocks = 0, yblocks = 0;
+  int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0, 3 unit + scales)
   // device tables in one arena: TileDesc per tile ((x block, y block) order,
   // masked ones flagged), x locations, x supports, y records, dof maps
   DevArena arena;
   size_t o_tiles = 0, o_xl_x = 0, o_xl_y = 0, o_xl_z = 0, o_xsup_start = 0, o_xsup_u = 0, o_xsup_c = 0, o_yrec = 0,
-         o_xperm = 0, o_yperm = 0;
+         o_xperm = 0, o_yperm = 0, o_yscale = 0;
   uint64_t device_bytes() const { return arena.bytes; }
 };
 
@@ -214,6 +215,13 @@ hvec<TileDesc> make_tile_descs(const TileTables& TX, const TileTables& T) {
   return d;
 }
 
+// k_assemble specialisation of a y side's tables (TileTables::unit_y records
+// carry unit coefficients and need the per-column scales, slots 3)
+int slots_of(const TileTables& T) {
+  if (T.unit_y) return 3;
+  return !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
+}
+
 std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
                                    const gk_options* opts, bool dry_run = false) {
   if (!test || !trial) throw std::invalid_argument("bem_dense: null side");
@@ -261,9 +269,11 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->x_halo = T.x_halo;
   P->y_halo = T.y_halo;
   P->natural = X.natural;
+  P->xblocks = (int64_t)T.xb_dof_start.size() - 1;
+  P->yblocks = (int64_t)T.yb_dof_start.size() - 1;
   P->ntiles = (int64_t)T.tile_i.size();
   P->nmtiles = (int64_t)T.mtile_i.size();
-  P->slots = !T.has_second_slot ? 0 : (T.equal_coefs ? 2 : 1);
+  P->slots = slots_of(T);
   if (dry_run) return P;
   DevArena& Ar = P->arena;
   const hvec<TileDesc> descs = make_tile_descs(T, T);
@@ -281,6 +291,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->o_yrec = Ar.add(T.yrec);
   P->o_xperm = Ar.add(X.perm);
   P->o_yperm = Ar.add(Yr.perm);
+  P->o_yscale = Ar.add(T.yscale);
   lap("stage");
   Ar.upload();
   lap("upload");
@@ -304,11 +315,13 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.yrec = Ar.at<YRec>(P->o_yrec);
   a.xperm = Ar.at<int32_t>(P->o_xperm);
   a.yperm = Ar.at<int32_t>(P->o_yperm);
+  a.yscale = P->slots == 3 ? Ar.at<double>(P->o_yscale) : nullptr;
   a.A = A;
   a.lda = lda;
   a.eps2 = P->eps * P->eps;
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
+  a.natural = P->natural ? 1 : 0;
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
   launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
 }
@@ -325,7 +338,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
 // pinned bounce buffers and a threaded host copy.
 struct SlabTables {
   hvec<char> blob;  // descs | yrec | yperm, 256-byte aligned sections
-  size_t o_desc = 0, o_yrec = 0, o_yperm = 0;
+  size_t o_desc = 0, o_yrec = 0, o_yperm = 0, o_yscale = 0;
   int64_t ntiles = 0;
   int slots = 0;
   bool ready = false;
@@ -425,12 +438,14 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     }
     build_tile_list(TX, TY, false, Cs, xl_id, yb_start, yb_list);
     const hvec<TileDesc> descs = make_tile_descs(TX, TY);
-    T.blob.reserve(descs.size() * sizeof(TileDesc) + TY.yrec.size() * sizeof(YRec) + Ys.perm.size() * 4 + 768);
+    T.blob.reserve(descs.size() * sizeof(TileDesc) + TY.yrec.size() * sizeof(YRec) + Ys.perm.size() * 4 +
+                   TY.yscale.size() * 8 + 1024);
     T.o_desc = blob_add(T.blob, descs);
     T.o_yrec = blob_add(T.blob, TY.yrec);
     T.o_yperm = blob_add(T.blob, Ys.perm);
+    T.o_yscale = blob_add(T.blob, TY.yscale);
     T.ntiles = (int64_t)descs.size();
-    T.slots = !TY.has_second_slot ? 0 : (TY.equal_coefs ? 2 : 1);
+    T.slots = slots_of(TY);
     build_us += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - b0).count();
   };
   std::vector<std::thread> workers;
@@ -579,6 +594,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     a.eps2 = eps * eps;
     a.kappa = 2.0 * k / M_PI;
     a.symmetric = 0;
+    a.natural = 0;
     double wait_ms = 0.0;
     for (int64_t s = 0; s < nslab; ++s) {
       {
@@ -625,6 +641,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
       a.tiles = reinterpret_cast<const TileDesc*>(static_cast<char*>(g.dev) + T.o_desc);
       a.yrec = reinterpret_cast<const YRec*>(static_cast<char*>(g.dev) + T.o_yrec);
       a.yperm = reinterpret_cast<const int32_t*>(static_cast<char*>(g.dev) + T.o_yperm);
+      a.yscale = T.slots == 3 ? reinterpret_cast<const double*>(static_cast<char*>(g.dev) + T.o_yscale) : nullptr;
       a.A = R.slab[s & 1].p;
       launch_assemble(a, T.ntiles, helm, T.slots, ks);
       cuda_check(cudaEventRecord(g.kern, ks), "cudaEventRecord");
@@ -706,6 +723,8 @@ gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
     info->x_halo = P->x_halo;
     info->y_halo = P->y_halo;
     info->natural_order = P->natural ? 1 : 0;
+    info->x_blocks = P->xblocks;
+    info->y_blocks = P->yblocks;
   });
 }
 

@@ -46,17 +46,18 @@ template <int SLOTS>
 constexpr int gather_cols() {
   return SLOTS == 2 ? 11 : 2;
 }
-static_assert(kJCap % gather_cols<2>() == 0 && kJCap % gather_cols<0>() == 0,
+static_assert(kJCap % gather_cols<2>() == 0 && kJCap % gather_cols<0>() == 0 && kJCap % gather_cols<3>() == 0,
               "gather column groups must tile the H rows");
 
 struct AsmSmem {
-  double2 H[kJCap * kUCap];
+  double2 H[kJCap * kHS];  // y-side partial sums H[j][u]
   YRec rec[kRCap];
   double xs_c[kXsCap];
   int32_t xs_u[kXsCap];
   int32_t xs_start[kIMax + 1];
   int32_t orow[kIMax];  // original row index of each tile row
   int32_t ocol[kJCap];  // original column index of each tile column
+  double ys[kJCap];      // per-column scale (SLOTS == 3)
 };
 
 __device__ __forceinline__ YRec load_rec(const YRec* p) {
@@ -108,12 +109,12 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   // stage with cp.async (no register staging): group 0 = the records the pair
   // loop needs now; group 1 = the x support lists and dof maps the gather
   // needs only after the pair loop, so their latency hides behind it.
-  // Records run in descending first-slot order, so each H row is first
-  // written by its own run flush (a plain store); only rows without a run
-  // (host bitmask) are zero-filled.
-  if (zero_rows)
-    for (int e = t; e < nJ * kUCap; e += kAsmThreads)
-      if ((zero_rows >> (e / kUCap)) & 1u) S.H[e] = make_double2(0.0, 0.0);
+  // Each H row is first written by its own run flush (a plain store; the
+  // host orders the runs so that every read-modify-write of a row comes
+  // after it); only rows without a run (host bitmask) are zero-filled.
+  // each thread zero-fills its own column of the rows without a run (the
+  // pair loop touches only that column; the gather comes after a barrier)
+  for (uint32_t m = zero_rows; m; m &= m - 1) S.H[(__ffs(m) - 1) * kHS + t] = make_double2(0.0, 0.0);
   {
     const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
     double2* dst = reinterpret_cast<double2*>(S.rec);
@@ -125,8 +126,12 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     cp_async4(S.xs_u + e, a.xsup_u + xs0 + e);
   }
   for (int e = t; e <= nI; e += kAsmThreads) cp_async4(S.xs_start + e, a.xsup_start + i0 + e);  // global offsets
-  for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
-  for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
+  if (!a.natural) {  // natural order: A's row/column index is the permuted one
+    for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
+    for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
+  }
+  if (SLOTS == 3)
+    for (int e = t; e < nJ; e += kAsmThreads) cp_async8(S.ys + e, a.yscale + j0 + e);
   cp_async_commit();
   // my x location; idle columns are far away (finite, never gathered)
   const double ux = t < nu ? __ldg(a.xl_x + l0 + t) : 1e100;
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     const bool fresh = p.off0 != cur;
     if (fresh) flush();
     cur = p.off0;
-    const double w0 = p.c0 * rinv;
+    const double w0 = SLOTS == 3 ? rinv : p.c0 * rinv;
     if (HELM) {
       ar = fma(cs, w0, fresh ? 0.0 : ar);
       ai = fma(sn, w0, fresh ? 0.0 : ai);
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       ai = 0.0;
     }
     if (SLOTS > 0 && p.off1 >= 0) {
-      const double w1 = SLOTS == 2 ? w0 : p.c1 * rinv;
+      const double w1 = SLOTS >= 2 ? w0 : p.c1 * rinv;
       double2* h = reinterpret_cast<double2*>(Hb + p.off1);
       double2 v = *h;
       if (HELM) {
@@ -210,45 +215,134 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   constexpr int kGC = gather_cols<SLOTS>();
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
   // the row's support entries are read once per item and feed kGC independent
-  // H loads; lanes run along rows (coalesced columns for the natural order).
+  // H loads; lanes run along rows (coalesced columns of the direct block).
   double2* A = reinterpret_cast<double2*>(a.A);
   const long long lda = a.lda;
-  const int items = nI * ((nJ + kGC - 1) / kGC);
-  // item e = (row e % nI, column group e / nI), advanced incrementally: one
-  // integer division per thread instead of two per item
-  const int nIs = max(nI, 1);  // items = 0 when nI = 0
-  const int di = kAsmThreads % nIs, dg = kAsmThreads / nIs;
-  int ii = t % nIs, jb = (t / nIs) * kGC;
-  for (int e = t; e < items; e += kAsmThreads, ii += di, jb += dg * kGC) {
-    if (ii >= nI) ii -= nI, jb += kGC;
-    const int pi = i0 + ii;
-    if (a.symmetric && pi > j0 + min(jb + kGC, nJ) - 1) continue;  // whole group below the diagonal
-    double re[kGC], im[kGC];
+  const int ngroups = (nJ + kGC - 1) / kGC;
+  const int nIs = max(nI, 1);  // no items when nI = 0
+  auto entries = [&](int ii, int jb, double (&re)[kGC], double (&im)[kGC]) {
 #pragma unroll
     for (int q = 0; q < kGC; ++q) re[q] = im[q] = 0.0;
-    const double2* Hr = S.H + jb * kUCap;  // rows past nJ hold stale values that are never stored
+    const double2* Hr = S.H + jb * kHS;  // rows past nJ hold stale values that are never stored
     const int s1 = S.xs_start[ii + 1] - xs0;
     for (int s = S.xs_start[ii] - xs0; s < s1; ++s) {
       const double c = S.xs_c[s];
       const int u = S.xs_u[s];
 #pragma unroll
       for (int q = 0; q < kGC; ++q) {
-        const double2 h = Hr[q * kUCap + u];
+        const double2 h = Hr[q * kHS + u];
         re[q] = fma(c, h.x, re[q]);
         im[q] = fma(c, h.y, im[q]);
       }
     }
-    const long long oi = S.orow[ii];
+    if (SLOTS == 3)
 #pragma unroll
-    for (int q = 0; q < kGC; ++q) {
-      const int jj = jb + q, pj = j0 + jj;
-      if (jj < nJ && !(a.symmetric && pi > pj)) {
-        const long long oj = S.ocol[jj];
-        const double2 v = make_double2(re[q], im[q]);
-        A[oi + oj * lda] = v;
-        if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
+      for (int q = 0; q < kGC; ++q) {
+        const double f = S.ys[min(jb + q, kJCap - 1)];
+        re[q] *= f;
+        im[q] *= f;
+      }
+  };
+  if (!a.symmetric || !a.natural) {
+    // non-symmetric plans, and symmetric ones whose rows are scattered in A
+    // (RCB order): direct (and mirror) stores straight from registers
+    const int items = nI * ngroups;
+    // item e = (row e % nI, column group e / nI), advanced incrementally
+    const int di = kAsmThreads % nIs, dg = kAsmThreads / nIs;
+    int ii = t % nIs, jb = (t / nIs) * kGC;
+    for (int e = t; e < items; e += kAsmThreads, ii += di, jb += dg * kGC) {
+      if (ii >= nI) ii -= nI, jb += kGC;
+      const int pi = i0 + ii;
+      if (a.symmetric && pi > j0 + min(jb + kGC, nJ) - 1) continue;  // whole group below the diagonal
+      double re[kGC], im[kGC];
+      entries(ii, jb, re, im);
+      const long long oi = a.natural ? pi : S.orow[ii];
+#pragma unroll
+      for (int q = 0; q < kGC; ++q) {
+        const int pj = j0 + jb + q;
+        if (jb + q < nJ && !(a.symmetric && pi > pj)) {
+          const long long oj = a.natural ? pj : S.ocol[jb + q];
+          const double2 v = make_double2(re[q], im[q]);
+          A[oi + oj * lda] = v;
+          if (a.symmetric && pi != pj) A[oj + oi * lda] = v;
+        }
       }
     }
+    return;
+  }
+  // Symmetric tiles in natural order (permuted index = A's index; rows and
+  // columns of a tile contiguous in A): thread = (row ii, strip of columns).
+  // The row's supports are loaded once into registers and feed every column
+  // of the strip; each entry is written to (i, j) — lanes along rows, one
+  // coalesced column segment per warp store — and to the mirror (j, i) —
+  // each lane a contiguous run down its own column, two entries per 32-byte
+  // store (STG.256) where aligned.  Only entries with row <= column are formed.
+  constexpr int kSupCache = 6;  // P0 rules up to 6 points: all supports in registers
+  const int nstrip = max(1, kAsmThreads / nIs);
+  const int ii = t % nIs, strip = t / nIs;
+  if (t >= nstrip * nIs || ii >= nI) return;
+  const int pi = i0 + ii;
+  const int jlo = max(strip * nJ / nstrip, pi - j0), jhi = (strip + 1) * nJ / nstrip;
+  if (jlo >= jhi) return;
+  const int sb = S.xs_start[ii] - xs0, ns = S.xs_start[ii + 1] - xs0 - sb;
+  int su[kSupCache];
+  double sc[kSupCache];
+#pragma unroll
+  for (int k = 0; k < kSupCache; ++k) {
+    su[k] = k < ns ? S.xs_u[sb + k] : 0;
+    sc[k] = k < ns ? S.xs_c[sb + k] : 0.0;
+  }
+  auto entry = [&](int j) {
+    const double2* Hr = S.H + j * kHS;
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int k = 0; k < kSupCache; ++k)
+      if (k < ns) {
+        const double2 h = Hr[su[k]];
+        re = fma(sc[k], h.x, re);
+        im = fma(sc[k], h.y, im);
+      }
+    for (int k = kSupCache; k < ns; ++k) {
+      const double c = S.xs_c[sb + k];
+      const double2 h = Hr[S.xs_u[sb + k]];
+      re = fma(c, h.x, re);
+      im = fma(c, h.y, im);
+    }
+    if (SLOTS == 3) {
+      const double f = S.ys[j];
+      re *= f;
+      im *= f;
+    }
+    return make_double2(re, im);
+  };
+  double2* dcol = A + pi + (long long)(j0 + jlo) * lda;  // (pi, j0 + j)
+  double2* mrow = A + (long long)pi * lda + j0;          // (j0 + j, pi) = mrow[j]
+  int j = jlo;
+  if (j0 + j == pi) {  // diagonal entry: written once
+    *dcol = entry(j);
+    dcol += lda;
+    ++j;
+  }
+  if (j < jhi && ((reinterpret_cast<uintptr_t>(mrow + j) & 31) != 0)) {
+    const double2 v = entry(j);
+    *dcol = v;
+    dcol += lda;
+    mrow[j] = v;
+    ++j;
+  }
+  for (; j + 1 < jhi; j += 2) {
+    const double2 v0 = entry(j), v1 = entry(j + 1);
+    dcol[0] = v0;
+    dcol[lda] = v1;
+    dcol += 2 * lda;
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(mrow + j), "d"(v0.x), "d"(v0.y), "d"(v1.x),
+                 "d"(v1.y)
+                 : "memory");
+  }
+  if (j < jhi) {
+    const double2 v = entry(j);
+    *dcol = v;
+    mrow[j] = v;
   }
 }
 
@@ -270,8 +364,10 @@ void launch_slots(const AsmArgs& a, int64_t ntiles, int slots, cudaStream_t s) {
     launch_one<HELM, 0>(a, ntiles, s);
   else if (slots == 1)
     launch_one<HELM, 1>(a, ntiles, s);
-  else
+  else if (slots == 2)
     launch_one<HELM, 2>(a, ntiles, s);
+  else
+    launch_one<HELM, 3>(a, ntiles, s);
 }
 
 // Tile tables from mapped pinned host memory into device memory by SM loads:

@@ -2,6 +2,8 @@
 // and the F_pair probe kernels used for the roofline accounting.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../../include/galerk_b200_diag.h"
 #include "gk_internal.hpp"
 #include "gk_math.cuh"
@@ -28,6 +30,40 @@ __global__ void __launch_bounds__(256) k_dfma_peak(long long iters, double seed,
   }
   const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
   if (s == 12345.678) sink[threadIdx.x] = s;  // never true; keeps the chains alive
+}
+
+// Sustained variant: the same DFMA chains plus a streaming 16-byte store per
+// two iterations (0.125 B/flop, the byte/flop ratio of the cfg-4 assembly's
+// 107 GB matrix write over its FP64 work), launched back to back for
+// seconds, so that the clock settles where the power cap puts it under a
+// DFMA + HBM-write load like k_assemble's.
+__global__ void __launch_bounds__(256) k_dfma_store(long long iters, double seed, double2* __restrict__ buf,
+                                                     long long n16, double* sink) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+         a7 = a0 + 7;
+  const double m = 0.999999999, c = 1e-9;
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fma(a0, m, c);
+      a1 = fma(a1, m, c);
+      a2 = fma(a2, m, c);
+      a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c);
+      a5 = fma(a5, m, c);
+      a6 = fma(a6, m, c);
+      a7 = fma(a7, m, c);
+    }
+    if (i & 1) {
+      __stcs(buf + idx, make_double2(a0, a1));
+      idx += nthr;
+      if (idx >= n16) idx -= n16;
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
 // Reference formula (kernels.cpp:94-114) with libdevice, plus one complex x
@@ -119,6 +155,47 @@ gk_status gk_diag_fp64_peak(int64_t iters, double* gflops, gk_stream stream) {
     cudaEventDestroy(e1);
     const double dfma = (double)blocks * 256.0 * (double)iters * 32.0;
     *gflops = 2.0 * dfma / (ms * 1e-3) / 1e9;
+  });
+}
+
+gk_status gk_diag_fp64_sustained(double seconds, void* scratch, uint64_t scratch_bytes, double* gflops,
+                                 double* elapsed_ms, gk_stream stream) {
+  return guard([&] {
+    require_device();
+    if (!gflops || !(seconds > 0.0) || !scratch || scratch_bytes < (uint64_t(1) << 20))
+      throw std::invalid_argument("gk_diag_fp64_sustained: bad arguments");
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    DevBuf sink;
+    sink.alloc(256 * sizeof(double));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int blocks = sms * 8;
+    const long long n16 = (long long)(scratch_bytes / 16);
+    double2* buf = static_cast<double2*>(scratch);
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    // calibrate one launch (~50 ms), then fill `seconds` with back-to-back launches
+    long long iters = 20000;
+    float ms = 0.f;
+    cudaEventRecord(e0, s);
+    k_dfma_store<<<blocks, 256, 0, s>>>(iters, 1.0, buf, n16, sink.as<double>());
+    cudaEventRecord(e1, s);
+    cuda_check(cudaEventSynchronize(e1), "sustained calibration");
+    cudaEventElapsedTime(&ms, e0, e1);
+    iters = std::max<long long>(1000, (long long)(iters * 50.0 / std::max(ms, 0.01f)));
+    const int launches = std::max(1, (int)(seconds * 1e3 / 50.0));
+    cudaEventRecord(e0, s);
+    for (int l = 0; l < launches; ++l) k_dfma_store<<<blocks, 256, 0, s>>>(iters, 1.0, buf, n16, sink.as<double>());
+    cudaEventRecord(e1, s);
+    cuda_check(cudaEventSynchronize(e1), "sustained run");
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double dfma = (double)launches * blocks * 256.0 * (double)iters * 32.0;
+    *gflops = 2.0 * dfma / (ms * 1e-3) / 1e9;
+    if (elapsed_ms) *elapsed_ms = ms;
   });
 }
 

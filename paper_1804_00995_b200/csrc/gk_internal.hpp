@@ -177,10 +177,11 @@ constexpr int kXsCap = 320;  // x support entries per tile (staged in shared mem
 constexpr int kAsmCtasPerSm = 4;
 constexpr int kAsmThreads = kUCap;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
+constexpr int kHS = kUCap;  // H row stride in 16-byte entries
 
 struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   double x, y, z, c0, c1;
-  int32_t off0, off1;  // byte offsets slot * kUCap * 16 into H; off1 = -1 if none
+  int32_t off0, off1;  // byte offsets slot * kHS * 16 into H (off0: run slot, off1: read-modify-write slot or -1)
 };
 static_assert(sizeof(YRec) == 48, "YRec layout");
 static_assert(kJCap <= 32, "per-block zero-fill mask is 32 bits");
@@ -210,6 +211,12 @@ struct TileTables {
   hvec<int32_t> mtile_i, mtile_j;        // masked tiles
   bool has_second_slot = false;                 // any record with off1 >= 0
   bool equal_coefs = true;                      // every such record has c1 == c0 (bitwise)
+  // unit_y: every y dof's contributions share one coefficient (P0 with an
+  // equal-weight rule: w = area/g at every point), so records carry unit
+  // coefficients and the dof's factor yscale[permuted dof] is applied once
+  // per matrix entry in the gather instead of once per pair.
+  bool unit_y = false;
+  hvec<double> yscale;
   int64_t pairs_evaluated = 0;
   double x_halo = 0.0, y_halo = 0.0;
 };
@@ -280,13 +287,16 @@ struct AsmArgs {
   const YRec* yrec;
   const int32_t* xperm;
   const int32_t* yperm;
+  const double* yscale;  // [permuted y dof] (slots == 3 only)
   void* A;
   int64_t lda;
   double eps2;
   double kappa;  // 2k/pi
   int32_t symmetric;
+  int32_t natural;  // dof orders are the identity: A's indices are the permuted ones (no perm lookups)
 };
-// slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0
+// slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0,
+// 3 = unit coefficients with per-column scales (TileTables::unit_y)
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream);
 // Copy ceil(bytes/16) 16-byte words from mapped pinned host memory (device
 // view) to device memory with SM loads (both 16-byte aligned and padded).

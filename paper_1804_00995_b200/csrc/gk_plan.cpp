@@ -262,6 +262,11 @@ void finalize_perm(Locations& L) {
     }
 }
 
+double env_frac(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : dflt;
+}
+
 struct RcbPoint {
   double c[3];
   int32_t dof;
@@ -314,16 +319,41 @@ void set_order(Locations& L, bool natural) {
         sz[d] += L.z[u];
         cnt[d]++;
       }
+    // RCB over units of `unit` consecutive dofs (aligned groups): the rows
+    // of a unit stay adjacent in every block, so matrix writes come in whole
+    // 32-byte sectors (unit 2) instead of scattered 16-byte halves.
+    const int64_t unit = std::max<int64_t>(1, (int64_t)env_frac("GK_UNIT", 1));
     hvec<RcbPoint> pts;
-    pts.reserve(n);
-    for (int64_t d = 0; d < n; ++d)
-      if (cnt[d]) pts.push_back({{sx[d] / cnt[d], sy[d] / cnt[d], sz[d] / cnt[d]}, (int32_t)d});
-    rcb(pts, 0, (int64_t)pts.size(), 4, 0, L.strength);
+    pts.reserve(n / unit + 1);
+    for (int64_t d0 = 0; d0 < n; d0 += unit) {
+      double c[3] = {0, 0, 0};
+      int64_t m = 0;
+      for (int64_t d = d0; d < std::min(n, d0 + unit); ++d) {
+        if (!cnt[d]) continue;
+        c[0] += sx[d] / cnt[d];
+        c[1] += sy[d] / cnt[d];
+        c[2] += sz[d] / cnt[d];
+        ++m;
+      }
+      if (m) pts.push_back({{c[0] / m, c[1] / m, c[2] / m}, (int32_t)d0});
+    }
+    hvec<int8_t> ustrength(pts.size() + 1, 0);
+    rcb(pts, 0, (int64_t)pts.size(), std::max<int64_t>(1, 4 / unit), 0, ustrength);
     L.perm.clear();
     L.perm.reserve(n);
-    for (const auto& p : pts) L.perm.push_back(p.dof);
+    hvec<char> placed(n, 0);
+    for (size_t u = 0; u < pts.size(); ++u) {
+      const int64_t pos = (int64_t)L.perm.size();
+      L.strength[pos] = ustrength[u];
+      for (int64_t d = pts[u].dof; d < std::min(n, (int64_t)pts[u].dof + unit); ++d)
+        if (cnt[d]) {
+          if (L.perm.size() > (size_t)pos) L.strength[L.perm.size()] = -1;  // inside a unit: never cut
+          L.perm.push_back((int32_t)d);
+          placed[d] = 1;
+        }
+    }
     for (int64_t d = 0; d < n; ++d)
-      if (!cnt[d]) L.perm.push_back((int32_t)d);
+      if (!placed[d]) L.perm.push_back((int32_t)d);
   }
   L.strength[0] = L.strength[n] = 127;
   finalize_perm(L);
@@ -332,9 +362,14 @@ void set_order(Locations& L, bool natural) {
 namespace {
 // Cut a greedy block [start, end_max) back to the strongest order boundary in
 // its last 20% so blocks are unions of whole spatial clusters.
-int64_t cut(const Locations& L, int64_t start, int64_t end_max) {
+int64_t cut(const Locations& L, int64_t start, int64_t end_max, double frac = 0.8) {
   if (end_max >= L.nfree) return end_max;
-  const int64_t lo = start + std::max<int64_t>(1, (int64_t)std::ceil(0.8 * (double)(end_max - start)));
+  if (frac >= 1.0) {  // no preference: the last position that is not inside a unit
+    int64_t e = end_max;
+    while (e > start + 1 && L.strength[e] < 0) --e;
+    return e;
+  }
+  const int64_t lo = start + std::max<int64_t>(1, (int64_t)std::ceil(frac * (double)(end_max - start)));
   int64_t best = end_max;
   for (int64_t e = end_max; e >= lo; --e)
     if (L.strength[e] > L.strength[best]) best = e;
@@ -368,7 +403,7 @@ void layout_x_blocks(const Locations& X, BlockLayout& B) {
     if (end == start)
       throw std::invalid_argument("bem_dense: a test dof is supported by more than " + std::to_string(kUCap) +
                                   " quadrature locations");
-    end = cut(X, start, end);
+    end = cut(X, start, end, env_frac("GK_XCUT", 0.8));
     ++trial_id;  // count the locations of the final block
     int64_t nloc = 0;
     for (int64_t q = start; q < end; ++q)
@@ -410,13 +445,13 @@ void layout_y_blocks(const Locations& Y, BlockLayout& B) {
   };
   B.yb.push_back(0);
   for (int64_t q0 = 0; q0 < ncols;) {
-    int64_t q1 = std::min<int64_t>(ncols, q0 + kJCap);
+    int64_t q1 = std::min<int64_t>(ncols, q0 + std::min<int64_t>(kJCap, (int64_t)env_frac("GK_JCAP", kJCap)));
     int64_t nrec = count_records(q0, q1);
     while (nrec > kRCap && q1 - q0 > 1) {
       q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 7 / 8);
       nrec = count_records(q0, q1);
     }
-    const int64_t qc = cut(Y, q0, q1);
+    const int64_t qc = cut(Y, q0, q1, env_frac("GK_YCUT", 0.8));
     if (qc != q1) {
       q1 = qc;
       nrec = count_records(q0, q1);
@@ -574,21 +609,44 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hve
                     hvec<int32_t>& yb_list) {
   const int64_t nJb = (int64_t)B.yb.size() - 1;
   // ---- y blocks (boundaries from the layout): records = incident locations,
-  // each carrying <= 2 (slot, coef) pairs.  Descending first slot: second
-  // slots are larger than first slots, so every second-slot update of a row
-  // comes after that row's own run has been flushed — the run flush is the
-  // row's first touch and can be a plain store; rows without a run of their
-  // own are only ever read-modify-written and get zero-filled (bitmask).
+  // each carrying <= 2 (slot, coef) pairs: a run slot (accumulated in a
+  // register run, flushed to its H row with a plain store when the run ends)
+  // and a read-modify-write slot.  Run order: breadth-first over the block's
+  // slot graph (slots joined by two-slot records) from a slot that has a
+  // single-slot record; every two-slot record runs on its later slot, so each
+  // row's run flush precedes all read-modify-writes of that row, and every
+  // slot reached from such a root has a run of its own.  Rows without a run
+  // (a component with no single-slot record) are zero-filled (bitmask).
+  // unit_y: every dof's contributions share one coefficient -> unit records,
+  // the factor goes to yscale (applied per entry in the gather).
+  bool unit = Y.nfree > 0;
+  T.yscale.assign(Y.nfree, 0.0);
+  for (int64_t q = 0; q < Y.nfree && unit; ++q)
+    for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
+      if (s == Y.dstart[q]) {
+        T.yscale[q] = Y.dcoef[s];
+      } else if (std::memcmp(&Y.dcoef[s], &T.yscale[q], sizeof(double)) != 0) {
+        unit = false;
+        break;
+      }
+    }
+  if (!unit) T.yscale.clear();
+  T.unit_y = unit;
   hvec<YBlock> yb(nJb);
   parallel_for(nJb, [&](int64_t b0, int64_t b1) {
     hvec<int64_t> ystamp(Y.size(), -1);
     hvec<std::pair<int32_t, double>> sl;  // slots of one location inside the block
     hvec<YRec> recs;
     hvec<int32_t> rec_loc, order;
+    int32_t pos[kJCap], queue[kJCap];
+    uint32_t adj[kJCap];
     for (int64_t b = b0; b < b1; ++b) {
       const int64_t q0 = B.yb[b], q1 = B.yb[b + 1];
+      const int nJ = (int)(q1 - q0);
       recs.clear();
       rec_loc.clear();
+      uint32_t single = 0;  // slots with a single-slot record
+      for (int j = 0; j < nJ; ++j) adj[j] = 0;
       for (int64_t q = q0; q < q1; ++q)
         for (int64_t s = Y.dstart[q]; s < Y.dstart[q + 1]; ++s) {
           const int32_t v = Y.dloc[s];
@@ -597,7 +655,7 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hve
           sl.clear();
           for (int64_t c = Y.cstart[v]; c < Y.cstart[v + 1]; ++c) {
             const int32_t pq = Y.iperm[Y.cdof[c]];
-            if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), Y.ccoef[c]});
+            if (pq >= q0 && pq < q1) sl.push_back({(int32_t)(pq - q0), unit ? 1.0 : Y.ccoef[c]});
           }
           std::stable_sort(sl.begin(), sl.end(), [](const auto& a, const auto& c) { return a.first < c.first; });
           for (size_t a = 0; a < sl.size(); a += 2) {
@@ -605,35 +663,66 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hve
             r.x = Y.x[v];
             r.y = Y.y[v];
             r.z = Y.z[v];
-            r.off0 = sl[a].first * kUCap * 16;
+            r.off0 = sl[a].first;  // slot indices for now, byte offsets below
             r.c0 = sl[a].second;
             if (a + 1 < sl.size()) {
-              r.off1 = sl[a + 1].first * kUCap * 16;
+              r.off1 = sl[a + 1].first;
               r.c1 = sl[a + 1].second;
+              adj[r.off0] |= 1u << r.off1;
+              adj[r.off1] |= 1u << r.off0;
             } else {
               r.off1 = -1;
               r.c1 = 0.0;
+              single |= 1u << r.off0;
             }
             recs.push_back(r);
             rec_loc.push_back(v);
           }
         }
+      // breadth-first slot positions, roots with single-slot records first
+      for (int j = 0; j < nJ; ++j) pos[j] = -1;
+      int npos = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int root = 0; root < nJ; ++root) {
+          if (pos[root] >= 0 || (pass == 0 && !((single >> root) & 1u))) continue;
+          int head = npos;
+          pos[root] = npos;
+          queue[npos++] = root;
+          while (head < npos) {
+            const int u = queue[head++];
+            for (uint32_t m = adj[u]; m; m &= m - 1) {
+              const int w = __builtin_ctz(m);
+              if (pos[w] < 0) {
+                pos[w] = npos;
+                queue[npos++] = w;
+              }
+            }
+          }
+        }
+      for (YRec& r : recs)
+        if (r.off1 >= 0 && pos[r.off1] > pos[r.off0]) {
+          std::swap(r.off0, r.off1);
+          std::swap(r.c0, r.c1);
+        }
       order.resize(recs.size());
       std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return recs[a].off0 > recs[c].off0; });
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t c) { return pos[recs[a].off0] < pos[recs[c].off0]; });
       YBlock& YB = yb[b];
       YB.recs.resize(recs.size());
       YB.loc.resize(recs.size());
       uint32_t has_run = 0;
       for (size_t i = 0; i < order.size(); ++i) {
-        const YRec& r = recs[order[i]];
+        YRec r = recs[order[i]];
+        has_run |= 1u << r.off0;
+        r.off0 *= kHS * 16;
+        if (r.off1 >= 0) r.off1 *= kHS * 16;
         YB.recs[i] = r;
         YB.loc[i] = rec_loc[order[i]];
         YB.second |= r.off1 >= 0;
         if (r.off1 >= 0 && std::memcmp(&r.c0, &r.c1, sizeof(double)) != 0) YB.equal = false;
-        has_run |= 1u << (r.off0 / (kUCap * 16));
       }
-      const uint32_t all = (q1 - q0) >= 32 ? 0xffffffffu : ((1u << (q1 - q0)) - 1u);
+      const uint32_t all = nJ >= 32 ? 0xffffffffu : ((1u << nJ) - 1u);
       YB.zero = all & ~has_run;
     }
   });

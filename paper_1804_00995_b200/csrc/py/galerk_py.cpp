@@ -66,6 +66,8 @@ py::dict info_dict(const gk_plan_info& i) {
   d["x_halo"] = i.x_halo;
   d["y_halo"] = i.y_halo;
   d["natural_order"] = (bool)i.natural_order;
+  d["x_blocks"] = i.x_blocks;
+  d["y_blocks"] = i.y_blocks;
   return d;
 }
 
@@ -495,6 +497,15 @@ PYBIND11_MODULE(_galerk, m) {
     double g = 0;
     throw_status(gk_diag_fp64_peak(iters, &g, as_stream(stream)));
     return g;
+  });
+  m.def("diag_fp64_sustained", [](double seconds, uintptr_t scratch, uint64_t bytes, uintptr_t stream) {
+    double gf = 0.0, ms = 0.0;
+    {
+      py::gil_scoped_release rel;
+      throw_status(gk_diag_fp64_sustained(seconds, reinterpret_cast<void*>(scratch), bytes, &gf, &ms,
+                                          as_stream(stream)));
+    }
+    return py::make_tuple(gf, ms);
   });
   m.def("diag_probe_pairs", [](int64_t n, uintptr_t x, uintptr_t y, uintptr_t z, double k, double eps, uintptr_t out,
                                bool fast, uintptr_t stream) {

@@ -50,3 +50,17 @@ def sphere_problem(g, n_target, gauss, family, perturb_seed=None):
     space = g.make_fem(mesh, family)
     hbar = g.edge_stats(mesh).mean_len
     return mesh, dom, space, hbar
+
+
+def load_ref():
+    """The reference's own mesh/quadrature/kernel sources compiled against the
+    Eigen-API shim (oracle/Makefile `ref`, test infrastructure), or None where
+    neither the built module nor /root/reference is available."""
+    out = os.path.join(ROOT, "oracle", "_ref")
+    if not glob.glob(os.path.join(out, "_ref*.so")):
+        if not os.path.isdir("/root/reference/proj/src"):
+            return None
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
+    if out not in sys.path:
+        sys.path.insert(0, out)
+    return importlib.import_module("_ref")
