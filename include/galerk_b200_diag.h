@@ -39,6 +39,14 @@ gk_status gk_diag_probe_pairs(int64_t n, const double* x, const double* y, const
 gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const double* z, double k,
                              double eps, gk_cplx* out, gk_stream stream);
 
+/* The canonical F_analytic probe: the reference formula of
+ * analytic_triangle_integrals (kernels.cpp:151-207, libdevice log / atan /
+ * sqrt / division) for n calls, call i = triangle i % ntri (device [ntri*9]
+ * vertex coordinates) against point i (device [n*3]); out: device [n*4].
+ * ncu's FP64 instruction counters over the launch / n give F_analytic. */
+gk_status gk_diag_probe_analytic(int64_t n, const double* tri, const double* pts, int64_t ntri, double* out,
+                                 gk_stream stream);
+
 /* Device math accuracy probe: out[i] = f(a[i], b[i]) for one scalar helper of
  * the kernels (gk_math.cuh), on device arrays; b may be NULL for unary f.
  *   GK_MATH_LOG_RATIO   log(a / b)            (near-field edge logs, K3)
@@ -49,6 +57,14 @@ gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const 
  *   GK_MATH_RSQRT       1 / sqrt(a)           (1/r of every kernel) */
 enum { GK_MATH_LOG_RATIO = 0, GK_MATH_ATAN2, GK_MATH_DIV, GK_MATH_SIN_QUARTER, GK_MATH_COS_QUARTER, GK_MATH_RSQRT };
 gk_status gk_diag_math(int32_t fn, int64_t n, const double* a, const double* b, double* out, gk_stream stream);
+
+/* Near-field pair list (element pairs in close_pairs order) and, after
+ * gk_nearfield_compute (element-pair form), the number of accepted leaves of
+ * the adaptive recursion per pair (accurate_adaptive, assembly.cpp:581-605):
+ * compared pair by pair with the oracle it counts accept/split decision flips.
+ * Host arrays of gk_nearfield_get_info's `pairs` entries; any may be NULL. */
+typedef struct gk_nearfield gk_nearfield;
+gk_status gk_diag_nearfield_pairs(const gk_nearfield* nf, int32_t* ex, int32_t* ey, int32_t* leaves);
 
 /* Host-only dry run of gk_plan_create (no device needed): fills the plan
  * statistics (locations, tiles, evaluated vs unique pairs) so the tiling can

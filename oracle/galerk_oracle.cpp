@@ -998,9 +998,13 @@ std::vector<Triplet> regularize(const Mesh& mx, int gx, Family fx, const Mesh& m
       stats->pairs++;
       stats->analytic_calls += r.calls;
       stats->gauss_evals += r.gauss;
-      for (int d = 0; d < 8; ++d) stats->depth_hist[d] += r.hist[d];
+      int64_t leaves = 0;
+      for (int d = 0; d < 8; ++d) stats->depth_hist[d] += r.hist[d], leaves += r.hist[d];
+      stats->pair_leaves.push_back((int32_t)leaves);
     }
   }
+  if (stats)
+    for (auto& pr : pairs) stats->pair_ex.push_back(pr.first), stats->pair_ey.push_back(pr.second);
   std::vector<Triplet> out;
   out.reserve(acc.size());
   for (auto& [k, v] : acc) out.push_back({k.second, k.first, v});

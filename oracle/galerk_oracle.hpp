@@ -165,6 +165,9 @@ struct RegStats {
   int64_t analytic_calls = 0;
   int64_t gauss_evals = 0;
   std::array<int64_t, 8> depth_hist{};  // leaves accepted per depth
+  // per near pair, in pair order: the accepted leaves of accurate_adaptive
+  // (a different accept/split decision anywhere changes the count)
+  std::vector<int32_t> pair_ex, pair_ey, pair_leaves;
 };
 enum class NearRule { Ref = 0, TwoHbar = 1 };
 std::vector<std::pair<int, int>> close_pairs(const std::vector<V3>& xc, const std::vector<double>& xr,

@@ -221,6 +221,9 @@ PYBIND11_MODULE(_oracle, m) {
           stats["analytic_calls"] = st.analytic_calls;
           stats["gauss_evals"] = st.gauss_evals;
           stats["depth_hist"] = std::vector<int64_t>(st.depth_hist.begin(), st.depth_hist.end());
+          stats["pair_ex"] = st.pair_ex;
+          stats["pair_ey"] = st.pair_ey;
+          stats["pair_leaves"] = st.pair_leaves;
           return py::make_tuple(r, c, v, stats);
         },
         py::arg("vx"), py::arg("ex"), py::arg("gx"), py::arg("fx"), py::arg("vy"), py::arg("ey"),

@@ -63,17 +63,27 @@ void DevBuf::upload(const void* src, size_t n) {
   if (n) cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
 }
 
+int current_device() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= kMaxDevices) throw CudaError("device index out of range");
+  return dev;
+}
+
 void ensure_pool() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = 256ull << 20;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  });
+  // per device: the release threshold is an attribute of each device's pool
+  static std::mutex m;
+  static uint64_t done = 0;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(m);
+  if ((done >> dev) & 1u) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 256ull << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done |= 1ull << dev;
 }
 
 void DevArena::upload() {
@@ -141,6 +151,12 @@ struct gk_plan {
   DevArena arena;
   size_t o_tiles = 0, o_xl_x = 0, o_xl_y = 0, o_xl_z = 0, o_xsup_start = 0, o_xsup_u = 0, o_xsup_c = 0, o_yrec = 0,
          o_xperm = 0, o_yperm = 0, o_yscale = 0;
+  // dofs supported by more locations than a tile holds (high-degree vertices
+  // with many-point rules): left out of the tiles and computed entry by entry
+  // (k_big_entries) from the full side tables
+  int64_t nbig_rows = 0, nbig_cols = 0;
+  size_t o_big_rows = 0, o_big_cols = 0, o_fx_start = 0, o_fx_loc = 0, o_fx_coef = 0, o_fx_xyz = 0, o_fy_start = 0,
+         o_fy_loc = 0, o_fy_coef = 0, o_fy_xyz = 0;
   uint64_t device_bytes() const { return arena.bytes; }
 };
 
@@ -215,6 +231,23 @@ hvec<TileDesc> make_tile_descs(const TileTables& TX, const TileTables& T) {
   return d;
 }
 
+struct BigDofs {
+  hvec<int32_t> rows, cols;
+};
+// A copy of side s with the listed dofs constrained (-1): they contribute
+// nothing to the tiled assembly.  `store` keeps the masked element table.
+gk_side mask_dofs(const gk_side& s, const hvec<int32_t>& dofs, hvec<int32_t>& store) {
+  gk_side t = s;
+  if (dofs.empty()) return t;
+  hvec<char> is_big((size_t)s.nfree, 0);
+  for (int32_t d : dofs) is_big[d] = 1;
+  store.assign(s.elem_dofs, s.elem_dofs + s.nelem * s.nloc);
+  for (int32_t& d : store)
+    if (d >= 0 && d < s.nfree && is_big[d]) d = -1;
+  t.elem_dofs = store.data();
+  return t;
+}
+
 // k_assemble specialisation of a y side's tables (TileTables::unit_y records
 // carry unit coefficients and need the per-column scales, slots 3)
 int slots_of(const TileTables& T) {
@@ -258,6 +291,34 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
     Y = build_locations(*trial, "bem_dense(trial)");
   }
   lap("locations(trial)");
+  // Oversized dofs: a row needs all its locations in one x block (<= kUCap),
+  // a column all its records in one y block (<= kRCap).  Such dofs (e.g. the
+  // apex of a fan of 24 triangles with a 7-point rule: 168 locations) are
+  // constrained out of the tiled sides (their rows/columns come out 0) and
+  // filled afterwards by k_big_entries from the full tables.
+  BigDofs big;
+  {
+    const Locations& Yf = P->symmetric ? X : Y;
+    for (int64_t d = 0; d < X.nfree; ++d)
+      if (X.dstart[d + 1] - X.dstart[d] > (P->symmetric ? std::min(kUCap, kRCap) : kUCap)) big.rows.push_back((int32_t)d);
+    if (P->symmetric)
+      big.cols = big.rows;
+    else
+      for (int64_t d = 0; d < Yf.nfree; ++d)
+        if (Yf.dstart[d + 1] - Yf.dstart[d] > kRCap) big.cols.push_back((int32_t)d);
+  }
+  Locations Xfull, Yfull;
+  if (!big.rows.empty() || !big.cols.empty()) {
+    hvec<int32_t> ex, ey;
+    const gk_side tx = mask_dofs(*test, big.rows, ex);
+    Xfull = std::move(X);
+    X = build_locations(tx, "bem_dense(test)");
+    if (!P->symmetric) {
+      const gk_side ty = mask_dofs(*trial, big.cols, ey);
+      Yfull = std::move(Y);
+      Y = build_locations(ty, "bem_dense(trial)");
+    }
+  }
   TileTables T = choose_order_and_tile(X, P->symmetric ? nullptr : &Y, P->symmetric, P->eps);
   lap("order+tiles");
   const Locations& Yr = P->symmetric ? X : Y;
@@ -292,6 +353,27 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->o_xperm = Ar.add(X.perm);
   P->o_yperm = Ar.add(Yr.perm);
   P->o_yscale = Ar.add(T.yscale);
+  if (!big.rows.empty() || !big.cols.empty()) {
+    const Locations& Yf = P->symmetric ? Xfull : Yfull;
+    P->nbig_rows = (int64_t)big.rows.size();
+    P->nbig_cols = (int64_t)big.cols.size();
+    P->o_big_rows = Ar.add(big.rows);
+    P->o_big_cols = Ar.add(big.cols);
+    auto side = [&](const Locations& L, size_t& o_start, size_t& o_loc, size_t& o_coef, size_t& o_xyz) {
+      o_start = Ar.add(L.dstart);
+      o_loc = Ar.add(L.dloc);
+      o_coef = Ar.add(L.dcoef);
+      hvec<double> xyz(3 * (size_t)L.size());
+      for (int64_t u = 0; u < L.size(); ++u) xyz[3 * u] = L.x[u], xyz[3 * u + 1] = L.y[u], xyz[3 * u + 2] = L.z[u];
+      o_xyz = Ar.add(xyz);
+    };
+    side(Xfull, P->o_fx_start, P->o_fx_loc, P->o_fx_coef, P->o_fx_xyz);
+    if (P->symmetric) {
+      P->o_fy_start = P->o_fx_start, P->o_fy_loc = P->o_fx_loc, P->o_fy_coef = P->o_fx_coef, P->o_fy_xyz = P->o_fx_xyz;
+    } else {
+      side(Yf, P->o_fy_start, P->o_fy_loc, P->o_fy_coef, P->o_fy_xyz);
+    }
+  }
   lap("stage");
   Ar.upload();
   lap("upload");
@@ -322,8 +404,51 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
   a.natural = P->natural ? 1 : 0;
+  a.prof = nullptr;
+  if (P->nbig_rows || P->nbig_cols) {
+    BigArgs b;
+    b.rows = Ar.at<int32_t>(P->o_big_rows);
+    b.cols = Ar.at<int32_t>(P->o_big_cols);
+    b.nbig_rows = P->nbig_rows;
+    b.nbig_cols = P->nbig_cols;
+    b.nrows = P->rows;
+    b.ncols = P->cols;
+    b.xs = Ar.at<int64_t>(P->o_fx_start);
+    b.xl = Ar.at<int32_t>(P->o_fx_loc);
+    b.xc = Ar.at<double>(P->o_fx_coef);
+    b.xp = Ar.at<double>(P->o_fx_xyz);
+    b.ys = Ar.at<int64_t>(P->o_fy_start);
+    b.yl = Ar.at<int32_t>(P->o_fy_loc);
+    b.yc = Ar.at<double>(P->o_fy_coef);
+    b.yp = Ar.at<double>(P->o_fy_xyz);
+    b.A = A;
+    b.lda = lda;
+    b.eps2 = a.eps2;
+    b.kappa = a.kappa;
+    b.symmetric = a.symmetric;
+    launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
+    launch_big_entries(b, P->helmholtz, stream);  // after the tiles: overwrites their zeros
+    return;
+  }
   // tiles that can hold a coincident pair apply the distance mask; the rest skip it
-  launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
+  if (!std::getenv("GK_ASM_PROF")) {
+    launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
+    return;
+  }
+  // diagnostics: per-tile phase cycles (staging / pair loop / gather + stores)
+  const int64_t nt = P->ntiles + P->nmtiles;
+  DevBuf prof;
+  prof.alloc(sizeof(unsigned long long) * 4 * std::max<int64_t>(1, nt));
+  a.prof = prof.as<unsigned long long>();
+  launch_assemble(a, nt, P->helmholtz, P->slots, stream);
+  cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "GK_ASM_PROF");
+  std::vector<unsigned long long> h((size_t)(4 * nt));
+  cuda_check(cudaMemcpy(h.data(), prof.p, h.size() * 8, cudaMemcpyDeviceToHost), "GK_ASM_PROF copy");
+  double sum[3] = {0, 0, 0};
+  for (int64_t i = 0; i < nt; ++i)
+    for (int k = 0; k < 3; ++k) sum[k] += (double)h[4 * i + k];
+  std::fprintf(stderr, "[gk_asm_prof] tiles %lld  mean cycles: staging %.0f  pair loop %.0f  gather+stores %.0f\n",
+               (long long)nt, sum[0] / nt, sum[1] / nt, sum[2] / nt);
 }
 
 
@@ -356,6 +481,20 @@ size_t blob_add(hvec<char>& b, const V& v) {
 
 
 // Column-slab width for a streamed one-shot call, or 0 for the whole-matrix path.
+// Whether some dof is supported by more points than a tile holds (an upper
+// bound on its merged locations): the streamed path has no oversized-dof
+// fix-up, so such sides take the whole-matrix plan.
+bool may_have_big_dofs(const gk_side& s) {
+  if (s.nfree <= 0 || s.nelem <= 0 || !s.elem_dofs) return false;
+  hvec<int32_t> cnt((size_t)s.nfree, 0);
+  for (int64_t e = 0; e < s.nelem; ++e)
+    for (int l = 0; l < s.nloc; ++l) {
+      const int32_t d = s.elem_dofs[e * s.nloc + l];
+      if (d >= 0 && d < s.nfree && (cnt[d] += s.g) > std::min(kUCap, kRCap)) return true;
+    }
+  return false;
+}
+
 int64_t stream_slab_cols(int64_t rows, int64_t cols) {
   const char* force = std::getenv("GK_SLAB_COLS");
   if (force) return std::max<int64_t>(0, std::atoll(force));
@@ -415,7 +554,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     const int64_t c0 = s * w, c1 = std::min(cols, c0 + w);
     hvec<int32_t> slab_of_full;
     Locations Ys = restrict_cols(Yf, c0, c1, slab_of_full);
-    set_order(Ys, O.natural);
+    set_order(Ys, O.natural, O.unit);
     BlockLayout Bs;
     layout_y_blocks(Ys, Bs);
     TileTables TY;
@@ -530,9 +669,12 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     DevBuf slab[2];
     cudaStream_t ks = nullptr, cs = nullptr;
   };
-  static std::mutex res_mutex;
-  static Resources R;
-  std::lock_guard<std::mutex> hold(res_mutex);
+  // streams, slab buffers and staging belong to one device: one set per device
+  static std::mutex res_mutex[kMaxDevices];
+  static Resources Rs[kMaxDevices];
+  const int dev = current_device();
+  std::lock_guard<std::mutex> hold(res_mutex[dev]);
+  Resources& R = Rs[dev];
   Stage* st = R.st;
   cudaPointerAttributes pa{};
   const bool pinned_dst = cudaPointerGetAttributes(&pa, A_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
@@ -595,6 +737,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     a.kappa = 2.0 * k / M_PI;
     a.symmetric = 0;
     a.natural = 0;
+    a.prof = nullptr;
     double wait_ms = 0.0;
     for (int64_t s = 0; s < nslab; ++s) {
       {
@@ -733,7 +876,7 @@ gk_status gk_plan_assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream
 }
 
 int32_t gk_plan_launches(const gk_plan* P) {
-  return P ? (P->ntiles + P->nmtiles > 0 ? 1 : 0) : 0;
+  return P ? (P->ntiles + P->nmtiles > 0 ? 1 : 0) + (P->nbig_rows + P->nbig_cols > 0 ? 1 : 0) : 0;
 }
 
 gk_status gk_plan_destroy(gk_plan* P) {
@@ -753,7 +896,8 @@ gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kerne
                    std::chrono::duration<double, std::milli>(t1 - t0).count());
       t0 = t1;
     };
-    if (test && trial && kernel && A_host && test->nfree > 0 && trial->nfree > 0 && lda >= test->nfree) {
+    if (test && trial && kernel && A_host && test->nfree > 0 && trial->nfree > 0 && lda >= test->nfree &&
+        !may_have_big_dofs(*test) && !may_have_big_dofs(*trial)) {
       const int64_t w = stream_slab_cols(test->nfree, trial->nfree);
       if (w > 0) {
         check_kernel(kernel);
@@ -776,9 +920,11 @@ gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kerne
     // The device matrix: a grow-only scratch buffer kept between calls up to
     // 16 GB (one-shot callers repeat with the same size, and mapping a fresh
     // 1.7 GB allocation costs ~9 ms); larger matrices are allocated per call.
-    static std::mutex scratch_mutex;
-    static DevBuf scratch;
-    std::unique_lock<std::mutex> hold(scratch_mutex, std::defer_lock);
+    static std::mutex scratch_mutex[kMaxDevices];
+    static DevBuf scratch_of[kMaxDevices];
+    const int dev = current_device();
+    DevBuf& scratch = scratch_of[dev];
+    std::unique_lock<std::mutex> hold(scratch_mutex[dev], std::defer_lock);
     DevBuf own;
     const size_t bytes = sizeof(gk_cplx) * (size_t)P->rows * (size_t)P->cols;
     void* A = nullptr;

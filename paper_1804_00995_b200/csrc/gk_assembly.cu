@@ -26,6 +26,7 @@
 // every record — the P1 edge-midpoint rule — so c*rinv is formed once).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <type_traits>
 
 #include "gk_internal.hpp"
@@ -58,6 +59,8 @@ struct AsmSmem {
   int32_t orow[kIMax];  // original row index of each tile row
   int32_t ocol[kJCap];  // original column index of each tile column
   double ys[kJCap];      // per-column scale (SLOTS == 3)
+  long long prof[3];     // diagnostics (GK_ASM_PROF): phase start clocks
+  unsigned prof_done;    // threads finished (the last one records the end)
 };
 
 __device__ __forceinline__ YRec load_rec(const YRec* p) {
@@ -98,6 +101,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int t = threadIdx.x;
+  if (a.prof && t == 0) S.prof[0] = clock64(), S.prof_done = 0;
   const int4* dp = reinterpret_cast<const int4*>(a.tiles + blockIdx.x);
   const int4 d0 = __ldg(dp), d1 = __ldg(dp + 1), d2 = __ldg(dp + 2);
   const int i0 = d0.x, nI = d0.y, j0 = d0.z, nJ = d0.w;
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     cp_async4(S.xs_u + e, a.xsup_u + xs0 + e);
   }
   for (int e = t; e <= nI; e += kAsmThreads) cp_async4(S.xs_start + e, a.xsup_start + i0 + e);  // global offsets
-  if (!a.natural) {  // natural order: A's row/column index is the permuted one
+  if (!a.natural) {  // natural order: A's row/column index is the permuted one (no maps)
     for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
     for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
   }
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   const double uz = t < nu ? __ldg(a.xl_z + l0 + t) : 0.0;
   cp_async_wait<1>();
   __syncthreads();
+  if (a.prof && t == 0) S.prof[1] = clock64();
 
   const double eps2 = a.eps2, kappa = a.kappa;
   char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
@@ -211,6 +216,27 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   if (nrec > 0) flush();
   cp_async_wait<0>();
   __syncthreads();
+  // diagnostics (GK_ASM_PROF=1): per-tile cycles of staging / pair loop / gather
+  struct PhaseProf {
+    const AsmArgs& a;
+    AsmSmem& S;
+    __device__ ~PhaseProf() {
+      if (!a.prof) return;
+      // no barrier: threads leave the gather at different points; the last
+      // one to finish records the end of the tile
+      __threadfence_block();
+      if (atomicAdd(&S.prof_done, 1u) == blockDim.x - 1) {
+        unsigned long long* o = a.prof + 4ull * blockIdx.x;
+        o[0] = (unsigned long long)(S.prof[1] - S.prof[0]);
+        o[1] = (unsigned long long)(S.prof[2] - S.prof[1]);
+        o[2] = (unsigned long long)(clock64() - S.prof[2]);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        o[3] = smid;
+      }
+    }
+  } prof_guard{a, S};
+  if (a.prof && t == 0) S.prof[2] = clock64();
 
   constexpr int kGC = gather_cols<SLOTS>();
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
@@ -243,9 +269,8 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
         im[q] *= f;
       }
   };
-  if (!a.symmetric || !a.natural) {
-    // non-symmetric plans, and symmetric ones whose rows are scattered in A
-    // (RCB order): direct (and mirror) stores straight from registers
+  if (!a.symmetric) {
+    // non-symmetric plans: direct stores straight from registers
     const int items = nI * ngroups;
     // item e = (row e % nI, column group e / nI), advanced incrementally
     const int di = kAsmThreads % nIs, dg = kAsmThreads / nIs;
@@ -270,13 +295,13 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     }
     return;
   }
-  // Symmetric tiles in natural order (permuted index = A's index; rows and
-  // columns of a tile contiguous in A): thread = (row ii, strip of columns).
-  // The row's supports are loaded once into registers and feed every column
-  // of the strip; each entry is written to (i, j) — lanes along rows, one
-  // coalesced column segment per warp store — and to the mirror (j, i) —
-  // each lane a contiguous run down its own column, two entries per 32-byte
-  // store (STG.256) where aligned.  Only entries with row <= column are formed.
+  // Symmetric tiles: thread = (row ii, strip of columns).  The row's supports
+  // are loaded once into registers and feed every column of the strip; each
+  // entry is written to (i, j) — lanes along rows: one column segment per
+  // warp store (natural order: contiguous; RCB units of 4: 64-byte runs) —
+  // and to the mirror (j, i) — each lane down its own column, two entries per
+  // 32-byte store (STG.256) where two consecutive tile columns are adjacent
+  // rows of A and aligned.  Only entries with row <= column are formed.
   constexpr int kSupCache = 6;  // P0 rules up to 6 points: all supports in registers
   const int nstrip = max(1, kAsmThreads / nIs);
   const int ii = t % nIs, strip = t / nIs;
@@ -285,23 +310,34 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   const int jlo = max(strip * nJ / nstrip, pi - j0), jhi = (strip + 1) * nJ / nstrip;
   if (jlo >= jhi) return;
   const int sb = S.xs_start[ii] - xs0, ns = S.xs_start[ii + 1] - xs0 - sb;
+  // supports padded with coefficient 0 on a real location (finite H): the
+  // first three terms are unconditional (P0 3-point rows have exactly three),
+  // the next three run only for longer rows — no per-term branches
   int su[kSupCache];
   double sc[kSupCache];
+  const int u0 = S.xs_u[sb];
 #pragma unroll
   for (int k = 0; k < kSupCache; ++k) {
-    su[k] = k < ns ? S.xs_u[sb + k] : 0;
+    su[k] = k < ns ? S.xs_u[sb + k] : u0;
     sc[k] = k < ns ? S.xs_c[sb + k] : 0.0;
   }
   auto entry = [&](int j) {
     const double2* Hr = S.H + j * kHS;
     double re = 0.0, im = 0.0;
 #pragma unroll
-    for (int k = 0; k < kSupCache; ++k)
-      if (k < ns) {
+    for (int k = 0; k < 3; ++k) {
+      const double2 h = Hr[su[k]];
+      re = fma(sc[k], h.x, re);
+      im = fma(sc[k], h.y, im);
+    }
+    if (ns > 3) {
+#pragma unroll
+      for (int k = 3; k < kSupCache; ++k) {
         const double2 h = Hr[su[k]];
         re = fma(sc[k], h.x, re);
         im = fma(sc[k], h.y, im);
       }
+    }
     for (int k = kSupCache; k < ns; ++k) {
       const double c = S.xs_c[sb + k];
       const double2 h = Hr[S.xs_u[sb + k]];
@@ -315,45 +351,50 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     }
     return make_double2(re, im);
   };
-  double2* dcol = A + pi + (long long)(j0 + jlo) * lda;  // (pi, j0 + j)
-  double2* mrow = A + (long long)pi * lda + j0;          // (j0 + j, pi) = mrow[j]
+  const bool nat = a.natural != 0;
+  auto ocol = [&](int j) -> long long { return nat ? (long long)(j0 + j) : (long long)S.ocol[j]; };
+  const long long oi = nat ? (long long)pi : (long long)S.orow[ii];
+  double2* const Arow = A + oi;        // direct (oi, oj) = Arow[oj * lda]
+  double2* const Acol = A + oi * lda;  // mirror (oj, oi) = Acol[oj]
   int j = jlo;
   if (j0 + j == pi) {  // diagonal entry: written once
-    *dcol = entry(j);
-    dcol += lda;
+    Arow[ocol(j) * lda] = entry(j);
     ++j;
   }
-  if (j < jhi && ((reinterpret_cast<uintptr_t>(mrow + j) & 31) != 0)) {
-    const double2 v = entry(j);
-    *dcol = v;
-    dcol += lda;
-    mrow[j] = v;
-    ++j;
-  }
-  for (; j + 1 < jhi; j += 2) {
-    const double2 v0 = entry(j), v1 = entry(j + 1);
-    dcol[0] = v0;
-    dcol[lda] = v1;
-    dcol += 2 * lda;
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(mrow + j), "d"(v0.x), "d"(v0.y), "d"(v1.x),
-                 "d"(v1.y)
-                 : "memory");
-  }
-  if (j < jhi) {
-    const double2 v = entry(j);
-    *dcol = v;
-    mrow[j] = v;
+  // The loads of the next entries do not wait for this entry's stores: the
+  // 256-bit store is an asm without a memory clobber (it aliases nothing the
+  // gather reads: shared memory only), so the compiler hoists the next
+  // iteration's LDS above it and the loop is throughput-, not latency-bound.
+#pragma unroll 2
+  while (j < jhi) {
+    const long long oj = ocol(j);
+    double2* const m = Acol + oj;
+    const bool two = j + 1 < jhi && (reinterpret_cast<uintptr_t>(m) & 31) == 0 && ocol(j + 1) == oj + 1;
+    const double2 v0 = entry(j);
+    const double2 v1 = two ? entry(j + 1) : v0;
+    Arow[oj * lda] = v0;
+    if (two) {
+      Arow[(oj + 1) * lda] = v1;
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(m), "d"(v0.x), "d"(v0.y), "d"(v1.x), "d"(v1.y));
+      j += 2;
+    } else {
+      *m = v0;
+      ++j;
+    }
   }
 }
 
 template <bool HELM, int SLOTS>
 void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
   const size_t smem = sizeof(AsmSmem);
-  static bool configured = false;  // one flag per instantiation
-  if (!configured) {
+  // the dynamic shared memory attribute is per device context: one flag per
+  // device and instantiation
+  static std::atomic<uint64_t> configured{0};
+  const int dev = current_device();
+  if (!((configured.load() >> dev) & 1u)) {
     cuda_check(cudaFuncSetAttribute(k_assemble<HELM, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "cudaFuncSetAttribute");
-    configured = true;
+    configured |= 1ull << dev;
   }
   k_assemble<HELM, SLOTS><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
 }
@@ -378,7 +419,60 @@ __global__ void __launch_bounds__(256) k_fetch_tables(int4* __restrict__ dst, co
   for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n16; i += (int64_t)gridDim.x * 256) dst[i] = src[i];
 }
 
+template <bool HELM>
+__global__ void __launch_bounds__(256) k_big_entries(const BigArgs b) {
+  const long long n_r = b.nbig_rows * b.ncols;  // big rows x all columns, then all rows x big columns
+  const long long n = n_r + (b.symmetric ? 0 : b.nrows * b.nbig_cols);
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  long long i, j;
+  if (e < n_r) {
+    i = b.rows[e / b.ncols];
+    j = e % b.ncols;
+  } else {
+    const long long f = e - n_r;
+    i = f % b.nrows;
+    j = b.cols[f / b.nrows];
+  }
+  double re = 0.0, im = 0.0;
+  for (int64_t p = b.xs[i]; p < b.xs[i + 1]; ++p) {
+    const int32_t u = b.xl[p];
+    const double ux = b.xp[3 * u], uy = b.xp[3 * u + 1], uz = b.xp[3 * u + 2];
+    double tr = 0.0, ti = 0.0;  // sum_v c_vj G(u, v)  (assembly.cpp:217, y side first)
+    for (int64_t q = b.ys[j]; q < b.ys[j + 1]; ++q) {
+      const int32_t v = b.yl[q];
+      double dx[1] = {ux - b.yp[3 * v]}, dy[1] = {uy - b.yp[3 * v + 1]}, dz[1] = {uz - b.yp[3 * v + 2]};
+      double cs[1], sn[1], rinv[1];
+      green_parts_n<HELM, 1, true>(dx, dy, dz, b.eps2, b.kappa, cs, sn, rinv);
+      const double w = b.yc[q] * rinv[0];
+      if (HELM) {
+        tr = fma(cs[0], w, tr);
+        ti = fma(sn[0], w, ti);
+      } else {
+        tr += w;
+      }
+    }
+    re = fma(b.xc[p], tr, re);
+    im = fma(b.xc[p], ti, im);
+  }
+  double2* A = reinterpret_cast<double2*>(b.A);
+  A[i + j * b.lda] = make_double2(re, im);
+  if (b.symmetric) A[j + i * b.lda] = make_double2(re, im);
+}
+
 }  // namespace
+
+void launch_big_entries(const BigArgs& b, bool helmholtz, void* stream) {
+  const long long n = b.nbig_rows * b.ncols + (b.symmetric ? 0 : b.nrows * b.nbig_cols);
+  if (n <= 0) return;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (helmholtz)
+    k_big_entries<true><<<blocks, 256, 0, s>>>(b);
+  else
+    k_big_entries<false><<<blocks, 256, 0, s>>>(b);
+  cuda_check(cudaGetLastError(), "k_big_entries launch");
+}
 
 void launch_fetch_tables(void* dst, const void* src_mapped, size_t bytes, void* stream) {
   const int64_t n16 = (int64_t)((bytes + 15) / 16);

@@ -88,6 +88,77 @@ __global__ void __launch_bounds__(256) k_probe(long long n, const double* __rest
   out[i] = make_double2(re, im);
 }
 
+// The reference formula of analytic_triangle_integrals (kernels.cpp:151-207)
+// with libdevice log / atan / sqrt / division: the canonical probe for
+// F_analytic (the FP64 work of one reference call), frozen by
+// ncu like F_pair.  Thread i: triangle i % ntri against point i.
+struct PV {
+  double x, y, z;
+};
+__device__ __forceinline__ PV pv_sub(PV a, PV b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double pv_dot(PV a, PV b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ PV pv_cross(PV a, PV b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double pv_norm(PV a) { return sqrt(pv_dot(a, a)); }
+__device__ __forceinline__ PV pv_scale(PV a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+
+__global__ void __launch_bounds__(256) k_probe_analytic(long long n, const double* __restrict__ tri,
+                                                        const double* __restrict__ pts, long long ntri,
+                                                        double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* t = tri + 9 * (i % ntri);
+  const PV a{t[0], t[1], t[2]}, b{t[3], t[4], t[5]}, c{t[6], t[7], t[8]};
+  const PV x{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  const PV cr = pv_cross(pv_sub(b, a), pv_sub(c, a));
+  const double area2 = pv_norm(cr);
+  const double diam = fmax(fmax(pv_norm(pv_sub(b, a)), pv_norm(pv_sub(c, b))), pv_norm(pv_sub(a, c)));
+  if (area2 <= 1e-14 * diam * diam) {
+    out[4 * i] = nan("");
+    return;
+  }
+  const PV nn = pv_scale(cr, 1.0 / area2);
+  const double w0 = pv_dot(pv_sub(x, a), nn), aw0 = fabs(w0);
+  const PV rho = pv_sub(x, pv_scale(nn, w0));
+  const PV verts[3] = {a, b, c};
+  double newton = 0.0, beta_total = 0.0;
+  PV grad{0, 0, 0}, moment{0, 0, 0};
+  for (int e = 0; e < 3; ++e) {
+    const PV pm = verts[e], pp = verts[(e + 1) % 3];
+    const double len = pv_norm(pv_sub(pp, pm));
+    if (len <= 1e-300) continue;
+    const PV s_hat = pv_scale(pv_sub(pp, pm), 1.0 / len);
+    const PV m_hat = pv_cross(s_hat, nn);
+    const double tt = pv_dot(pv_sub(pm, rho), m_hat);
+    const double sm = pv_dot(pv_sub(pm, rho), s_hat);
+    const double sp = pv_dot(pv_sub(pp, rho), s_hat);
+    const double rm = pv_norm(pv_sub(x, pm));
+    const double rp = pv_norm(pv_sub(x, pp));
+    const double r0sq = tt * tt + w0 * w0;
+    double f = 0.0;
+    if (r0sq > 1e-28 * len * len) {
+      if (sm >= 0.0)
+        f = log((rp + sp) / (rm + sm));
+      else if (sp <= 0.0)
+        f = log((rm - sm) / (rp - sp));
+      else
+        f = log((rp + sp) * (rm - sm) / r0sq);
+    }
+    const double beta = atan(tt * sp / (r0sq + aw0 * rp)) - atan(tt * sm / (r0sq + aw0 * rm));
+    newton += tt * f - aw0 * beta;
+    beta_total += beta;
+    grad = {grad.x + m_hat.x * f, grad.y + m_hat.y * f, grad.z + m_hat.z * f};
+    const double mf = 0.5 * (r0sq * f + sp * rp - sm * rm);
+    moment = {moment.x + m_hat.x * mf, moment.y + m_hat.y * mf, moment.z + m_hat.z * mf};
+  }
+  const double sgn = (w0 > 0.0) ? 1.0 : (w0 < 0.0 ? -1.0 : 0.0);
+  out[4 * i] = newton;
+  out[4 * i + 1] = grad.x + nn.x * (sgn * beta_total);
+  out[4 * i + 2] = moment.x + moment.y + moment.z;
+  out[4 * i + 3] = grad.y + grad.z;
+}
+
 __global__ void __launch_bounds__(256) k_fast(long long n, const double* __restrict__ x, const double* __restrict__ y,
                                               const double* __restrict__ z, double kappa, double eps2,
                                               double2* __restrict__ out) {
@@ -216,6 +287,17 @@ gk_status gk_diag_fast_pairs(int64_t n, const double* x, const double* y, const 
     k_fast<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         n, x, y, z, 2.0 * k / M_PI, eps * eps, reinterpret_cast<double2*>(out));
     cuda_check(cudaGetLastError(), "k_fast");
+  });
+}
+
+gk_status gk_diag_probe_analytic(int64_t n, const double* tri, const double* pts, int64_t ntri, double* out,
+                                 gk_stream stream) {
+  return guard([&] {
+    require_device();
+    if (n <= 0 || ntri <= 0) throw std::invalid_argument("gk_diag_probe_analytic: bad sizes");
+    k_probe_analytic<<<(unsigned)((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, tri, pts, ntri,
+                                                                                                  out);
+    cuda_check(cudaGetLastError(), "k_probe_analytic");
   });
 }
 

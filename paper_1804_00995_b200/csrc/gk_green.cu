@@ -158,18 +158,26 @@ __global__ void __launch_bounds__(kGThreads) k_green32(const GreenArgs a, const 
   __shared__ float2 sq[kGTile];
   const long long t0 = ((long long)blockIdx.x * kGThreads + threadIdx.x) * 2;
   const bool v0 = t0 < a.nt, v1 = t0 + 1 < a.nt;
-  // target-relative source coordinates keep fp32 differences accurate
-  const float x0 = v0 ? a.txf[t0] : 0.f, y0 = v0 ? a.tyf[t0] : 0.f, z0 = v0 ? a.tzf[t0] : 0.f;
-  const float x1 = v1 ? a.txf[t0 + 1] : 0.f, y1 = v1 ? a.tyf[t0 + 1] : 0.f, z1 = v1 ? a.tzf[t0 + 1] : 0.f;
+  // Coordinates relative to the CTA's first target, formed in fp64 and then
+  // rounded to fp32: a near pair's difference carries the fp32 error of the
+  // local offsets (~ the block's extent) instead of that of the absolute
+  // coordinates (~ the scene); far pairs keep ~ulp(scene) in r, which only
+  // moves their phase (K5).
+  const long long tc = min((long long)blockIdx.x * kGThreads * 2, (long long)a.nt - 1);
+  const double cx = a.tx[tc], cy = a.ty[tc], cz = a.tz[tc];
+  const float x0 = v0 ? (float)(a.tx[t0] - cx) : 0.f, y0 = v0 ? (float)(a.ty[t0] - cy) : 0.f,
+              z0 = v0 ? (float)(a.tz[t0] - cz) : 0.f;
+  const float x1 = v1 ? (float)(a.tx[t0 + 1] - cx) : 0.f, y1 = v1 ? (float)(a.ty[t0 + 1] - cy) : 0.f,
+              z1 = v1 ? (float)(a.tz[t0 + 1] - cz) : 0.f;
   double R0 = 0.0, I0 = 0.0, R1 = 0.0, I1 = 0.0;
   const float eps2 = a.eps2f, kappa = a.kappaf;
   for (long long b = 0; b < a.ns; b += kGTile) {
     const int n = (int)min((long long)kGTile, a.ns - b);
     __syncthreads();
     for (int s = threadIdx.x; s < n; s += kGThreads) {
-      sx[s] = a.sxf[b + s];
-      sy[s] = a.syf[b + s];
-      sz[s] = a.szf[b + s];
+      sx[s] = (float)(a.sx[b + s] - cx);
+      sy[s] = (float)(a.sy[b + s] - cy);
+      sz[s] = (float)(a.sz[b + s] - cz);
       const double2 q = Q[b + s];
       sq[s] = make_float2((float)q.x, (float)q.y);
     }
@@ -326,12 +334,15 @@ __global__ void __launch_bounds__(128) k_green32_sym(const GreenArgs a, const do
   int I, J;
   tile_of(blockIdx.x, I0, nb, I, J);
   const long long U = a.nt;
+  // coordinates relative to block I's first location (see k_green32)
+  const long long tc = (long long)I * kSB;
+  const double cx = a.tx[tc], cy = a.ty[tc], cz = a.tz[tc];
   for (int e = threadIdx.x; e < kSB; e += 128) {
     const long long v = (long long)J * kSB + e;
     const bool ok = v < U;
-    sx[e] = ok ? a.txf[v] : 1e6f;  // padding as in the fp64 tile
-    sy[e] = ok ? a.tyf[v] : 0.f;
-    sz[e] = ok ? a.tzf[v] : 0.f;
+    sx[e] = ok ? (float)(a.tx[v] - cx) : 1e6f;  // padding as in the fp64 tile
+    sy[e] = ok ? (float)(a.ty[v] - cy) : 0.f;
+    sz[e] = ok ? (float)(a.tz[v] - cz) : 0.f;
     const double2 qq = ok ? Q[v] : make_double2(0.0, 0.0);
     sq[e] = make_float2((float)qq.x, (float)qq.y);
   }
@@ -342,9 +353,9 @@ __global__ void __launch_bounds__(128) k_green32_sym(const GreenArgs a, const do
   for (int k = 0; k < 2; ++k) {
     const long long v = (long long)I * kSB + w * 64 + 32 * k + lane;
     const bool ok = v < U;
-    tx[k] = ok ? a.txf[v] : -1e6f;
-    ty[k] = ok ? a.tyf[v] : 0.f;
-    tz[k] = ok ? a.tzf[v] : 0.f;
+    tx[k] = ok ? (float)(a.tx[v] - cx) : -1e6f;
+    ty[k] = ok ? (float)(a.ty[v] - cy) : 0.f;
+    tz[k] = ok ? (float)(a.tz[v] - cz) : 0.f;
     const double2 qq = ok ? Q[v] : make_double2(0.0, 0.0);
     tq[k] = make_float2((float)qq.x, (float)qq.y);
   }

@@ -132,7 +132,9 @@ struct DevArena {
     return reinterpret_cast<T*>(static_cast<char*>(p) + off);
   }
 };
-void ensure_pool();  // default memory pool keeps up to 256 MB cached
+void ensure_pool();  // default memory pool keeps up to 256 MB cached (per device)
+constexpr int kMaxDevices = 64;  // process-wide device caches are per device index
+int current_device();            // cudaGetDevice, checked against kMaxDevices
 
 // ---- unique quadrature locations of one side (host) -----------------------------
 // Points that are bit-identical (the edge-midpoint rule's twins, SURVEY trap 1)
@@ -147,6 +149,8 @@ struct Locations {
   hvec<double> ccoef;             // sum over twins of w_k * phi_dof(x_k)
   hvec<int32_t> perm, iperm;      // locality order: perm[p] = dof
   bool natural = false;                  // perm is the identity
+  int unit = 1;                          // RCB over aligned groups of `unit` consecutive dofs
+  double xcut = 0.8;                     // x blocks cut back to a strong boundary in their last (1 - xcut)
   hvec<int8_t> strength;          // [nfree+1] boundary strength of each cut position
   hvec<int64_t> dstart;           // [nfree+1] by permuted dof
   hvec<int32_t> dloc;             // location id
@@ -189,7 +193,7 @@ static_assert(kJCap <= 32, "per-block zero-fill mask is 32 bits");
 // Dof order used for tiling: natural (input numbering; blocks cut at 4^k
 // boundaries of subdivided meshes, rows of A stay contiguous) or recursive
 // coordinate bisection of the dof locations (blocks cut at bisection splits).
-void set_order(Locations& L, bool natural);
+void set_order(Locations& L, bool natural, int unit = 1, double xcut = 0.8);
 
 struct TileTables {
   // x blocks
@@ -232,7 +236,8 @@ Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same,
 struct BlockLayout {
   hvec<int32_t> xb, xloc;  // x block dof starts [nIb+1], locations per block
   hvec<int32_t> yb, yrec;  // y block dof starts [nJb+1], records per block
-  int64_t pairs = 0;
+  int64_t pairs = 0;       // location pairs the tiles evaluate
+  int64_t lane_pairs = 0;  // the same with every x block rounded up to whole warps (issued work)
 };
 BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric);
 TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, const Coincidence& C,
@@ -244,6 +249,7 @@ TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, dou
 // The pieces, for planners that tile one side once and the other in slabs.
 struct OrderChoice {
   bool natural = true;
+  int unit = 1;
   BlockLayout B;
   Coincidence C;
 };
@@ -294,7 +300,30 @@ struct AsmArgs {
   double kappa;  // 2k/pi
   int32_t symmetric;
   int32_t natural;  // dof orders are the identity: A's indices are the permuted ones (no perm lookups)
+  unsigned long long* prof;  // diagnostics: [tile][4] phase cycles + SM id, or null
 };
+// Entries of oversized dofs (rows `rows` x all columns, all rows x columns
+// `cols`; symmetric: rows == cols and both orientations are written), one
+// thread per entry from the full per-dof tables: A_ij = sum_u c_ui sum_v c_vj
+// G(u, v) with the distance mask, in bem_product's nesting.
+struct BigArgs {
+  const int32_t* rows;
+  const int32_t* cols;
+  int64_t nbig_rows, nbig_cols, nrows, ncols;
+  const int64_t* xs;
+  const int32_t* xl;
+  const double* xc;
+  const double* xp;  // [U][3]
+  const int64_t* ys;
+  const int32_t* yl;
+  const double* yc;
+  const double* yp;
+  void* A;
+  int64_t lda;
+  double eps2, kappa;
+  int32_t symmetric;
+};
+void launch_big_entries(const BigArgs& b, bool helmholtz, void* stream);
 // slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0,
 // 3 = unit coefficients with per-column scales (TileTables::unit_y)
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream);

@@ -25,6 +25,7 @@
 #include <map>
 #include <memory>
 
+#include "../../include/galerk_b200_diag.h"
 #include "gk_internal.hpp"
 #include "gk_math.cuh"
 
@@ -120,6 +121,7 @@ struct NfArgs {
   double* local;     // [npairs * kMaxLoc]
   unsigned long long* work;   // atomic pair counter
   unsigned long long* stats;  // [0] analytic calls, [1..7] leaves per depth, [8] degenerate flag
+  int32_t* pair_leaves;       // [npairs] accepted leaves of accurate_adaptive per pair (diagnostics)
 };
 
 __constant__ double c_r7_bary[7][3];
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, NfTune<NT * NTR>::minb) k_nearf
       }
     }
     calls += 7;  // the probe
+    int pair_leaves = 0;
     double adapt[NL];  // leader lanes: accepted splits, in acceptance order
 #pragma unroll
     for (int t = 0; t < NL; ++t) adapt[t] = 0.0;
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(32 * kNfWarps, NfTune<NT * NTR>::minb) k_nearf
           const unsigned m = __ballot_sync(0xffffffffu, leaf && min(depth, 6) == d);
           if (lane == 0 && m) S.leaves[d] += (unsigned long long)__popc(m);
         }
+        pair_leaves += __popc(__ballot_sync(0xffffffffu, leaf));
       }
       const unsigned refused = __ballot_sync(0xffffffffu, leader && !accept);
       const bool mine = (refused >> (lane & ~3)) & 1u;  // my node is refused: push my sub-cell
@@ -577,8 +581,10 @@ __global__ void __launch_bounds__(32 * kNfWarps, NfTune<NT * NTR>::minb) k_nearf
       for (int kk = 0; kk < 8; ++kk) tot += __shfl_sync(0xffffffffu, adapt[t], 4 * kk);
       adapt[t] = tot;
     }
-    if (lane == 0)
+    if (lane == 0) {
       for (int t = 0; t < NL; ++t) a.local[p * kMaxLoc + t] = S.acc[t] + adapt[t];
+      a.pair_leaves[p] = pair_leaves;
+    }
     __syncwarp();
   }
   __syncwarp();
@@ -685,6 +691,25 @@ struct HostMesh {
     }
     return {c.x / 3.0, c.y / 3.0, c.z / 3.0};
   }
+  // kernels.cpp:151-157: analytic_triangle_integrals refuses a triangle with
+  // |(b-a)x(c-a)| <= 1e-14 diam^2 (the regularize loop calls it for the y
+  // triangle of every near pair).  Checked here, on the host, so that
+  // compute / apply / triplets all raise the reference's exception before any
+  // device work (the kernel's own flag stays as a second line of defence).
+  bool degenerate(int64_t k) const {
+    const HV3 a = vert(k, 0), b = vert(k, 1), c = vert(k, 2);
+    const double area2 = hnrm(hcross(hsub(b, a), hsub(c, a)));
+    const double diam = std::max({hnrm(hsub(b, a)), hnrm(hsub(c, b)), hnrm(hsub(a, c))});
+    return area2 <= 1e-14 * diam * diam;
+  }
+  void check_pairs(const std::vector<int32_t>& pey) const {
+    std::vector<char> seen((size_t)ne, 0);
+    for (int32_t e : pey)
+      if (!seen[e]) {
+        seen[e] = 1;
+        if (degenerate(e)) throw std::invalid_argument("analytic_triangle_integrals: degenerate triangle");
+      }
+  }
   double circumradius(int64_t k) const {  // assembly.cpp:358-366
     const HV3 a = vert(k, 0), b = vert(k, 1), c = vert(k, 2);
     const double area = 0.5 * hnrm(hcross(hsub(b, a), hsub(c, a)));
@@ -761,7 +786,7 @@ struct gk_nearfield {
   int64_t npairs = 0, nentries = 0;
   double eps = 0.0;
   DevBuf pair_ex, pair_ey, xv, xe, yv, ye, xq, yq, local, work, stats, ent_row, ent_col, ent_start, ent_src, vals,
-      xrule, yrule;
+      xrule, yrule, leaves;
   std::vector<int32_t> h_row, h_col;
   bool computed = false;
 };
@@ -838,6 +863,7 @@ gk_status gk_nearfield_create(const gk_mesh_side* test, const gk_mesh_side* tria
           }
     }
     N->npairs = (int64_t)pex.size();
+    my.check_pairs(pey);
     // summed entries (setFromTriplets): col-major order, contributions in pair order
     std::map<std::pair<int32_t, int32_t>, std::vector<int64_t>> ent;
     for (int64_t p = 0; p < N->npairs; ++p)
@@ -865,6 +891,7 @@ gk_status gk_nearfield_create(const gk_mesh_side* test, const gk_mesh_side* tria
     N->xq.upload(xq);
     N->yq.upload(yq);
     N->local.alloc(sizeof(double) * kMaxLoc * std::max<int64_t>(1, N->npairs));
+    N->leaves.alloc(sizeof(int32_t) * std::max<int64_t>(1, N->npairs));
     N->work.alloc(sizeof(unsigned long long));
     N->stats.alloc(sizeof(unsigned long long) * 9);
     N->ent_row.upload(N->h_row);
@@ -949,6 +976,7 @@ gk_status gk_nearfield_create_points(int64_t npts, const double* points, const g
           }
     }
     N->npairs = (int64_t)ppt.size();
+    my.check_pairs(pey);
     std::map<std::pair<int32_t, int32_t>, std::vector<int64_t>> ent;  // (col,row) -> contributions
     for (int64_t p = 0; p < N->npairs; ++p)
       for (int j = 0; j < N->ntr; ++j) {
@@ -971,6 +999,7 @@ gk_status gk_nearfield_create_points(int64_t npts, const double* points, const g
     N->ye.upload(trial->elements, sizeof(int32_t) * 3 * trial->ne);
     N->yq.upload(yq);
     N->local.alloc(sizeof(double) * kMaxLoc * std::max<int64_t>(1, N->npairs));
+    N->leaves.alloc(sizeof(int32_t) * std::max<int64_t>(1, N->npairs));
     N->work.alloc(sizeof(unsigned long long));
     N->stats.alloc(sizeof(unsigned long long) * 9);
     N->ent_row.upload(N->h_row);
@@ -1019,6 +1048,7 @@ gk_status gk_nearfield_compute(gk_nearfield* N, gk_stream stream) {
       a.local = N->local.as<double>();
       a.work = N->work.as<unsigned long long>();
       a.stats = N->stats.as<unsigned long long>();
+      a.pair_leaves = N->leaves.as<int32_t>();
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1081,6 +1111,19 @@ gk_status gk_nearfield_triplets(gk_nearfield* N, int32_t* rows, int32_t* cols, d
     if (rows) std::copy(N->h_row.begin(), N->h_row.end(), rows);
     if (cols) std::copy(N->h_col.begin(), N->h_col.end(), cols);
     if (vals) cuda_check(cudaMemcpy(vals, N->vals.p, sizeof(double) * N->nentries, cudaMemcpyDeviceToHost), "vals");
+  });
+}
+
+gk_status gk_diag_nearfield_pairs(const gk_nearfield* N, int32_t* ex, int32_t* ey, int32_t* leaves) {
+  return guard([&] {
+    if (!N) throw std::invalid_argument("gk_diag_nearfield_pairs: null handle");
+    if (N->npairs == 0) return;
+    if (ex) cuda_check(cudaMemcpy(ex, N->pair_ex.p, sizeof(int32_t) * N->npairs, cudaMemcpyDeviceToHost), "pairs");
+    if (ey) cuda_check(cudaMemcpy(ey, N->pair_ey.p, sizeof(int32_t) * N->npairs, cudaMemcpyDeviceToHost), "pairs");
+    if (leaves) {
+      if (!N->computed || N->points) throw std::invalid_argument("gk_diag_nearfield_pairs: no adaptive pass computed");
+      cuda_check(cudaMemcpy(leaves, N->leaves.p, sizeof(int32_t) * N->npairs, cudaMemcpyDeviceToHost), "leaves");
+    }
   });
 }
 

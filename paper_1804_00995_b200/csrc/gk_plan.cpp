@@ -293,9 +293,11 @@ void rcb(hvec<RcbPoint>& pts, int64_t lo, int64_t hi, int64_t leaf, int depth, h
 }
 }  // namespace
 
-void set_order(Locations& L, bool natural) {
+void set_order(Locations& L, bool natural, int unit_req, double xcut) {
   const int64_t n = L.nfree, U = L.size();
   L.natural = natural;
+  L.unit = natural ? 1 : std::max(1, (int)env_frac("GK_UNIT", unit_req));
+  L.xcut = env_frac("GK_XCUT", xcut);
   L.strength.assign(n + 1, 0);
   if (natural) {
     // subdivided meshes number children 4-by-4: boundaries at multiples of 4^k
@@ -322,7 +324,7 @@ void set_order(Locations& L, bool natural) {
     // RCB over units of `unit` consecutive dofs (aligned groups): the rows
     // of a unit stay adjacent in every block, so matrix writes come in whole
     // 32-byte sectors (unit 2) instead of scattered 16-byte halves.
-    const int64_t unit = std::max<int64_t>(1, (int64_t)env_frac("GK_UNIT", 1));
+    const int64_t unit = L.unit;
     hvec<RcbPoint> pts;
     pts.reserve(n / unit + 1);
     for (int64_t d0 = 0; d0 < n; d0 += unit) {
@@ -403,7 +405,7 @@ void layout_x_blocks(const Locations& X, BlockLayout& B) {
     if (end == start)
       throw std::invalid_argument("bem_dense: a test dof is supported by more than " + std::to_string(kUCap) +
                                   " quadrature locations");
-    end = cut(X, start, end, env_frac("GK_XCUT", 0.8));
+    end = cut(X, start, end, X.xcut);
     ++trial_id;  // count the locations of the final block
     int64_t nloc = 0;
     for (int64_t q = start; q < end; ++q)
@@ -465,7 +467,7 @@ void layout_y_blocks(const Locations& Y, BlockLayout& B) {
   }
 }
 
-int64_t layout_pairs(const BlockLayout& B, bool symmetric) {
+int64_t layout_pairs(const BlockLayout& B, bool symmetric, bool lanes = false) {
   int64_t pairs = 0;
   // ---- evaluated pairs: symmetric plans keep tiles whose last column >= first row
   const int64_t nJb = (int64_t)B.yrec.size();
@@ -475,7 +477,7 @@ int64_t layout_pairs(const BlockLayout& B, bool symmetric) {
     int64_t first = 0;
     if (symmetric)  // first y block with yb[bj+1] - 1 >= xb[bi]
       first = std::upper_bound(B.yb.begin() + 1, B.yb.end(), B.xb[bi]) - (B.yb.begin() + 1);
-    pairs += (int64_t)B.xloc[bi] * suffix[first];
+    pairs += (int64_t)(lanes ? (B.xloc[bi] + 31) / 32 * 32 : B.xloc[bi]) * suffix[first];
   }
   return pairs;
 }
@@ -485,6 +487,7 @@ BlockLayout layout_blocks(const Locations& X, const Locations& Y, bool symmetric
   layout_x_blocks(X, B);
   layout_y_blocks(Y, B);
   B.pairs = layout_pairs(B, symmetric);
+  B.lane_pairs = layout_pairs(B, symmetric, true);
   return B;
 }
 
@@ -886,61 +889,95 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
                  std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  // The coincidence sweep and the two candidate orders are independent (the
-  // sweep reads coordinates only; RCB works on copies), so they run
+  // The coincidence sweep and the candidate orders are independent (the
+  // sweep reads coordinates only; the candidates work on copies), so they run
   // concurrently; build_locations left X and Y in natural order.
   auto sweep = std::async(std::launch::async, [&] { return find_coincidences(X, Y ? *Y : X, Y == nullptr, eps); });
   auto layout_of = [&](Locations& Lx, Locations* Ly) { return layout_blocks(Lx, Ly ? *Ly : Lx, symmetric); };
-  bool natural;
-  BlockLayout B;
-  if (f == "natural") {
-    natural = true;
-    B = layout_of(X, Y);
-  } else if (f == "rcb") {
-    natural = false;
-    set_order(X, false);
-    if (Y) set_order(*Y, false);
-    B = layout_of(X, Y);
-  } else {
-    // Natural order keeps the rows of every tile contiguous in A (full-sector,
-    // coalesced writes; a scattered 16-byte write costs a DRAM read-modify-write
-    // of its sector), so it wins unless RCB evaluates >10% fewer pairs.
-    // accept_natural > 0: take natural order without building RCB when it
-    // evaluates at most that many pairs per unique pair (callers whose kernel
-    // time hides under a larger cost, like the PCIe-bound streamed path).
-    if (accept_natural > 0.0) {
-      B = layout_of(X, Y);
-      const double unique = (double)X.size() * (double)(Y ? Y->size() : X.size()) * (symmetric ? 0.5 : 1.0);
-      if ((double)B.pairs <= accept_natural * unique) {
-        OrderChoice O;
-        O.C = sweep.get();
-        O.natural = true;
-        O.B = std::move(B);
-        lap("coincidences+orders (natural accepted)");
-        return O;
-      }
-    }
-    Locations Xr = X, Yr;
-    if (Y) Yr = *Y;
-    auto rcb = std::async(std::launch::async, [&] {
-      set_order(Xr, false);
-      if (Y) set_order(Yr, false);
-      return layout_of(Xr, Y ? &Yr : nullptr);
-    });
-    B = layout_of(X, Y);
-    BlockLayout Br = rcb.get();
-    natural = (double)B.pairs <= 1.10 * (double)Br.pairs;
-    if (!natural) {
-      X = std::move(Xr);
-      if (Y) *Y = std::move(Yr);
-      B = std::move(Br);
+  OrderChoice O;
+  O.natural = true;
+  O.unit = 1;
+  // Candidates (natural, RCB unit, x cut):
+  //  - natural: the input numbering (subdivided meshes number children 4 by
+  //    4), blocks cut back to 4^k subtree boundaries; rows of a tile are
+  //    contiguous in A;
+  //  - RCB over aligned units of 4 consecutive dofs (P0 on a subdivided mesh:
+  //    the 4 children of one parent triangle), x blocks filled to 128
+  //    locations: compact blocks with whole warps busy, and matrix writes in
+  //    64-byte runs;
+  //  - RCB over single dofs, x blocks filled: the most compact blocks for
+  //    unstructured numberings (P1 vertices), but every matrix write is a
+  //    scattered 16-byte half sector (a DRAM read-modify-write): charged 1.25x.
+  // Cost = location pairs issued by whole warps.  The measured cfg-4 P0 tile
+  // structure (L5: natural 2.97 ms vs RCB-unit-4 vs RCB-unit-1 5.0 ms with the
+  // scattered writes) is what set the penalty.
+  struct Cand {
+    bool natural;
+    int unit;
+    double xcut, penalty;
+  };
+  std::vector<Cand> cands;
+  if (f == "natural")
+    cands = {{true, 1, 0.8, 1.0}};
+  else if (f == "rcb")
+    cands = {{false, 1, 1.0, 1.0}};
+  else if (f == "rcb4")
+    cands = {{false, 4, 1.0, 1.0}};
+  else
+    cands = {{true, 1, 0.8, 1.0}, {false, 4, 1.0, 1.0}, {false, 1, 1.0, 1.25}};
+  if (accept_natural > 0.0 && cands.size() > 1) {
+    // take natural order without building the others when it evaluates at
+    // most accept_natural pairs per unique pair (callers whose kernel time
+    // hides under a larger cost, like the PCIe-bound streamed path)
+    BlockLayout B = layout_of(X, Y);
+    const double unique = (double)X.size() * (double)(Y ? Y->size() : X.size()) * (symmetric ? 0.5 : 1.0);
+    if ((double)B.pairs <= accept_natural * unique) {
+      O.C = sweep.get();
+      O.B = std::move(B);
+      lap("coincidences+orders (natural accepted)");
+      return O;
     }
   }
-  OrderChoice O;
+  struct Result {
+    Locations X, Y;
+    BlockLayout B;
+    double cost = 0.0;
+  };
+  std::vector<std::future<Result>> futs;
+  for (size_t c = 1; c < cands.size(); ++c)
+    futs.push_back(std::async(std::launch::async, [&, c] {
+      Result R;
+      R.X = X;
+      if (Y) R.Y = *Y;
+      set_order(R.X, cands[c].natural, cands[c].unit, cands[c].xcut);
+      if (Y) set_order(R.Y, cands[c].natural, cands[c].unit, cands[c].xcut);
+      R.B = layout_of(R.X, Y ? &R.Y : nullptr);
+      R.cost = (double)R.B.lane_pairs * cands[c].penalty;
+      return R;
+    }));
+  if (!cands[0].natural) {
+    set_order(X, false, cands[0].unit, cands[0].xcut);
+    if (Y) set_order(*Y, false, cands[0].unit, cands[0].xcut);
+  }
+  BlockLayout B = layout_of(X, Y);
+  double best = (double)B.lane_pairs * cands[0].penalty;
+  O.natural = cands[0].natural;
+  O.unit = cands[0].unit;
+  for (size_t c = 1; c < cands.size(); ++c) {
+    Result R = futs[c - 1].get();
+    if (R.cost < best) {
+      best = R.cost;
+      X = std::move(R.X);
+      if (Y) *Y = std::move(R.Y);
+      B = std::move(R.B);
+      O.natural = cands[c].natural;
+      O.unit = cands[c].unit;
+    }
+  }
   O.C = sweep.get();
-  O.natural = natural;
   O.B = std::move(B);
-  lap(natural ? "coincidences+orders (natural)" : "coincidences+orders (rcb)");
+  lap(O.natural ? "coincidences+orders (natural)" : (O.unit > 1 ? "coincidences+orders (rcb units)"
+                                                                 : "coincidences+orders (rcb)"));
   return O;
 }
 

@@ -157,6 +157,15 @@ class NearField {
     throw_status(gk_nearfield_triplets(p_, r.data(), c.data(), v.data()));
     return py::make_tuple(r, c, v);
   }
+  // (ex, ey, leaves) per near pair (gk_diag_nearfield_pairs)
+  py::tuple pair_leaves() const {
+    int64_t pairs = 0, entries = 0;
+    throw_status(gk_nearfield_get_info(p_, &pairs, &entries));
+    std::vector<int32_t> ex(pairs), ey(pairs), lv(pairs);
+    throw_status(gk_stream_synchronize(nullptr));
+    throw_status(gk_diag_nearfield_pairs(p_, ex.data(), ey.data(), lv.data()));
+    return py::make_tuple(ex, ey, lv);
+  }
   py::tuple stats() const {
     int64_t calls = 0, hist[8] = {0};
     throw_status(gk_nearfield_stats(p_, &calls, hist));
@@ -408,7 +417,8 @@ PYBIND11_MODULE(_galerk, m) {
       .def("apply", &NearField::apply, py::arg("A"), py::arg("lda"), py::arg("stream") = 0)
       .def("info", &NearField::info)
       .def("triplets", &NearField::triplets)
-      .def("stats", &NearField::stats);
+      .def("stats", &NearField::stats)
+      .def("pair_leaves", &NearField::pair_leaves);
   m.attr("NEAR_REF") = GK_NEAR_REF;
   m.attr("NEAR_2HBAR") = GK_NEAR_2HBAR;
 
@@ -512,6 +522,11 @@ PYBIND11_MODULE(_galerk, m) {
     auto f = fast ? gk_diag_fast_pairs : gk_diag_probe_pairs;
     throw_status(f(n, reinterpret_cast<const double*>(x), reinterpret_cast<const double*>(y),
                    reinterpret_cast<const double*>(z), k, eps, reinterpret_cast<gk_cplx*>(out), as_stream(stream)));
+  });
+  m.def("diag_probe_analytic", [](int64_t n, uintptr_t tri, uintptr_t pts, int64_t ntri, uintptr_t out,
+                                  uintptr_t stream) {
+    throw_status(gk_diag_probe_analytic(n, reinterpret_cast<const double*>(tri), reinterpret_cast<const double*>(pts),
+                                        ntri, reinterpret_cast<double*>(out), as_stream(stream)));
   });
   m.def("diag_math", [](int fn, int64_t n, uintptr_t a, uintptr_t b, uintptr_t out, uintptr_t stream) {
     throw_status(gk_diag_math(fn, n, reinterpret_cast<const double*>(a), reinterpret_cast<const double*>(b),

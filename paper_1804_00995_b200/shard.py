@@ -39,11 +39,12 @@ def row_partition(n: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def _dist():
+def _dist(group=None):
+    """(dist, rank, world) of `group` (default: the whole job)."""
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized():
-        return dist, dist.get_rank(), dist.get_world_size()
+        return dist, dist.get_rank(group), dist.get_world_size(group)
     return None, 0, 1
 
 
@@ -53,7 +54,7 @@ def gather_rows(y_local: torch.Tensor, n: int, group=None) -> torch.Tensor:
     Slabs are padded to the largest slab so that one ``all_gather_into_tensor``
     (NCCL) or ``all_gather`` (gloo) moves them; complex data travels as its
     real view."""
-    dist, rank, world = _dist()
+    dist, rank, world = _dist(group)
     parts = row_partition(n, world)
     if world == 1:
         return y_local
@@ -76,33 +77,41 @@ class ShardedOperator:
     """This rank's row slab of the dense single-layer operator, resident on its GPU.
 
     ``A`` is the (r1 - r0) x cols slab, column-major (``lda = max(1, r1 - r0)``),
-    the same layout ``bem_dense`` returns for the whole matrix."""
+    the same layout ``bem_dense`` returns for the whole matrix.  Rank and
+    slab come from ``group`` (the whole job by default), and every device call
+    runs with ``device`` current, so the plan's tables, the slab and the
+    launches all live on that GPU."""
 
     def __init__(self, dom_x, dom_y, test, kernel, trial, opts=None, device=None, group=None):
-        _, rank, world = _dist()
+        _, rank, world = _dist(group)
         self.rows = test.free_count()
         self.cols = trial.free_count()
         self.r0, self.r1 = row_partition(self.rows, world)[rank]
         self.group = group
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         args = (dom_x, dom_y, test, kernel, trial) + ((opts,) if opts is not None else ())
-        self.plan = AssemblyPlan(*args, row_begin=self.r0, row_end=self.r1)
+        with torch.cuda.device(self.device):
+            self.plan = AssemblyPlan(*args, row_begin=self.r0, row_end=self.r1)
         self.lda = max(1, self.r1 - self.r0)
         self.A = torch.empty(self.cols * self.lda, dtype=torch.complex128, device=self.device)
 
     def assemble(self, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if self.r1 > self.r0:
-            self.plan.assemble(self.A.data_ptr(), self.lda, s.cuda_stream)
+            with torch.cuda.device(self.device):
+                self.plan.assemble(self.A.data_ptr(), self.lda, s.cuda_stream)
         return self
 
     def matvec_local(self, x: torch.Tensor, stream=None) -> torch.Tensor:
         """y[r0:r1] = A[r0:r1, :] x (x replicated, on this rank's device)."""
+        if x.device != self.device:
+            raise ValueError(f"ShardedOperator.matvec_local: x is on {x.device}, the slab on {self.device}")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         y = torch.empty(self.r1 - self.r0, dtype=torch.complex128, device=self.device)
         if self.r1 > self.r0:
-            _matvec(self.A.data_ptr(), self.r1 - self.r0, self.cols, self.lda, x.data_ptr(), y.data_ptr(),
-                    s.cuda_stream)
+            with torch.cuda.device(self.device):
+                _matvec(self.A.data_ptr(), self.r1 - self.r0, self.cols, self.lda, x.data_ptr(), y.data_ptr(),
+                        s.cuda_stream)
         return y
 
     def matvec(self, x: torch.Tensor, stream=None) -> torch.Tensor:
