@@ -131,6 +131,11 @@ gk_status gk_plan_create(const gk_side* test, const gk_side* trial, const gk_ker
 gk_status gk_plan_get_info(const gk_plan* plan, gk_plan_info* info);
 /* A: device, N_test x N_trial, column-major, lda >= N_test.  Overwrites A. */
 gk_status gk_plan_assemble(gk_plan* plan, gk_cplx* A, int64_t lda, gk_stream stream);
+/* Re-targets a plan to another wavenumber: the tables depend only on the
+ * geometry, so one plan serves a frequency sweep (gk_plan_set_wavenumber, then
+ * gk_plan_assemble, per k).  The kernel kind is kept: a "[1/r]" plan stays
+ * k = 0 (kernels.cpp:47-49); k must be finite. */
+gk_status gk_plan_set_wavenumber(gk_plan* plan, double k);
 /* Number of kernel launches gk_plan_assemble issues (for launch accounting). */
 int32_t gk_plan_launches(const gk_plan* plan);
 gk_status gk_plan_destroy(gk_plan* plan);
@@ -228,6 +233,16 @@ typedef struct gk_block {
  * (returns after the results are in the callers' buffers). */
 gk_status gk_evaluator_eval(gk_evaluator* ev, int32_t nblocks, const gk_block* blocks, gk_stream stream);
 gk_status gk_evaluator_destroy(gk_evaluator* ev);
+
+/* Kernel::evaluate_blocks (kernels.hpp:37-39, kernels.cpp:76-131) as one
+ * device panel: out(i, j) = G(x_i, y_j) for the built-in scalar kernels, no
+ * 1/(4 pi), column-major nx x ny (ldo >= nx), HOST arrays (X: nx x 3 and
+ * Y: ny x 3 row-major xyz, out).  mask = 1: pairs with r^2 <= eps_r^2 give 0.
+ * mask = 0: a pair with r^2 <= eps_r^2 fails with GK_ERUNTIME and the
+ * reference's message "kernel evaluation at singular point pair (i,j), r=..."
+ * naming the first such pair in the reference's loop order. */
+gk_status gk_evaluate_blocks(int64_t nx, const double* X, int64_t ny, const double* Y, const gk_kernel* kernel,
+                             double eps_r, int32_t mask, gk_cplx* out, int64_t ldo, gk_stream stream);
 
 /* ---- solve step on the device-resident matrix ------------------------------ */
 /* Partial-pivot LU in place, replacing Eigen's partialPivLu()

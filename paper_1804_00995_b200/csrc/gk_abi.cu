@@ -139,7 +139,7 @@ using namespace gk;
 
 struct gk_plan {
   int64_t rows = 0, cols = 0;
-  bool symmetric = false, helmholtz = false;
+  bool symmetric = false, helmholtz = false, laplace = false;
   double eps = 0.0, k = 0.0;
   int64_t xloc = 0, yloc = 0, pairs_ref = 0, pairs_unique = 0, pairs_eval = 0, ntiles = 0, nmtiles = 0;
   double x_halo = 0.0, y_halo = 0.0;
@@ -269,6 +269,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->cols = trial->nfree;
   P->helmholtz = kernel->kind == GK_HELMHOLTZ && kernel->k != 0.0;
   P->k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;  // "[1/r]" forces k = 0 (kernels.cpp:47-49)
+  P->laplace = kernel->kind == GK_LAPLACE;
   P->eps = guard_radius(*test, *trial);
   P->symmetric = o.symmetric == 1 || (o.symmetric < 0 && sides_identical(*test, *trial));
   const bool timing = std::getenv("GK_TIMING") != nullptr;
@@ -873,6 +874,16 @@ gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
 
 gk_status gk_plan_assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   return guard([&] { assemble(P, A, lda, stream); });
+}
+
+gk_status gk_plan_set_wavenumber(gk_plan* P, double k) {
+  return guard([&] {
+    if (!P) throw std::invalid_argument("gk_plan_set_wavenumber: null plan");
+    if (!std::isfinite(k)) throw std::invalid_argument("bem_dense: wavenumber must be finite");
+    if (P->laplace) return;  // "[1/r]" forces k = 0 (kernels.cpp:47-49)
+    P->k = k;
+    P->helmholtz = k != 0.0;
+  });
 }
 
 int32_t gk_plan_launches(const gk_plan* P) {

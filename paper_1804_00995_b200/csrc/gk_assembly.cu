@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   // the next three run only for longer rows — no per-term branches
   int su[kSupCache];
   double sc[kSupCache];
-  const int u0 = S.xs_u[sb];
+  const int u0 = ns > 0 ? S.xs_u[sb] : 0;  // rows without supports (constrained or oversized dofs): entries 0
 #pragma unroll
   for (int k = 0; k < kSupCache; ++k) {
     su[k] = k < ns ? S.xs_u[sb + k] : u0;

@@ -17,8 +17,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
+#include <string>
+#include <vector>
 
 #include "gk_internal.hpp"
 #include "gk_math.cuh"
@@ -89,6 +92,25 @@ __global__ void __launch_bounds__(256) k_block_eval(const EvalArgs a) {
     im = fma(a.xc[p], si, im);
   }
   a.out[e] = make_double2(re, im);
+}
+
+// Kernel::evaluate_blocks (kernels.cpp:76-131) as a panel: out(i, j) =
+// G(x_i, y_j), column-major nx x ny, one thread per entry (lanes along i).
+// mask = 1: pairs with r^2 <= eps^2 are 0.  mask = 0: the reference raises for
+// the first such pair in its loop order (j outer, i inner = column-major), so
+// the smallest linear index i + j*nx of a singular pair is kept (atomicMin).
+template <bool HELM>
+__global__ void __launch_bounds__(256) k_panel(long long nx, long long ny, const double* __restrict__ X,
+                                               const double* __restrict__ Y, double eps2, double kappa, int mask,
+                                               double2* __restrict__ out, unsigned long long* first_singular) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nx * ny) return;
+  const long long i = e % nx, j = e / nx;
+  const double dx = X[i] - Y[j], dy = X[nx + i] - Y[ny + j], dz = X[2 * nx + i] - Y[2 * ny + j];
+  double cs[1], sn[1], rinv[1], ddx[1] = {dx}, ddy[1] = {dy}, ddz[1] = {dz};
+  green_parts_n<HELM, 1, true>(ddx, ddy, ddz, eps2, kappa, cs, sn, rinv);
+  if (!mask && rinv[0] == 0.0) atomicMin(first_singular, (unsigned long long)e);
+  out[e] = HELM ? make_double2(cs[0] * rinv[0], sn[0] * rinv[0]) : make_double2(rinv[0], 0.0);
 }
 
 void upload_side(SideDev& D, const Locations& L) {
@@ -280,6 +302,61 @@ gk_status gk_evaluator_eval(gk_evaluator* E, int32_t nblocks, const gk_block* bl
         std::memcpy(B.out + (int64_t)j * B.ldo, src + (int64_t)j * B.nrows, sizeof(double2) * B.nrows);
       ++k;
     }
+  });
+}
+
+gk_status gk_evaluate_blocks(int64_t nx, const double* X, int64_t ny, const double* Y, const gk_kernel* kernel,
+                             double eps_r, int32_t mask, gk_cplx* out, int64_t ldo, gk_stream stream) {
+  return guard([&] {
+    if (!kernel) throw std::invalid_argument("evaluate_blocks: null kernel");
+    if (kernel->components != 1)
+      throw std::invalid_argument("assembly: incompatible operand components (1," + std::to_string(kernel->components) +
+                                  ",1)");
+    if (kernel->kind != GK_LAPLACE && kernel->kind != GK_HELMHOLTZ)
+      throw std::invalid_argument("evaluate_blocks: only the built-in scalar Green kernels run on the GPU path");
+    if (nx < 0 || ny < 0 || (nx > 0 && !X) || (ny > 0 && !Y)) throw std::invalid_argument("evaluate_blocks: bad points");
+    if (nx == 0 || ny == 0) return;
+    if (!out || ldo < nx) throw std::invalid_argument("evaluate_blocks: bad output (null or ldo < nx)");
+    require_device();
+    const double k = kernel->kind == GK_LAPLACE ? 0.0 : kernel->k;  // kernels.cpp:47-49
+    const bool helm = k != 0.0;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // SoA point tables (host xyz rows -> device x | y | z)
+    std::vector<double> soa(3 * (size_t)(nx + ny));
+    for (int64_t i = 0; i < nx; ++i)
+      for (int c = 0; c < 3; ++c) soa[c * nx + i] = X[3 * i + c];
+    for (int64_t j = 0; j < ny; ++j)
+      for (int c = 0; c < 3; ++c) soa[3 * nx + c * ny + j] = Y[3 * j + c];
+    DevBuf pts, dout, flag;
+    pts.upload(soa.data(), soa.size() * sizeof(double));
+    dout.alloc(sizeof(double2) * (size_t)(nx * ny));
+    const unsigned long long none = ~0ull;
+    flag.upload(&none, sizeof(none));
+    const long long n = nx * ny;
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    auto launch = [&](auto kern) {
+      kern<<<grid, 256, 0, s>>>(nx, ny, pts.as<double>(), pts.as<double>() + 3 * nx, eps_r * eps_r, 2.0 * k / M_PI,
+                                mask ? 1 : 0, dout.as<double2>(), flag.as<unsigned long long>());
+    };
+    if (helm)
+      launch(k_panel<true>);
+    else
+      launch(k_panel<false>);
+    cuda_check(cudaGetLastError(), "k_panel launch");
+    unsigned long long first = none;
+    cuda_check(cudaMemcpyAsync(&first, flag.p, sizeof(first), cudaMemcpyDeviceToHost, s), "panel flag");
+    cuda_check(cudaStreamSynchronize(s), "panel");
+    if (!mask && first != none) {
+      // kernels.cpp:104-108: the message names the first singular pair and its r
+      const int64_t i = (int64_t)(first % (unsigned long long)nx), j = (int64_t)(first / (unsigned long long)nx);
+      const double dx = X[3 * i] - Y[3 * j], dy = X[3 * i + 1] - Y[3 * j + 1], dz = X[3 * i + 2] - Y[3 * j + 2];
+      const double r = std::sqrt(dx * dx + dy * dy + dz * dz);
+      throw std::runtime_error("kernel evaluation at singular point pair (" + std::to_string(i) + "," +
+                               std::to_string(j) + "), r=" + std::to_string(r));
+    }
+    cuda_check(cudaMemcpy2D(out, sizeof(gk_cplx) * ldo, dout.p, sizeof(gk_cplx) * nx, sizeof(gk_cplx) * nx, ny,
+                            cudaMemcpyDeviceToHost),
+               "panel D2H");
   });
 }
 

@@ -903,14 +903,16 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
   //    contiguous in A;
   //  - RCB over aligned units of 4 consecutive dofs (P0 on a subdivided mesh:
   //    the 4 children of one parent triangle), x blocks filled to 128
-  //    locations: compact blocks with whole warps busy, and matrix writes in
-  //    64-byte runs;
+  //    locations: compact blocks with whole warps busy, but matrix writes in
+  //    64-byte runs only;
   //  - RCB over single dofs, x blocks filled: the most compact blocks for
   //    unstructured numberings (P1 vertices), but every matrix write is a
-  //    scattered 16-byte half sector (a DRAM read-modify-write): charged 1.25x.
-  // Cost = location pairs issued by whole warps.  The measured cfg-4 P0 tile
-  // structure (L5: natural 2.97 ms vs RCB-unit-4 vs RCB-unit-1 5.0 ms with the
-  // scattered writes) is what set the penalty.
+  //    scattered 16-byte half sector (a DRAM read-modify-write).
+  // Cost = location pairs issued by whole warps; both RCB candidates are
+  // charged 1.25x for their writes.  Measured on the cfg-4 P0 tile structure:
+  // natural 47.1 ms vs RCB units of 4 48.6-49.2 ms (17% fewer issued pairs,
+  // but a 1.6x longer gather + store phase) vs RCB single dofs 5.0 vs 3.0 ms
+  // on L5; on P1 (cfg 2) natural issues 1.65x the pairs and RCB wins.
   struct Cand {
     bool natural;
     int unit;
@@ -924,7 +926,7 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
   else if (f == "rcb4")
     cands = {{false, 4, 1.0, 1.0}};
   else
-    cands = {{true, 1, 0.8, 1.0}, {false, 4, 1.0, 1.0}, {false, 1, 1.0, 1.25}};
+    cands = {{true, 1, 0.8, 1.0}, {false, 4, 1.0, 1.25}, {false, 1, 1.0, 1.25}};
   if (accept_natural > 0.0 && cands.size() > 1) {
     // take natural order without building the others when it evaluates at
     // most accept_natural pairs per unique pair (callers whose kernel time

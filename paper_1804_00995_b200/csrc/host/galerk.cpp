@@ -349,6 +349,21 @@ gk_kernel Kernel::abi() const {
   return k;
 }
 
+void Kernel::evaluate_blocks(const std::vector<Vec3>& X, const std::vector<Vec3>& Y, std::vector<MatrixXcd>& out,
+                             double eps_r, bool mask_singular) const {
+  if (custom_) throw std::invalid_argument(
+      "evaluate_blocks: custom kernels have no GPU path (the B200 build has no CPU fallback)");
+  const gk_kernel k = abi();
+  const int64_t nx = (int64_t)X.size(), ny = (int64_t)Y.size();
+  std::vector<double> x(3 * (size_t)nx), y(3 * (size_t)ny);
+  for (int64_t i = 0; i < nx; ++i) x[3 * i] = X[i].x, x[3 * i + 1] = X[i].y, x[3 * i + 2] = X[i].z;
+  for (int64_t j = 0; j < ny; ++j) y[3 * j] = Y[j].x, y[3 * j + 1] = Y[j].y, y[3 * j + 2] = Y[j].z;
+  out.clear();
+  out.emplace_back(nx, ny);  // MatrixXcd is move-only
+  throw_status(gk_evaluate_blocks(nx, x.data(), ny, y.data(), &k, eps_r, mask_singular ? 1 : 0,
+                                  reinterpret_cast<gk_cplx*>(out[0].data()), std::max<int64_t>(1, nx), nullptr));
+}
+
 Kernel green_kernel(const std::string& name, double wavenumber) { return Kernel::green(name, wavenumber); }
 
 double singular_guard_radius(const QuadratureSet& X, const QuadratureSet& Y) {
@@ -611,6 +626,8 @@ gk_plan_info AssemblyPlan::info() const {
 }
 
 int AssemblyPlan::launches() const { return gk_plan_launches(plan_); }
+
+void AssemblyPlan::set_wavenumber(double k) { throw_status(gk_plan_set_wavenumber(plan_, k)); }
 
 // ---------------------------------------------------------------------------------
 GalerkinEvaluator::GalerkinEvaluator(const Domain& dom_x, const Domain& dom_y, const FemSpace& test,

@@ -101,6 +101,7 @@ class FemSpace {
 FemSpace make_fem(const Mesh& mesh, const std::string& family_name);  // P0 | P1
 
 // ---- kernels.hpp ----------------------------------------------------------------
+class MatrixXcd;
 class Kernel {
  public:
   static Kernel green(const std::string& name, double wavenumber);  // kernels.cpp:21-54
@@ -113,6 +114,11 @@ class Kernel {
   // GPU path has no CPU fallback, so assembling with one raises invalid_argument.
   static Kernel custom(int components, const std::string& name = "custom");
   gk_kernel abi() const;
+  // kernels.cpp:76-131 (kernels.hpp:37-39): all components at all point pairs,
+  // pairs within eps_r zeroed (mask) or raising runtime_error "(i,j)" (no
+  // mask); computed on the device (gk_evaluate_blocks).
+  void evaluate_blocks(const std::vector<Vec3>& X, const std::vector<Vec3>& Y, std::vector<MatrixXcd>& out,
+                       double eps_r, bool mask_singular) const;
 
  private:
   int kind_ = GK_HELMHOLTZ;
@@ -202,6 +208,8 @@ class AssemblyPlan {
   AssemblyPlan(const AssemblyPlan&) = delete;
   AssemblyPlan& operator=(const AssemblyPlan&) = delete;
   void assemble(gk_cplx* A_device, int64_t lda, gk_stream stream = nullptr);
+  // frequency sweeps: the same tables at another wavenumber ("[1/r]" stays k = 0)
+  void set_wavenumber(double k);
   gk_plan_info info() const;
   int launches() const;
 

@@ -307,6 +307,7 @@ PYBIND11_MODULE(_galerk, m) {
             p.assemble(reinterpret_cast<gk_cplx*>(A), lda, as_stream(stream));
           },
           py::arg("A"), py::arg("lda"), py::arg("stream") = 0)
+      .def("set_wavenumber", &AssemblyPlan::set_wavenumber, py::arg("k"))
       .def("info", [](const AssemblyPlan& p) { return info_dict(p.info()); })
       .def("launches", &AssemblyPlan::launches);
 
@@ -320,6 +321,24 @@ PYBIND11_MODULE(_galerk, m) {
       py::arg("A"), py::arg("rows"), py::arg("cols"), py::arg("lda"), py::arg("x"), py::arg("y"),
       py::arg("stream") = 0);
   m.def("matvec_launches", &gk_matvec_launches);
+  m.def(
+      "evaluate_blocks",
+      [](F64 X, F64 Y, const Kernel& K, double eps, bool mask) {
+        auto x = X.unchecked<2>();
+        auto y = Y.unchecked<2>();
+        if (x.shape(1) != 3 || y.shape(1) != 3) throw std::invalid_argument("evaluate_blocks: points must be n x 3");
+        const gk_kernel kk = K.abi();
+        const int64_t nx = x.shape(0), ny = y.shape(0);
+        py::array_t<std::complex<double>, py::array::f_style> out({(py::ssize_t)nx, (py::ssize_t)ny});
+        {
+          py::gil_scoped_release rel;
+          throw_status(gk_evaluate_blocks(nx, X.data(), ny, Y.data(), &kk, eps, mask ? 1 : 0,
+                                          reinterpret_cast<gk_cplx*>(out.mutable_data()), std::max<int64_t>(1, nx),
+                                          nullptr));
+        }
+        return out;
+      },
+      py::arg("X"), py::arg("Y"), py::arg("kernel"), py::arg("eps"), py::arg("mask") = true);
   m.def(
       "lu_factor",
       [](uintptr_t A, int64_t n, int64_t lda, uintptr_t ipiv, uintptr_t stream) {
