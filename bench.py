@@ -49,6 +49,11 @@ F_PAIR_PROBE_FLOPS = {True: 106.0, False: 23.0}
 # the production pair loop (SASS count incl. the y-side accumulation), for
 # the executed-work fraction: P1 cfg 2 23 DFMA + 7 DMUL + 4 DADD = 57 flops/pair
 F_PAIR_PROD_FLOPS = {True: 57.0, False: 19.0}
+# F_analytic: FP64 flops of one reference analytic_triangle_integrals
+# call (kernels.cpp:151-207 with libdevice log/atan/sqrt/division), frozen by ncu
+# on the cfg-3 call mix (scripts/fanalytic_probe.py, profiles/r02_fanalytic_probe.txt):
+# 395.8 DFMA + 135.1 DMUL + 108.0 DADD per call = 1034.7 flops.
+F_ANALYTIC_FLOPS = 1034.7
 METRIC = "quadrature-pair kernel evals/s (reference-equivalent M_x*M_y per step, fp64)"
 METRIC_GREEN = "matrix-free Green matvec pair evals/s (reference-equivalent M^2 per matvec, fp64)"
 
@@ -452,6 +457,7 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
             "nearfield": (dict(zip(("pairs", "entries"), nf.info())) | {"analytic_calls": nf.stats()[0], "rule": "ref"})
             if nf else None,
             "nearfield_2hbar": nf_2h,
+            "nearfield_roofline": nearfield_roofline(nf, nf_ms, peaks_fp64) if nf else None,
             "matvec_ms": mv_ms, "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
             "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
             "pairs_evaluated_per_unique": info["pairs_evaluated"] / info["pairs_unique"],
@@ -487,6 +493,30 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
     if with_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
     return out
+
+
+def nearfield_roofline(nf, nf_ms, peaks_fp64):
+    """K3 against the FP64 pipe with the reference algorithm's work: every
+    analytic call accurate_adaptive makes (assembly.cpp:548-605: the probe, then
+    per visited node the node's own 7-point sum again plus its four children's —
+    the device carries the parent's sub-cell value down, 28 calls per node)
+    times F_analytic, plus the Gauss x Gauss 1/r pairs (YContext::gauss,
+    assembly.cpp:504-543) times the Laplace pair probe."""
+    pairs, _ = nf.info()
+    dev_calls = nf.stats()[0]
+    nodes = (dev_calls - 7 * pairs) / 28.0
+    ref_calls = dev_calls + 7.0 * nodes
+    gauss_pairs = pairs * 36  # 6-point rule on both triangles (cfg 3)
+    work = ref_calls * F_ANALYTIC_FLOPS + gauss_pairs * F_PAIR_PROBE_FLOPS[False]
+    achieved = work / (nf_ms * 1e-3) / 1e12
+    burst, sustained, _, _ = peaks_fp64
+    return {"bound": "fp64", "kernel": "k_nearfield_b (K3)", "achieved": achieved, "peak": sustained,
+            "unit": "TFLOP/s", "frac": achieved / sustained, "frac_of_burst": achieved / burst,
+            "reference_calls": ref_calls, "device_calls": dev_calls, "F_analytic_flops": F_ANALYTIC_FLOPS,
+            "work": "reference analytic calls x F_analytic (canonical libdevice probe) + 36 Gauss 1/r pairs per "
+                    "near pair x the Laplace probe; > 1 means the device formulation (solid angle, one log per "
+                    "edge, carried parent values) needs fewer flops than the canonical one",
+            "ncu_fp64_pipe_pct": profile_summary(3).get("k_nearfield_fp64_pipe_pct")}
 
 
 def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup):

@@ -1,9 +1,10 @@
-// TEST INFRASTRUCTURE ONLY.  Python binding of the REFERENCE's own leaf
-// sources, compiled unchanged from /root/reference/proj/src/{mesh,quadrature,
-// kernels}.cpp against the Eigen-API shim in oracle/eigen_shim (recipe:
-// oracle/Makefile target `ref`, output oracle/_ref/).  tests/test_ref_pins.py
-// compares the oracle restatement and the product's host tables with these
-// functions bit for bit, which pins:
+// TEST INFRASTRUCTURE ONLY.  Python binding of the REFERENCE's own sources,
+// compiled unchanged from /root/reference/proj/src/{mesh,quadrature,kernels,
+// femspace,assembly}.cpp and proj/tests/support/oracles.cpp against the
+// Eigen-API shim in oracle/eigen_shim (recipe: oracle/Makefile target `ref`,
+// output oracle/_ref/; the H-matrix engine is stubbed, ref_stubs.cpp).
+// tests/test_ref_pins.py compares the oracle restatement and the product's
+// host tables with these functions, which pins bit for bit:
 //   build_sphere            mesh.cpp:253-309
 //   edge_stats              mesh.cpp:535-567
 //   element_measure         mesh.cpp:47-69
@@ -12,14 +13,21 @@
 //   singular_guard_radius   kernels.cpp:14-19
 //   Kernel::green + evaluate_blocks   kernels.cpp:21-54, 76-131
 //   analytic_triangle_integrals       kernels.cpp:151-207
+// and to rounding (the shim's sparse products sum in their own order):
+//   bem_dense / bem_product            assembly.cpp:144-222, 313-320
+//   radiation_dense                    assembly.cpp:173-190, 334-341
+//   regularize / regularize_radiation  assembly.cpp:355-750
+//   naive_bem                          tests/support/oracles.cpp:332-360
 #include <pybind11/complex.h>
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include "galerk/assembly.hpp"
 #include "galerk/kernels.hpp"
 #include "galerk/mesh.hpp"
 #include "galerk/quadrature.hpp"
+#include "oracles.hpp"
 
 namespace py = pybind11;
 using galerk::MatX3;
@@ -102,6 +110,70 @@ PYBIND11_MODULE(_ref, m) {
   m.def("kernel_info", [](const std::string& name, double k) {
     const galerk::Kernel K = galerk::green_kernel(name, k);
     return py::make_tuple(K.components(), K.wavenumber(), K.singular_name());
+  });
+  auto fem = [](const galerk::Mesh& mm, int fam) { return galerk::make_fem(mm, fam == 1 ? "P1" : "P0"); };
+  auto dense_out = [](const Eigen::MatrixXcd& A) {
+    py::array_t<std::complex<double>, py::array::f_style> out({(py::ssize_t)A.rows(), (py::ssize_t)A.cols()});
+    std::copy(A.data(), A.data() + A.rows() * A.cols(), out.mutable_data());
+    return out;
+  };
+  auto sparse_out = [](const galerk::SpMat& S) {  // col-major triplets
+    std::vector<int> r, c;
+    std::vector<double> v;
+    for (Eigen::Index j = 0; j < S.outerSize(); ++j)
+      for (galerk::SpMat::InnerIterator it(S, j); it; ++it) {
+        r.push_back((int)it.row());
+        c.push_back((int)j);
+        v.push_back(it.value());
+      }
+    return py::make_tuple(r, c, v);
+  };
+  m.def("bem_dense", [=](F64 vx, I32 ex, int gx, int fx, F64 vy, I32 ey, int gy, int fy, const std::string& name,
+                         double k, double cap) {
+    const galerk::Mesh mx = to_mesh(vx, ex), my = to_mesh(vy, ey);
+    galerk::BemOptions o;
+    if (cap > 0) o.memory_cap_bytes = (size_t)cap;
+    Eigen::MatrixXcd A;
+    {
+      py::gil_scoped_release rel;
+      A = galerk::bem_dense(galerk::make_domain(mx, gx), galerk::make_domain(my, gy), fem(mx, fx),
+                            galerk::green_kernel(name, k), fem(my, fy), o);
+    }
+    return dense_out(A);
+  }, py::arg("vx"), py::arg("ex"), py::arg("gx"), py::arg("fx"), py::arg("vy"), py::arg("ey"), py::arg("gy"),
+     py::arg("fy"), py::arg("name"), py::arg("k"), py::arg("cap") = -1.0);
+  m.def("radiation_dense", [=](F64 pts, F64 vy, I32 ey, int gy, int fy, const std::string& name, double k) {
+    const galerk::Mesh my = to_mesh(vy, ey);
+    const MatX3 P = to_x3(pts);
+    Eigen::MatrixXcd A;
+    {
+      py::gil_scoped_release rel;
+      A = galerk::radiation_dense(P, galerk::make_domain(my, gy), galerk::green_kernel(name, k), fem(my, fy));
+    }
+    return dense_out(A);
+  });
+  m.def("naive_bem", [=](F64 vx, I32 ex, int gx, int fx, F64 vy, I32 ey, int gy, int fy, const std::string& name,
+                         double k) {
+    const galerk::Mesh mx = to_mesh(vx, ex), my = to_mesh(vy, ey);
+    return dense_out(oracles::naive_bem(galerk::make_domain(mx, gx), galerk::make_domain(my, gy), fem(mx, fx),
+                                        galerk::green_kernel(name, k), fem(my, fy)));
+  });
+  m.def("regularize", [=](F64 vx, I32 ex, int gx, int fx, F64 vy, I32 ey, int gy, int fy, const std::string& name) {
+    const galerk::Mesh mx = to_mesh(vx, ex), my = to_mesh(vy, ey);
+    galerk::SpMat S;
+    {
+      py::gil_scoped_release rel;
+      S = galerk::regularize(galerk::make_domain(mx, gx), galerk::make_domain(my, gy), fem(mx, fx), name,
+                             fem(my, fy));
+    }
+    return sparse_out(S);
+  });
+  m.def("regularize_radiation", [=](F64 pts, F64 vy, I32 ey, int gy, int fy, const std::string& name) {
+    const galerk::Mesh my = to_mesh(vy, ey);
+    return sparse_out(galerk::regularize_radiation(to_x3(pts), galerk::make_domain(my, gy), name, fem(my, fy)));
+  });
+  m.def("double_newton_oracle", [](py::sequence a, py::sequence b, py::sequence c, double tol) {
+    return oracles::double_newton_oracle(v3(a), v3(b), v3(c), tol);
   });
   m.def("analytic", [](py::sequence a, py::sequence b, py::sequence c, py::sequence x) {
     const galerk::TriangleNewton t = galerk::analytic_triangle_integrals(v3(a), v3(b), v3(c), v3(x));

@@ -350,7 +350,7 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->o_xsup_start = Ar.add(T.xsup_start);
   P->o_xsup_u = Ar.add(T.xsup_u);
   P->o_xsup_c = Ar.add(T.xsup_c);
-  P->o_yrec = Ar.add(T.yrec);
+  P->o_yrec = Ar.add(device_records(T.yrec, P->slots == 3));
   P->o_xperm = Ar.add(X.perm);
   P->o_yperm = Ar.add(Yr.perm);
   P->o_yscale = Ar.add(T.yscale);
@@ -406,6 +406,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.symmetric = P->symmetric ? 1 : 0;
   a.natural = P->natural ? 1 : 0;
   a.prof = nullptr;
+  a.dbg = std::getenv("GK_ASM_DBG") ? std::atoi(std::getenv("GK_ASM_DBG")) : 0;
   if (P->nbig_rows || P->nbig_cols) {
     BigArgs b;
     b.rows = Ar.at<int32_t>(P->o_big_rows);
@@ -581,7 +582,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     T.blob.reserve(descs.size() * sizeof(TileDesc) + TY.yrec.size() * sizeof(YRec) + Ys.perm.size() * 4 +
                    TY.yscale.size() * 8 + 1024);
     T.o_desc = blob_add(T.blob, descs);
-    T.o_yrec = blob_add(T.blob, TY.yrec);
+    T.o_yrec = blob_add(T.blob, device_records(TY.yrec, slots_of(TY) == 3));
     T.o_yperm = blob_add(T.blob, Ys.perm);
     T.o_yscale = blob_add(T.blob, TY.yscale);
     T.ntiles = (int64_t)descs.size();
@@ -739,6 +740,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     a.symmetric = 0;
     a.natural = 0;
     a.prof = nullptr;
+    a.dbg = 0;
     double wait_ms = 0.0;
     for (int64_t s = 0; s < nslab; ++s) {
       {

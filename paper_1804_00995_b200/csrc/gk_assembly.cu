@@ -63,10 +63,27 @@ struct AsmSmem {
   unsigned prof_done;    // threads finished (the last one records the end)
 };
 
-__device__ __forceinline__ YRec load_rec(const YRec* p) {
-  const double2* src = reinterpret_cast<const double2*>(p);
-  const double2 a0 = src[0], a1 = src[1], a2 = src[2];
+// Records in shared memory: 48-byte YRec, or 32-byte YRecU in the unit
+// coefficient mode (SLOTS == 3: no coefficients; two LDS.128 per record).
+template <int SLOTS>
+constexpr int rec_words() {  // 16-byte words per record
+  return SLOTS == 3 ? 2 : 3;
+}
+template <int SLOTS>
+__device__ __forceinline__ YRec load_rec(const double2* src) {
   YRec r;
+  if (SLOTS == 3) {
+    const double2 a0 = src[0], a1 = src[1];
+    r.x = a0.x;
+    r.y = a0.y;
+    r.z = a1.x;
+    r.c0 = r.c1 = 1.0;
+    const long long s = __double_as_longlong(a1.y);
+    r.off0 = (int32_t)(s & 0xffffffffll);
+    r.off1 = (int32_t)(s >> 32);
+    return r;
+  }
+  const double2 a0 = src[0], a1 = src[1], a2 = src[2];
   r.x = a0.x;
   r.y = a0.y;
   r.z = a1.x;
@@ -119,10 +136,12 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   // each thread zero-fills its own column of the rows without a run (the
   // pair loop touches only that column; the gather comes after a barrier)
   for (uint32_t m = zero_rows; m; m &= m - 1) S.H[(__ffs(m) - 1) * kHS + t] = make_double2(0.0, 0.0);
+  constexpr int kRW = rec_words<SLOTS>();
+  const double2* const recs = reinterpret_cast<const double2*>(S.rec);
   {
-    const double2* src = reinterpret_cast<const double2*>(a.yrec + r0);
+    const double2* src = reinterpret_cast<const double2*>(a.yrec) + (long long)r0 * kRW;
     double2* dst = reinterpret_cast<double2*>(S.rec);
-    for (int e = t; e < nrec * 3; e += kAsmThreads) cp_async16(dst + e, src + e);
+    for (int e = t; e < nrec * kRW; e += kAsmThreads) cp_async16(dst + e, src + e);
   }
   cp_async_commit();
   for (int e = t; e < nxs; e += kAsmThreads) {
@@ -149,7 +168,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
   // run accumulator of the current first slot; cur starts at the first
   // record's slot so that the fold below needs no "first run" case
-  int cur = nrec > 0 ? S.rec[0].off0 : 0;  // byte offset of the run's slot row
+  int cur = nrec > 0 ? load_rec<SLOTS>(recs).off0 : 0;  // byte offset of the run's slot row
   double ar = 0.0, ai = 0.0;
   auto flush = [&]() { *reinterpret_cast<double2*>(Hb + cur) = make_double2(ar, ai); };
   // fold one record's evaluated pair G = (cs + i sn) rinv: a run change stores
@@ -188,7 +207,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       // stores in fold() would otherwise force re-loads of every field
       YRec rr[kRecUnroll];
 #pragma unroll
-      for (int k = 0; k < kRecUnroll; ++k) rr[k] = load_rec(&S.rec[r + k]);
+      for (int k = 0; k < kRecUnroll; ++k) rr[k] = load_rec<SLOTS>(recs + (r + k) * kRW);
       double dx[kRecUnroll], dy[kRecUnroll], dz[kRecUnroll];
 #pragma unroll
       for (int k = 0; k < kRecUnroll; ++k) {
@@ -202,7 +221,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       for (int k = 0; k < kRecUnroll; ++k) fold(rr[k], cs[k], sn[k], rinv[k]);
     }
     for (; r < nrec; ++r) {
-      const YRec p = load_rec(&S.rec[r]);
+      const YRec p = load_rec<SLOTS>(recs + r * kRW);
       double dx[1] = {ux - p.x}, dy[1] = {uy - p.y}, dz[1] = {uz - p.z};
       double cs[1], sn[1], rinv[1];
       green_parts_n<HELM, 1, MASK>(dx, dy, dz, eps2, kappa, cs, sn, rinv);
@@ -303,6 +322,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   // 32-byte store (STG.256) where two consecutive tile columns are adjacent
   // rows of A and aligned.  Only entries with row <= column are formed.
   constexpr int kSupCache = 6;  // P0 rules up to 6 points: all supports in registers
+  if (a.dbg & 2) return;
   const int nstrip = max(1, kAsmThreads / nIs);
   const int ii = t % nIs, strip = t / nIs;
   if (t >= nstrip * nIs || ii >= nI) return;
@@ -361,10 +381,10 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     Arow[ocol(j) * lda] = entry(j);
     ++j;
   }
-  // The loads of the next entries do not wait for this entry's stores: the
-  // 256-bit store is an asm without a memory clobber (it aliases nothing the
-  // gather reads: shared memory only), so the compiler hoists the next
-  // iteration's LDS above it and the loop is throughput-, not latency-bound.
+  // (A branch-free natural-order variant of this loop — six hoisted LDS.128
+  // per column pair, no per-pair checks — measured slower overall, 51.3 vs
+  // 47.7 ms on cfg 4: its faster bursts of loads and stores stretch the other
+  // CTAs' pair loops, which share the MIO/L1 pipe.)
 #pragma unroll 2
   while (j < jhi) {
     const long long oj = ocol(j);
@@ -372,6 +392,11 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     const bool two = j + 1 < jhi && (reinterpret_cast<uintptr_t>(m) & 31) == 0 && ocol(j + 1) == oj + 1;
     const double2 v0 = entry(j);
     const double2 v1 = two ? entry(j + 1) : v0;
+    if (a.dbg & 1) {  // timing experiment: no stores (keep the values live)
+      if (v0.x == 1234.5 && v1.y == 6.5) Arow[0] = v0;
+      j += two ? 2 : 1;
+      continue;
+    }
     Arow[oj * lda] = v0;
     if (two) {
       Arow[(oj + 1) * lda] = v1;

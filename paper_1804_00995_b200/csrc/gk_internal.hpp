@@ -188,6 +188,13 @@ struct YRec {  // one y location restricted to one tile's dofs (<= 2 slots)
   int32_t off0, off1;  // byte offsets slot * kHS * 16 into H (off0: run slot, off1: read-modify-write slot or -1)
 };
 static_assert(sizeof(YRec) == 48, "YRec layout");
+struct YRecU {  // the 32-byte record of the unit-coefficient mode (k_assemble SLOTS 3)
+  double x, y, z;
+  int32_t off0, off1;
+};
+static_assert(sizeof(YRecU) == 32, "YRecU layout");
+// The device record table of a y side: YRecU for unit coefficients, else YRec.
+hvec<char> device_records(const hvec<YRec>& recs, bool unit);
 static_assert(kJCap <= 32, "per-block zero-fill mask is 32 bits");
 
 // Dof order used for tiling: natural (input numbering; blocks cut at 4^k
@@ -301,6 +308,7 @@ struct AsmArgs {
   int32_t symmetric;
   int32_t natural;  // dof orders are the identity: A's indices are the permuted ones (no perm lookups)
   unsigned long long* prof;  // diagnostics: [tile][4] phase cycles + SM id, or null
+  int32_t dbg;               // timing experiments only (GK_ASM_DBG; results invalid when set): 1 no stores, 2 no gather
 };
 // Entries of oversized dofs (rows `rows` x all columns, all rows x columns
 // `cols`; symmetric: rows == cols and both orientations are written), one

@@ -4,6 +4,7 @@
 // matrices (W B)^T and per-dof std::map lists; here the same information is
 // laid out for the device as unique locations + per-tile tables.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -544,6 +545,74 @@ struct YBlock {  // one y block's records, in descending first-slot order
 };
 }  // namespace
 
+namespace {
+// Location slots of one x block, chosen so that the gather's shared-memory
+// reads are free of bank conflicts.  The gather thread of row ii reads
+// H[j][u_k(ii)] for its k-th support; a 16-byte LDS is served in four phases
+// of eight consecutive lanes (rows), each conflict-free iff its eight slots
+// lie in distinct 16-byte bank groups (slot mod 8).  First-appearance slots
+// put the supports of neighbouring rows at slot ~1.5 ii, two per bank group.
+// Here locations are greedily coloured with residues mod 8 such that no two
+// different locations at the same support position k of rows in the same
+// phase share a residue (capacity kUCap/8 locations per residue), and the
+// slot of a location is its residue + 8 x its rank within the residue.
+// The slot is also the pair-loop thread that owns the location, so nothing
+// else changes.  Falls back to first-appearance slots if the colouring fails.
+void bank_balance(XBlock& XB) {
+  const int nl = (int)XB.locs.size();
+  if (nl == 0 || nl > kUCap) return;
+  const int nrows = (int)XB.sup_n.size();
+  hvec<int32_t> start(nrows + 1, 0);
+  for (int r = 0; r < nrows; ++r) start[r + 1] = start[r] + XB.sup_n[r];
+  // conflict graph: bitsets over locations (<= 128) per location
+  std::vector<std::array<uint64_t, 2>> adj(nl, {0ull, 0ull});
+  auto link = [&](int a, int b) {
+    if (a == b) return;
+    adj[a][b >> 6] |= 1ull << (b & 63);
+    adj[b][a >> 6] |= 1ull << (a & 63);
+  };
+  for (int p0 = 0; p0 < nrows; p0 += 8)
+    for (int k = 0; k < 8; ++k)
+      for (int r1 = p0; r1 < std::min(nrows, p0 + 8); ++r1)
+        for (int r2 = r1 + 1; r2 < std::min(nrows, p0 + 8); ++r2)
+          if (k < XB.sup_n[r1] && k < XB.sup_n[r2]) link(XB.sup_u[start[r1] + k], XB.sup_u[start[r2] + k]);
+  hvec<int8_t> color(nl, -1);
+  int load[8] = {0};
+  const int cap = kUCap / 8;
+  // most constrained first (degree), ties by first appearance
+  hvec<int32_t> order(nl);
+  std::iota(order.begin(), order.end(), 0);
+  auto deg = [&](int a) { return __builtin_popcountll(adj[a][0]) + __builtin_popcountll(adj[a][1]); };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return deg(a) > deg(b); });
+  for (int a : order) {
+    int clash[8] = {0};  // coloured neighbours per residue
+    for (int w = 0; w < 2; ++w)
+      for (uint64_t m = adj[a][w]; m; m &= m - 1) {
+        const int b = w * 64 + __builtin_ctzll(m);
+        if (color[b] >= 0) ++clash[color[b]];
+      }
+    int best = -1;  // fewest clashes (a clash costs one extra wavefront), then lightest residue
+    for (int c = 0; c < 8; ++c)
+      if (load[c] < cap && (best < 0 || clash[c] < clash[best] || (clash[c] == clash[best] && load[c] < load[best])))
+        best = c;
+    if (best < 0) return;  // keep first-appearance slots
+    color[a] = (int8_t)best;
+    ++load[best];
+  }
+  hvec<int32_t> slot(nl), rank(8, 0);
+  for (int a = 0; a < nl; ++a) slot[a] = color[a] + 8 * rank[color[a]]++;
+  hvec<int32_t> locs(kUCap, -1);
+  for (int a = 0; a < nl; ++a) locs[slot[a]] = XB.locs[a];
+  for (int32_t& u : XB.sup_u) u = slot[u];
+  // slots are sparse now: unused ones hold no location (the pair loop's
+  // padding threads), so the block's location list keeps kUCap-granular holes
+  int top = 0;
+  for (int i = 0; i < kUCap; ++i)
+    if (locs[i] >= 0) top = i + 1;
+  XB.locs.assign(locs.begin(), locs.begin() + top);
+}
+}  // namespace
+
 void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, hvec<int32_t>& xl_id) {
   const int64_t nrows = X.nfree;
   const int64_t nIb = (int64_t)B.xb.size() - 1;
@@ -567,6 +636,7 @@ void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, hve
         }
         XB.sup_n.push_back((int32_t)(X.dstart[p + 1] - X.dstart[p]));
       }
+      bank_balance(XB);
     }
   });
   xl_id.clear();  // global x location id of every block entry (parallel to xl_x)
@@ -597,15 +667,30 @@ void build_x_tables(const Locations& X, const BlockLayout& B, TileTables& T, hve
       T.xsup_u.insert(T.xsup_u.end(), XB.sup_u.begin(), XB.sup_u.end());
       T.xsup_c.insert(T.xsup_c.end(), XB.sup_c.begin(), XB.sup_c.end());
       for (int32_t u : XB.locs) {
-        T.xl_x.push_back(X.x[u]);
-        T.xl_y.push_back(X.y[u]);
-        T.xl_z.push_back(X.z[u]);
+        // bank_balance holes: an unused slot is a far point (finite pair
+        // values in a column no row reads), like the kernel's idle lanes
+        T.xl_x.push_back(u >= 0 ? X.x[u] : 1e100);
+        T.xl_y.push_back(u >= 0 ? X.y[u] : 0.0);
+        T.xl_z.push_back(u >= 0 ? X.z[u] : 0.0);
         xl_id.push_back(u);
       }
       T.xb_dof_start.push_back((int32_t)p);
       T.xb_loc_start.push_back((int32_t)T.xl_x.size());
     }
   }
+}
+
+hvec<char> device_records(const hvec<YRec>& recs, bool unit) {
+  hvec<char> out;
+  if (!unit) {
+    out.resize(recs.size() * sizeof(YRec));
+    if (!recs.empty()) std::memcpy(out.data(), recs.data(), out.size());
+    return out;
+  }
+  out.resize(recs.size() * sizeof(YRecU));
+  YRecU* u = reinterpret_cast<YRecU*>(out.data());
+  for (size_t i = 0; i < recs.size(); ++i) u[i] = {recs[i].x, recs[i].y, recs[i].z, recs[i].off0, recs[i].off1};
+  return out;
 }
 
 void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hvec<int64_t>& yb_start,
@@ -788,6 +873,7 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
     parallel_for(nIb, [&](int64_t b0, int64_t b1) {
       for (int64_t bi = b0; bi < b1; ++bi) {
         for (int32_t e = TX.xb_loc_start[bi]; e < TX.xb_loc_start[bi + 1]; ++e) {
+          if (xl_id[e] < 0) continue;  // a bank_balance hole
           const int32_t v = C.y_of_x[xl_id[e]];
           if (v >= 0)
             masked_j[bi].insert(masked_j[bi].end(), yb_list.begin() + yb_start[v], yb_list.begin() + yb_start[v + 1]);
