@@ -6,7 +6,10 @@ that fits one GPU): unit-sphere icosphere L6 (40962 vertices, 81920
 triangles), P0, 3-point (edge-midpoint) rule, Helmholtz single layer with
 k = 2 pi / (10 hbar).  One step = dense assembly of the 81920 x 81920
 complex128 matrix (107 GB, resident in HBM; K1+K2) followed by 10 stored
-matvecs y = A x (K4) with seeded complex N(0,1) vectors (seed 3).
+matvecs y = A x (K4) with seeded complex N(0,1) vectors (seed 3).  The ten
+vectors are independent, so the step multiplies them in one pass over A
+(gk_matvec_multi, Y = A X; --matvec single: one gk_matvec per vector, ten
+passes).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                   [--config 1|2|3|4|5] [--extras 2,3,5|none]
@@ -14,7 +17,8 @@ matvecs y = A x (K4) with seeded complex N(0,1) vectors (seed 3).
 Metric: reference-equivalent quadrature-pair kernel evaluations per second
 (M_x * M_y per step / step time).  `roofline` is the assembly kernel against
 the FP64 pipe (sustained DFMA peak measured in the same run); `roofline_matvec`
-the stored matvec against HBM.  With the default config the cfg 2 / cfg 3 /
+the single-vector stored matvec against HBM; `roofline_matvec_multi` the
+step's one-pass multiply of all vectors (FP64 or HBM, whichever binds).  With the default config the cfg 2 / cfg 3 /
 cfg 5 lines (smaller workloads, BASELINE configs[1], [2], [4]) are measured
 first and nested under "other_configs".
 
@@ -78,6 +82,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-chunks", type=int, default=8, help="1024-point x chunks of the 1-thread CPU baseline")
+    p.add_argument("--matvec", choices=["multi", "single"], default="multi",
+                   help="the step's stored matvecs: one pass over A for all vectors (gk_matvec_multi) or one "
+                        "gk_matvec per vector")
     return p.parse_args()
 
 
@@ -381,7 +388,10 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     nf = g.NearField(dom, dom, space, "[1/r]", space) if cfg == 3 else None
-    launches_per_step = plan.launches() + nmv * g.matvec_launches(n, n) + (3 if nf else 0)
+    multi = args.matvec == "multi" and nmv > 1
+    Y = torch.empty((nmv, n), dtype=torch.complex128, device=dev)
+    mv_launches = g.matvec_multi_launches(n, n, nmv) if multi else nmv * g.matvec_launches(n, n)
+    launches_per_step = plan.launches() + mv_launches + (3 if nf else 0)
 
     def step(ev=None):
         if ev:
@@ -394,8 +404,11 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
             nf.apply(A.data_ptr(), n, sp)
         if ev:
             ev[1].record(stream)
-        for i in range(nmv):
-            g.matvec(A.data_ptr(), n, n, n, X[i].data_ptr(), y.data_ptr(), sp)
+        if multi:  # the nmv independent vectors in one pass over A
+            g.matvec_multi(A.data_ptr(), n, n, n, X.data_ptr(), n, Y.data_ptr(), n, nmv, sp)
+        else:
+            for i in range(nmv):
+                g.matvec(A.data_ptr(), n, n, n, X[i].data_ptr(), Y[i].data_ptr(), sp)
         if ev:
             ev[2].record(stream)
 
@@ -418,8 +431,17 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
     total_ms = max_over_ranks(t0.elapsed_time(t1), dist, dev)
     asm_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in evs]))
     nf_ms = float(np.mean([e[3].elapsed_time(e[1]) for e in evs])) if nf else None
-    mv_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs])) / nmv
+    mvs_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))  # all of the step's matvecs
     ms_step = total_ms / steps
+    # the single-vector stored matvec (K4, HBM-bound) timed on its own
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.matvec(A.data_ptr(), n, n, n, X[0].data_ptr(), y.data_ptr(), sp)
+    m0.record(stream)
+    for _ in range(5):
+        g.matvec(A.data_ptr(), n, n, n, X[0].data_ptr(), y.data_ptr(), sp)
+    m1.record(stream)
+    torch.cuda.synchronize(dev)
+    mv_ms = m0.elapsed_time(m1) / 5
     pairs_ref = info["pairs_reference"]
     value = aggregate_value(pairs_ref, world, ms_step)
     nf_2h = None
@@ -459,6 +481,8 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
             "nearfield_2hbar": nf_2h,
             "nearfield_roofline": nearfield_roofline(nf, nf_ms, peaks_fp64) if nf else None,
             "matvec_ms": mv_ms, "matvec_gbs": mv_bytes / (mv_ms * 1e-3) / 1e9,
+            "matvecs_step_ms": mvs_ms, "matvec_mode": "multi (gk_matvec_multi: %d vectors, one pass over A)" % nmv
+            if multi else "single (one gk_matvec per vector)",
             "unique_pairs_per_s": info["pairs_unique"] / (asm_ms * 1e-3),
             "pairs_evaluated_per_unique": info["pairs_evaluated"] / info["pairs_unique"],
             "plan": {k_: info[k_] for k_ in ("tiles", "x_halo", "y_halo", "natural_order", "device_bytes")},
@@ -481,18 +505,34 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
                                 "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
                                 "traffic": prof.get("k_matvec_dram_bytes_per_call"),
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "roofline_matvec_multi": matvec_multi_roofline(n, nmv, mvs_ms, hbm, peaks_fp64) if multi else None,
             "step_share": {"assembly": asm_ms / ms_step, "nearfield": (nf_ms or 0.0) / ms_step,
-                           "matvecs": mv_ms * nmv / ms_step},
+                           "matvecs": mvs_ms / ms_step},
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * steps,
         }
     if with_e2e and rank == 0:
         del A  # the e2e leg allocates its own device matrix
         torch.cuda.empty_cache()
-        out["e2e"] = e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup)
+        out["e2e"] = e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup, multi)
     if with_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
     return out
+
+
+def matvec_multi_roofline(n, nmv, ms, hbm, peaks_fp64):
+    """Y = A X over nmv vectors in one pass: 16 N^2 bytes of A (+ X, Y) against
+    HBM, and 8 flops per complex multiply-add per vector (4 DFMA) against the
+    FP64 pipe; the bound is the larger fraction."""
+    t = ms * 1e-3
+    gbs = (16.0 * n * n + 32.0 * n * nmv) / t / 1e9
+    tfs = 8.0 * n * n * nmv / t / 1e12
+    sustained = peaks_fp64[1]
+    fh, ff = gbs / hbm, tfs / sustained
+    return {"bound": "fp64" if ff >= fh else "hbm", "kernel": "k_matvec_multi_partial<%d> + reduce (K4, %d right-hand "
+            "sides)" % (min(nmv, 10), nmv), "achieved": tfs if ff >= fh else gbs,
+            "peak": sustained if ff >= fh else hbm, "unit": "TFLOP/s" if ff >= fh else "GB/s", "frac": max(ff, fh),
+            "hbm_gbs": gbs, "frac_hbm": fh, "fp64_tflops": tfs, "frac_fp64": ff, "ms": ms}
 
 
 def nearfield_roofline(nf, nf_ms, peaks_fp64):
@@ -519,11 +559,12 @@ def nearfield_roofline(nf, nf_ms, peaks_fp64):
             "ncu_fp64_pipe_pct": profile_summary(3).get("k_nearfield_fp64_pipe_pct")}
 
 
-def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup):
+def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup, multi):
     """The same step through the public host API with HOST buffers: host side
     tables -> AssemblyPlan (gk_plan_create: host planning + table upload) ->
     gk_plan_assemble into the device-resident matrix [-> NearField] -> per
-    vector: pinned x host->device, gk_matvec, y device->host.  Wall clock per
+    vector: pinned x host->device, gk_matvec, y device->host (multi: all vectors
+    host->device, one gk_matvec_multi, all results device->host).  Wall clock per
     step, everything inside; the matrix buffer is allocated once (the device
     memory the caller keeps A in)."""
     s = SPECS[cfg]
@@ -531,8 +572,8 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
     A = torch.empty(n * n, dtype=torch.complex128, device=dev)
     xh = torch.tensor(np.asarray(xs, dtype=np.complex128).reshape(nmv, n)).pin_memory()
     yh = torch.empty((nmv, n), dtype=torch.complex128).pin_memory()
-    xd = torch.empty(n, dtype=torch.complex128, device=dev)
-    yd = torch.empty(n, dtype=torch.complex128, device=dev)
+    xd = torch.empty((nmv, n), dtype=torch.complex128, device=dev)
+    yd = torch.empty((nmv, n), dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     h2d_tables = [0]
@@ -545,10 +586,15 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
             nf = g.NearField(dom, dom, space, "[1/r]", space)
             nf.compute(sp)
             nf.apply(A.data_ptr(), n, sp)
-        for i in range(nmv):
-            xd.copy_(xh[i], non_blocking=True)
-            g.matvec(A.data_ptr(), n, n, n, xd.data_ptr(), yd.data_ptr(), sp)
-            yh[i].copy_(yd, non_blocking=True)
+        if multi:
+            xd.copy_(xh, non_blocking=True)
+            g.matvec_multi(A.data_ptr(), n, n, n, xd.data_ptr(), n, yd.data_ptr(), n, nmv, sp)
+            yh.copy_(yd, non_blocking=True)
+        else:
+            for i in range(nmv):
+                xd[0].copy_(xh[i], non_blocking=True)
+                g.matvec(A.data_ptr(), n, n, n, xd[0].data_ptr(), yd[0].data_ptr(), sp)
+                yh[i].copy_(yd[0], non_blocking=True)
         torch.cuda.synchronize(dev)
 
     for _ in range(max(1, min(3, warmup))):
@@ -565,8 +611,10 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
             "d2h_bytes_per_step": int(16 * n * nmv), "s_per_step": t, "s_per_step_median": float(np.median(ts)),
             "steps": steps,
             "path": "C-ABI through the host API: host mesh tables -> gk_plan_create (host plan + table upload) -> "
-                    "gk_plan_assemble (device-resident A)%s -> %d x (x pinned H2D, gk_matvec, y D2H); wall clock"
-                    % (" -> gk_nearfield_create/compute/apply" if cfg == 3 else "", nmv)}
+                    "gk_plan_assemble (device-resident A)%s -> %s; wall clock"
+                    % (" -> gk_nearfield_create/compute/apply" if cfg == 3 else "",
+                       "%d x pinned H2D, gk_matvec_multi, %d x D2H" % (nmv, nmv) if multi else
+                       "%d x (x pinned H2D, gk_matvec, y D2H)" % nmv)}
 
 
 def run_green(args, g, torch, dev, rank, world, dist, steps, warmup, peaks_fp64, with_cpu, with_e2e):

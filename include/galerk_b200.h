@@ -149,6 +149,14 @@ gk_status gk_bem_dense(const gk_side* test, const gk_side* trial, const gk_kerne
 gk_status gk_matvec(const gk_cplx* A, int64_t rows, int64_t cols, int64_t lda, const gk_cplx* x,
                     gk_cplx* y, gk_stream stream);
 int32_t gk_matvec_launches(int64_t rows, int64_t cols);
+/* Y = A X for nrhs right-hand sides in one pass over A (X, Y column-major with
+   leading dimensions ldx, ldy >= rows/cols; device).  Replaces nrhs
+   MatrixXcd * VectorXcd products with independent vectors (the matvec sites
+   test_assembly.cpp:233,277 repeated; Eigen's MatrixXcd * MatrixXcd).  Column r
+   of Y is computed in a fixed order that does not depend on the other columns. */
+gk_status gk_matvec_multi(const gk_cplx* A, int64_t rows, int64_t cols, int64_t lda, const gk_cplx* X,
+                          int64_t ldx, gk_cplx* Y, int64_t ldy, int32_t nrhs, gk_stream stream);
+int32_t gk_matvec_multi_launches(int64_t rows, int64_t cols, int32_t nrhs);
 
 /* ---- matrix-free Green matvec -------------------------------------------- */
 typedef struct gk_green_plan gk_green_plan;

@@ -59,6 +59,8 @@ NEAR_REF = _native.NEAR_REF
 NEAR_2HBAR = _native.NEAR_2HBAR
 matvec = _native.matvec
 matvec_launches = _native.matvec_launches
+matvec_multi = _native.matvec_multi
+matvec_multi_launches = _native.matvec_multi_launches
 evaluate_blocks = _native.evaluate_blocks
 lu_factor = _native.lu_factor
 lu_solve = _native.lu_solve

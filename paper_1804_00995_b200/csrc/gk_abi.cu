@@ -977,6 +977,23 @@ gk_status gk_matvec(const gk_cplx* A, int64_t rows, int64_t cols, int64_t lda, c
 
 int32_t gk_matvec_launches(int64_t rows, int64_t cols) { return matvec_launch_count(rows, cols); }
 
+gk_status gk_matvec_multi(const gk_cplx* A, int64_t rows, int64_t cols, int64_t lda, const gk_cplx* X,
+                          int64_t ldx, gk_cplx* Y, int64_t ldy, int32_t nrhs, gk_stream stream) {
+  return guard([&] {
+    if (rows < 0 || cols < 0 || nrhs < 0) throw std::invalid_argument("gk_matvec_multi: negative size");
+    if (rows > 0 && cols > 0 && nrhs > 0 && (!A || !X)) throw std::invalid_argument("gk_matvec_multi: null input");
+    if (rows > 0 && nrhs > 0 && !Y) throw std::invalid_argument("gk_matvec_multi: null output");
+    if (lda < rows) throw std::invalid_argument("gk_matvec_multi: lda < rows");
+    if (nrhs > 1 && (ldx < cols || ldy < rows)) throw std::invalid_argument("gk_matvec_multi: ldx < cols or ldy < rows");
+    require_device();
+    launch_matvec_multi(A, rows, cols, lda, X, ldx, Y, ldy, nrhs, stream);
+  });
+}
+
+int32_t gk_matvec_multi_launches(int64_t rows, int64_t cols, int32_t nrhs) {
+  return matvec_multi_launch_count(rows, cols, nrhs);
+}
+
 gk_status gk_green_plan_create(int64_t nt, const double* tx, const double* ty, const double* tz, int64_t ns,
                                const double* sx, const double* sy, const double* sz, const gk_kernel* kernel,
                                gk_green_plan** out) {

@@ -343,6 +343,9 @@ void launch_fetch_tables(void* dst, const void* src_mapped, size_t bytes, void* 
 void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* x, void* y,
                    void* stream);
 int matvec_launch_count(int64_t rows, int64_t cols);
+void launch_matvec_multi(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* X, int64_t ldx, void* Y,
+                         int64_t ldy, int32_t nrhs, void* stream);
+int matvec_multi_launch_count(int64_t rows, int64_t cols, int32_t nrhs);
 
 // ---- green matvec ------------------------------------------------------------------------
 struct GreenArgs {

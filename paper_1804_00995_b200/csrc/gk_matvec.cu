@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <mutex>
+#include <utility>
 
 #include "gk_internal.hpp"
 
@@ -96,6 +98,99 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
   splits = (cols + cps - 1) / cps;
 }
 
+// ---- several right-hand sides in one pass over A: Y = A X -------------------
+// (Eigen::MatrixXcd * MatrixXcd with a few columns; the stored-matrix step of
+// BASELINE cfg 4 multiplies A by 10 independent vectors.)  Per 16-byte element
+// of A a thread now issues 4 R DFMAs, so for R >= ~8 the FP64 pipe, not HBM,
+// bounds the pass: each thread owns one row and R complex accumulators (one
+// chain per component; the R independent chains are the ILP), x values are
+// warp-uniform broadcast loads.  Same split-K + fixed-order reduce as above:
+// deterministic, and each column of Y is computed in the same order whatever
+// the other columns are.
+template <int R>
+__global__ void __launch_bounds__(kMvThreads, 2)
+    k_matvec_multi_partial(const double2* __restrict__ A, long long rows, long long cols, long long lda,
+                           const double2* __restrict__ X, long long ldx, double2* __restrict__ P, long long cps,
+                           int splits) {
+  const long long i = (long long)blockIdx.x * kMvThreads + threadIdx.x;
+  const long long c0 = (long long)blockIdx.y * cps;
+  const long long c1 = min(cols, c0 + cps);
+  if (i >= rows) return;
+  const double2* a = A + i + c0 * lda;
+  double re[R], im[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) re[r] = im[r] = 0.0;
+  auto mac = [&](const double2 v, long long j) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 xj = __ldg(X + r * ldx + j);
+      re[r] = fma(v.x, xj.x, re[r]);
+      re[r] = fma(-v.y, xj.y, re[r]);
+      im[r] = fma(v.x, xj.y, im[r]);
+      im[r] = fma(v.y, xj.x, im[r]);
+    }
+  };
+  // loads in flight per thread: more for few right-hand sides (HBM-bound)
+  constexpr int kMmUnroll = R <= 4 ? 8 : 4;
+  long long j = c0;
+  for (; j + kMmUnroll <= c1; j += kMmUnroll) {
+    double2 v[kMmUnroll];
+#pragma unroll
+    for (int u = 0; u < kMmUnroll; ++u) v[u] = ld_stream(a + (long long)u * lda);
+#pragma unroll
+    for (int u = 0; u < kMmUnroll; ++u) mac(v[u], j + u);
+    a += kMmUnroll * lda;
+  }
+  for (; j < c1; ++j, a += lda) mac(ld_stream(a), j);
+#pragma unroll
+  for (int r = 0; r < R; ++r) P[((long long)r * splits + blockIdx.y) * rows + i] = make_double2(re[r], im[r]);
+}
+
+__global__ void k_matvec_multi_reduce(const double2* __restrict__ P, long long rows, int splits, int nr,
+                                      double2* __restrict__ Y, long long ldy) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * nr) return;
+  const long long r = e / rows, i = e - r * rows;
+  const double2* p = P + r * splits * rows + i;
+  double re = 0.0, im = 0.0;
+  for (int s = 0; s < splits; ++s) {
+    const double2 v = p[(long long)s * rows];
+    re += v.x;
+    im += v.y;
+  }
+  Y[r * ldy + i] = make_double2(re, im);
+}
+
+constexpr int kMmMaxR = 10;  // right-hand sides per pass (larger counts: several passes)
+
+template <int R>
+void launch_multi_r(const double2* A, int64_t rows, int64_t cols, int64_t lda, const double2* X, int64_t ldx,
+                    double2* P, int64_t cps, int64_t splits, cudaStream_t s) {
+  const dim3 grid((unsigned)((rows + kMvThreads - 1) / kMvThreads), (unsigned)splits);
+  k_matvec_multi_partial<R><<<grid, kMvThreads, 0, s>>>(A, rows, cols, lda, X, ldx, P, cps, (int)splits);
+}
+
+using MultiFn = void (*)(const double2*, int64_t, int64_t, int64_t, const double2*, int64_t, double2*, int64_t,
+                         int64_t, cudaStream_t);
+template <int... Rs>
+constexpr auto multi_table(std::integer_sequence<int, Rs...>) {
+  return std::array<MultiFn, sizeof...(Rs)>{&launch_multi_r<Rs + 1>...};
+}
+
+void plan_multi(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // FP64-bound: two resident CTAs per SM, about eight waves (short tail)
+  const int64_t row_blocks = (rows + kMvThreads - 1) / kMvThreads;
+  const int64_t target = (int64_t)sms * 2 * 8;
+  splits = std::max<int64_t>(1, std::min<int64_t>((target + row_blocks / 2) / row_blocks,
+                                                  std::max<int64_t>(1, cols / 64)));
+  splits = std::min<int64_t>(splits, 65535);
+  cps = (cols + splits - 1) / splits;
+  splits = (cols + cps - 1) / cps;
+}
+
 // The partial sums live in stream-ordered memory (cudaMallocAsync from the
 // device's default pool, see ensure_pool), so matvecs on different streams
 // never share a scratch buffer.
@@ -130,6 +225,48 @@ void launch_matvec(const void* A, int64_t rows, int64_t cols, int64_t lda, const
   cudaFreeAsync(P, s);
   cuda_check(e1, "k_matvec_partial launch");
   cuda_check(e2, "k_matvec_reduce launch");
+}
+
+int matvec_multi_launch_count(int64_t rows, int64_t cols, int32_t nrhs) {
+  if (rows <= 0 || nrhs <= 0) return 0;
+  if (cols <= 0) return nrhs;
+  return 2 * (int)((nrhs + kMmMaxR - 1) / kMmMaxR);
+}
+
+void launch_matvec_multi(const void* A, int64_t rows, int64_t cols, int64_t lda, const void* X, int64_t ldx, void* Y,
+                         int64_t ldy, int32_t nrhs, void* stream) {
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rows <= 0 || nrhs <= 0) return;
+  if (cols <= 0) {
+    for (int32_t r = 0; r < nrhs; ++r)
+      cuda_check(cudaMemsetAsync(static_cast<double2*>(Y) + r * ldy, 0, sizeof(double2) * rows, s),
+                 "cudaMemsetAsync");
+    return;
+  }
+  int64_t splits, cps;
+  plan_multi(rows, cols, splits, cps);
+  const int32_t rpass = std::min<int32_t>(nrhs, kMmMaxR);
+  const size_t need = sizeof(double2) * (size_t)rows * (size_t)splits * (size_t)rpass;
+  ensure_pool();
+  void* P = nullptr;
+  if (cudaMallocAsync(&P, need, s) != cudaSuccess) {
+    cudaGetLastError();
+    throw NoMemError("gk_matvec_multi: scratch allocation failed");
+  }
+  static constexpr auto table = multi_table(std::make_integer_sequence<int, kMmMaxR>{});
+  cudaError_t e = cudaSuccess;
+  for (int32_t r0 = 0; r0 < nrhs && e == cudaSuccess; r0 += kMmMaxR) {
+    const int32_t nr = std::min<int32_t>(kMmMaxR, nrhs - r0);
+    table[nr - 1](static_cast<const double2*>(A), rows, cols, lda, static_cast<const double2*>(X) + r0 * ldx, ldx,
+                  static_cast<double2*>(P), cps, splits, s);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) break;
+    k_matvec_multi_reduce<<<(unsigned)((rows * nr + 255) / 256), 256, 0, s>>>(
+        static_cast<const double2*>(P), rows, (int)splits, nr, static_cast<double2*>(Y) + r0 * ldy, ldy);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(P, s);
+  cuda_check(e, "k_matvec_multi launch");
 }
 
 }  // namespace gk

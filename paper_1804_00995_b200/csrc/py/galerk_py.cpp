@@ -322,6 +322,17 @@ PYBIND11_MODULE(_galerk, m) {
       py::arg("stream") = 0);
   m.def("matvec_launches", &gk_matvec_launches);
   m.def(
+      "matvec_multi",
+      [](uintptr_t A, int64_t rows, int64_t cols, int64_t lda, uintptr_t X, int64_t ldx, uintptr_t Y, int64_t ldy,
+         int32_t nrhs, uintptr_t stream) {
+        throw_status(gk_matvec_multi(reinterpret_cast<const gk_cplx*>(A), rows, cols, lda,
+                                     reinterpret_cast<const gk_cplx*>(X), ldx, reinterpret_cast<gk_cplx*>(Y), ldy,
+                                     nrhs, as_stream(stream)));
+      },
+      py::arg("A"), py::arg("rows"), py::arg("cols"), py::arg("lda"), py::arg("X"), py::arg("ldx"), py::arg("Y"),
+      py::arg("ldy"), py::arg("nrhs"), py::arg("stream") = 0);
+  m.def("matvec_multi_launches", &gk_matvec_multi_launches);
+  m.def(
       "evaluate_blocks",
       [](F64 X, F64 Y, const Kernel& K, double eps, bool mask) {
         auto x = X.unchecked<2>();

@@ -236,3 +236,44 @@ def test_matvec_random_shapes(galerk):
         torch.cuda.synchronize()
         ref = A[:, :rows].T @ x
         assert rel_fro(yd.cpu().numpy(), ref) <= 1e-13
+
+
+def test_matvec_multi_matches_single_matvecs(galerk):
+    """gk_matvec_multi (one pass over A for several right-hand sides) against
+    numpy and against one gk_matvec per vector; more than ten right-hand sides
+    run in several passes; padded leading dimensions; empty shapes."""
+    torch = _torch()
+    rng = np.random.default_rng(11)
+    for rows, cols, nrhs, pad in ((1, 1, 1, 0), (7, 300, 3, 2), (1000, 17, 10, 0), (4099, 2500, 13, 1),
+                                  (3000, 4000, 10, 5)):
+        lda, ldx, ldy = rows + pad, cols + pad, rows + 2 * pad
+        A = rng.standard_normal((cols, lda)) + 1j * rng.standard_normal((cols, lda))
+        X = rng.standard_normal((nrhs, ldx)) + 1j * rng.standard_normal((nrhs, ldx))
+        Ad = torch.tensor(A.ravel(), device="cuda")
+        Xd = torch.tensor(X.ravel(), device="cuda")
+        Yd = torch.full((nrhs * ldy,), 7.0 + 0j, dtype=torch.complex128, device="cuda")
+        galerk.matvec_multi(Ad.data_ptr(), rows, cols, lda, Xd.data_ptr(), ldx, Yd.data_ptr(), ldy, nrhs, 0)
+        ys = torch.empty(rows, dtype=torch.complex128, device="cuda")
+        Y = Yd.cpu().numpy().reshape(nrhs, ldy)
+        for r in range(nrhs):
+            ref = A[:, :rows].T @ X[r, :cols]
+            assert rel_fro(Y[r, :rows], ref) <= 1e-13, (rows, cols, nrhs, r)
+            galerk.matvec(Ad.data_ptr(), rows, cols, lda, Xd[r * ldx:].data_ptr(), ys.data_ptr(), 0)
+            assert rel_fro(Y[r, :rows], ys.cpu().numpy()) <= 1e-14
+            assert np.all(Y[r, rows:] == 7.0)  # padding untouched
+    # columns do not influence each other: the same vector alone gives the same bits
+    rows, cols = 2000, 3000
+    A = rng.standard_normal((cols, rows)) + 1j * rng.standard_normal((cols, rows))
+    X = rng.standard_normal((10, cols)) + 1j * rng.standard_normal((10, cols))
+    Ad, Xd = torch.tensor(A.ravel(), device="cuda"), torch.tensor(X.ravel(), device="cuda")
+    Y10 = torch.empty(10 * rows, dtype=torch.complex128, device="cuda")
+    galerk.matvec_multi(Ad.data_ptr(), rows, cols, rows, Xd.data_ptr(), cols, Y10.data_ptr(), rows, 10, 0)
+    Y3 = torch.empty(3 * rows, dtype=torch.complex128, device="cuda")
+    galerk.matvec_multi(Ad.data_ptr(), rows, cols, rows, Xd[4 * cols:].data_ptr(), cols, Y3.data_ptr(), rows, 3, 0)
+    assert torch.equal(Y10[4 * rows:7 * rows], Y3)
+    # empty shapes: cols = 0 zero-fills, rows = 0 / nrhs = 0 do nothing
+    Yz = torch.full((2 * 5,), 3.0 + 0j, dtype=torch.complex128, device="cuda")
+    galerk.matvec_multi(Ad.data_ptr(), 5, 0, 5, Xd.data_ptr(), 1, Yz.data_ptr(), 5, 2, 0)
+    assert torch.count_nonzero(Yz).item() == 0
+    galerk.matvec_multi(0, 0, 5, 1, Xd.data_ptr(), 5, 0, 1, 3, 0)
+    torch.cuda.synchronize()

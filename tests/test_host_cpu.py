@@ -99,6 +99,10 @@ def test_c_abi_argument_errors_without_device():
     assert lib.gk_plan_create(None, None, None, None, ctypes.byref(out)) == 1
     assert b"null" in lib.gk_last_error()
     assert lib.gk_matvec(None, -1, 0, 0, None, None, None) == 1
+    i64, vp = ctypes.c_int64, ctypes.c_void_p
+    lib.gk_matvec_multi.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, ctypes.c_int32, vp]
+    assert lib.gk_matvec_multi(None, 4, 4, 4, None, 4, None, 4, -1, None) == 1
+    assert b"negative" in lib.gk_last_error()
 
 
 def test_no_cpu_fallback(galerk):
