@@ -759,6 +759,131 @@ def main():
         dist.destroy_process_group()
 
 
+def load_ref_module():
+    """The reference's OWN sources (proj/src/{mesh,quadrature,kernels,femspace,
+    assembly}.cpp) compiled against the Eigen-API shim into oracle/_ref/ by
+    oracle/Makefile `ref` (test infrastructure; built in the build container,
+    the .so travels to the GPU box).  None if it was not built."""
+    import glob
+    import importlib
+
+    d = os.path.join(ROOT, "oracle", "_ref")
+    if not glob.glob(os.path.join(d, "_ref*.so")):
+        return None
+    if d not in sys.path:
+        sys.path.insert(0, d)
+    return importlib.import_module("_ref")
+
+
+def mem_available_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
+
+
+def reference_arm_compiled(args, R, cfg):
+    """The reference's own bem_product (assembly.cpp:192-222, through bem_dense
+    :313-320, single-threaded as written) on the box's host cores: each step,
+    every worker thread runs the reference on its own contiguous slice of test
+    triangles (the complete trial side), all threads at once; the step time is
+    the wall time of that parallel sample extrapolated linearly in test
+    quadrature points to the whole matrix, plus the step's stored matvecs on
+    the rows the sample produced (numpy, all vectors in one product, scaled by
+    rows).  Mesh, statistics and k come from the reference's own build_sphere /
+    edge_stats (bit-identical to the product's, tests/test_ref_pins.py)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    s = SPECS[cfg]
+    v, e = R.build_sphere(s["n"], 1.0)
+    v, e = np.asarray(v), np.asarray(e)
+    hbar = R.edge_stats(v, e)[2]
+    k = 2 * math.pi / (10 * hbar) if s["helm"] else 0.0
+    name = "[exp(ikr)/r]" if s["helm"] else "[1/r]"
+    fam = 1 if s["fam"] == "P1" else 0
+    ne, nv, g = len(e), len(v), s["gauss"]
+    N = nv if fam == 1 else ne
+    M = ne * g
+    R.rule(g)  # the reference's rule cache (a std::map) is filled before the threads start
+    threads = os.cpu_count() or 1
+    # per-thread slice: about 96 test triangles (288 points, well under the
+    # reference's 1024-point chunk) — a few seconds of single-core work
+    per = max(1, min(96, ne // threads))
+    per_thread_bytes = 16.0 * (per * g * M + per * g * N + per * 3 * N) * 1.3
+    threads = max(1, min(threads, int(0.5 * mem_available_bytes() / per_thread_bytes)))
+    nslices = max(1, ne // per)
+    xs = np.stack([complex_normal_ref(s["seed"], N * s["nmv"])[i * N:(i + 1) * N] for i in range(s["nmv"])]
+                  if not s["real_x"] else [np.asarray(ref_normal(s["seed"], N), dtype=np.complex128)])
+
+    def slice_mesh(j):
+        t0 = (j * 7919) % nslices * per  # slices spread over the mesh, cycled
+        sub = e[t0:t0 + per]
+        if fam == 0:
+            return v, sub, None
+        used, inv = np.unique(sub.ravel(), return_inverse=True)  # P1: the slice's own vertices
+        return v[used], inv.reshape(sub.shape).astype(np.int32), used
+
+    def work(j):
+        vx, ex, used = slice_mesh(j)
+        t = time.perf_counter()
+        A = R.bem_dense(vx, ex, g, fam, v, e, g, fam, name, k, 1e15)
+        return A, time.perf_counter() - t
+
+    pool = ThreadPoolExecutor(max_workers=threads)
+    step_id = [0]
+
+    def one_step():
+        ids = [step_id[0] * threads + i for i in range(threads)]
+        step_id[0] += 1
+        t0 = time.perf_counter()
+        res = list(pool.map(work, ids))
+        wall = time.perf_counter() - t0
+        rows = np.concatenate([r[0] for r in res], axis=0)  # sample rows x N
+        t1 = time.perf_counter()
+        Y = rows @ xs.T  # the step's matvecs on the sampled rows
+        t_mv = time.perf_counter() - t1
+        assert np.isfinite(Y).all()
+        pts = threads * per * g
+        return wall * M / pts + t_mv * N / rows.shape[0], wall, t_mv, rows.shape[0]
+
+    one_step()  # warm-up (page faults, thread start)
+    for _ in range(max(0, min(args.warmup, 1) - 1)):
+        one_step()
+    ests, walls = [], []
+    for _ in range(args.steps):
+        est, wall, t_mv, nrows = one_step()
+        ests.append(est)
+        walls.append(wall)
+    pool.shutdown()
+    est = float(np.mean(ests))
+    sample = (f"the reference's own bem_dense/bem_product (proj/src, compiled unchanged against the Eigen-API shim, "
+              f"oracle/_ref) on {threads} host threads at once, each on a slice of {per} test triangles "
+              f"({per * g} x points) x all {M} trial points ({float(np.mean(walls)):.1f} s wall per step), "
+              f"+ {s['nmv']} matvecs on the sampled rows (numpy); extrapolated linearly in x points / rows "
+              f"to the full {N} x {N} step")
+    return dict(value=M * M / est, est=est, sample=sample, threads=threads, N=N, M=M, k=k, hbar=hbar, nv=nv, ne=ne)
+
+
+def complex_normal_ref(seed, n):
+    """complex_normal without the product: the oracle's SplitMix64 stream."""
+    return complex_normal_np(load_oracle(), seed, n)
+
+
+def ref_normal(seed, n):
+    o = load_oracle()
+    u = np.asarray(o.uniform01_stream(seed, 2 * ((n + 1) // 2)))
+    r = np.sqrt(-2.0 * np.log(1.0 - u[0::2]))
+    t = 2.0 * np.pi * u[1::2]
+    z = np.empty(2 * len(r))
+    z[0::2] = r * np.cos(t)
+    z[1::2] = r * np.sin(t)
+    return z[:n]
+
+
 def reference_arm(args, rank, world, dist):
     """The reference's CPU path on the host cores: the oracle (C++ restatement
     of bem_product / regularize / zgemv / the matrix-free loop; the reference
@@ -770,9 +895,29 @@ def reference_arm(args, rank, world, dist):
         if dist:
             dist.destroy_process_group()
         return
-    o = load_oracle()
     cfg = args.config
     s = SPECS[cfg]
+    R = load_ref_module() if cfg in (1, 2, 4) else None  # cfg 3's 6-point rule and cfg 5's matrix-free
+    # loop are not in the reference: those configs time the oracle restatement (kind "port")
+    if R is not None:
+        r = reference_arm_compiled(args, R, cfg)
+        cfgd = config_dict(cfg, r["nv"], r["ne"], r["N"], r["M"], r["k"], r["hbar"]) | {
+            "parallelism": f"replicas x{world}"}
+        value = r["value"]
+        out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["est"] * 1e3, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)",
+               "data": "synthetic (seeded icosphere mesh per BASELINE config, SplitMix64/Box-Muller vectors)",
+               "config": cfgd,
+               "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": r["threads"], "kind": "reference",
+                                "sample": r["sample"]},
+               "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        assert "paper_1804_00995_b200" not in sys.modules, "the reference arm must not load the product"
+        print(json.dumps(out))
+        if dist:
+            dist.destroy_process_group()
+        return
+    o = load_oracle()
     P = oracle_problem(o, cfg)
     threads = os.cpu_count() or 1
     if cfg == 5:

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <mutex>
 #include <utility>
 
@@ -101,49 +102,145 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
 // ---- several right-hand sides in one pass over A: Y = A X -------------------
 // (Eigen::MatrixXcd * MatrixXcd with a few columns; the stored-matrix step of
 // BASELINE cfg 4 multiplies A by 10 independent vectors.)  Per 16-byte element
-// of A a thread now issues 4 R DFMAs, so for R >= ~8 the FP64 pipe, not HBM,
-// bounds the pass: each thread owns one row and R complex accumulators (one
-// chain per component; the R independent chains are the ILP), x values are
-// warp-uniform broadcast loads.  Same split-K + fixed-order reduce as above:
-// deterministic, and each column of Y is computed in the same order whatever
-// the other columns are.
+// of A, R right-hand sides cost 4 R DFMAs: for R = 10 the FP64 pipe and HBM
+// bound the pass about equally, so the A stream must never wait on the FP64
+// work.  A register-prefetch version stalled on its loads (long_scoreboard 66%,
+// FP64 pipe 44%), so the stream is asynchronous: one elected thread per CTA
+// issues bulk copies (cp.async.bulk, the TMA engine; one contiguous 4 KB
+// column segment of the CTA's 256 rows per column, L2 evict-first) into a
+// ring of shared-memory stages completed on mbarriers, while all 256 threads
+// multiply the stage that has landed (thread = row; A from shared memory,
+// conflict-free; x values broadcast from the stage's copy of X).  Each
+// (row, right-hand side) sums its columns in order in one chain; the same
+// split-K + fixed-order reduce as above: deterministic, and column r of Y does
+// not depend on the other columns.
+constexpr int kBkStages = 3;  // stages in the ring (2 CTAs x ~99 KB per SM)
+constexpr int kMmMaxR = 10;   // right-hand sides per pass (larger counts: several passes)
+// Rows per thread: 2 for many right-hand sides (each broadcast x value then
+// feeds two rows: 9 instead of 14 shared-memory wavefronts per 32 rows and
+// column at R = 10), 1 otherwise.  A stage holds 256 RPT rows x 8 / RPT
+// columns (32 KB).
+template <int R>
+constexpr int mm_rpt() {
+  return R >= 6 ? 2 : 1;
+}
+template <int RPT>
+struct MmSmem {
+  static constexpr int kRows = kMvThreads * RPT, kCols = 8 / RPT;
+  double2 a[kBkStages][kCols][kRows];
+  double2 x[kBkStages][kMmMaxR][kCols];
+  unsigned long long full[kBkStages];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                         unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 template <int R>
 __global__ void __launch_bounds__(kMvThreads, 2)
     k_matvec_multi_partial(const double2* __restrict__ A, long long rows, long long cols, long long lda,
                            const double2* __restrict__ X, long long ldx, double2* __restrict__ P, long long cps,
                            int splits) {
-  const long long i = (long long)blockIdx.x * kMvThreads + threadIdx.x;
+  constexpr int RPT = mm_rpt<R>();
+  using Smem = MmSmem<RPT>;
+  constexpr int kRows = Smem::kRows, kCols = Smem::kCols;
+  extern __shared__ __align__(128) unsigned char mm_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(mm_raw);
+  const int t = threadIdx.x;
+  const long long ib = (long long)blockIdx.x * kRows;
+  const int nr = (int)min((long long)kRows, rows - ib);
   const long long c0 = (long long)blockIdx.y * cps;
   const long long c1 = min(cols, c0 + cps);
-  if (i >= rows) return;
-  const double2* a = A + i + c0 * lda;
-  double re[R], im[R];
+  const long long ngroups = (c1 - c0 + kCols - 1) / kCols;
+  unsigned long long policy = 0;
+  if (t == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (int q = 0; q < kBkStages; ++q) mbar_init(&S.full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](long long g) {  // thread 0 only
+    const int buf = (int)(g % kBkStages);
+    const long long j = c0 + g * kCols;
+    const int nc = (int)min((long long)kCols, c1 - j);
+    mbar_expect_tx(&S.full[buf], (unsigned)(16 * nc * (nr + R)));
+    for (int c = 0; c < nc; ++c) bulk_g2s(&S.a[buf][c][0], A + ib + (j + c) * lda, 16u * nr, &S.full[buf], policy);
+    for (int r = 0; r < R; ++r) bulk_g2s(&S.x[buf][r][0], X + r * ldx + j, 16u * nc, &S.full[buf], policy);
+  };
+  if (t == 0)
+    for (long long g = 0; g < min((long long)kBkStages, ngroups); ++g) issue(g);
+  // rows t and t + 256 (RPT = 2): both conflict-free in the stage
+  double re[RPT][R], im[RPT][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) re[r] = im[r] = 0.0;
-  auto mac = [&](const double2 v, long long j) {
+  for (int k = 0; k < RPT; ++k)
+#pragma unroll
+    for (int r = 0; r < R; ++r) re[k][r] = im[k][r] = 0.0;
+  bool act[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) act[k] = t + k * kMvThreads < nr;
+  auto column = [&](int buf, int c) {
+    double2 v[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) v[k] = S.a[buf][c][t + k * kMvThreads];  // rows past nr: stale, never stored
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double2 xj = __ldg(X + r * ldx + j);
-      re[r] = fma(v.x, xj.x, re[r]);
-      re[r] = fma(-v.y, xj.y, re[r]);
-      im[r] = fma(v.x, xj.y, im[r]);
-      im[r] = fma(v.y, xj.x, im[r]);
+      const double2 xj = S.x[buf][r][c];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        re[k][r] = fma(v[k].x, xj.x, re[k][r]);
+        re[k][r] = fma(-v[k].y, xj.y, re[k][r]);
+        im[k][r] = fma(v[k].x, xj.y, im[k][r]);
+        im[k][r] = fma(v[k].y, xj.x, im[k][r]);
+      }
     }
   };
-  // loads in flight per thread: more for few right-hand sides (HBM-bound)
-  constexpr int kMmUnroll = R <= 4 ? 8 : 4;
-  long long j = c0;
-  for (; j + kMmUnroll <= c1; j += kMmUnroll) {
-    double2 v[kMmUnroll];
+  for (long long g = 0; g < ngroups; ++g) {
+    const int buf = (int)(g % kBkStages);
+    const int nc = (int)min((long long)kCols, c1 - (c0 + g * kCols));
+    mbar_wait(&S.full[buf], (unsigned)((g / kBkStages) & 1));
+    if (act[0]) {
+      if (nc == kCols) {
 #pragma unroll
-    for (int u = 0; u < kMmUnroll; ++u) v[u] = ld_stream(a + (long long)u * lda);
-#pragma unroll
-    for (int u = 0; u < kMmUnroll; ++u) mac(v[u], j + u);
-    a += kMmUnroll * lda;
+        for (int c = 0; c < kCols; ++c) column(buf, c);
+      } else {
+        for (int c = 0; c < nc; ++c) column(buf, c);
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (t == 0 && g + kBkStages < ngroups) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+      issue(g + kBkStages);
+    }
   }
-  for (; j < c1; ++j, a += lda) mac(ld_stream(a), j);
 #pragma unroll
-  for (int r = 0; r < R; ++r) P[((long long)r * splits + blockIdx.y) * rows + i] = make_double2(re[r], im[r]);
+  for (int k = 0; k < RPT; ++k)
+    if (act[k])
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        P[((long long)r * splits + blockIdx.y) * rows + ib + t + k * kMvThreads] = make_double2(re[k][r], im[k][r]);
 }
 
 __global__ void k_matvec_multi_reduce(const double2* __restrict__ P, long long rows, int splits, int nr,
@@ -161,13 +258,20 @@ __global__ void k_matvec_multi_reduce(const double2* __restrict__ P, long long r
   Y[r * ldy + i] = make_double2(re, im);
 }
 
-constexpr int kMmMaxR = 10;  // right-hand sides per pass (larger counts: several passes)
-
 template <int R>
 void launch_multi_r(const double2* A, int64_t rows, int64_t cols, int64_t lda, const double2* X, int64_t ldx,
                     double2* P, int64_t cps, int64_t splits, cudaStream_t s) {
-  const dim3 grid((unsigned)((rows + kMvThreads - 1) / kMvThreads), (unsigned)splits);
-  k_matvec_multi_partial<R><<<grid, kMvThreads, 0, s>>>(A, rows, cols, lda, X, ldx, P, cps, (int)splits);
+  constexpr int kRows = MmSmem<mm_rpt<R>()>::kRows;
+  const dim3 grid((unsigned)((rows + kRows - 1) / kRows), (unsigned)splits);
+  const size_t smem = sizeof(MmSmem<mm_rpt<R>()>);
+  static std::atomic<uint64_t> configured{0};  // the attribute is per device context
+  const int dev = current_device();
+  if (!((configured.load() >> dev) & 1u)) {
+    cuda_check(cudaFuncSetAttribute(k_matvec_multi_partial<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute");
+    configured |= 1ull << dev;
+  }
+  k_matvec_multi_partial<R><<<grid, kMvThreads, smem, s>>>(A, rows, cols, lda, X, ldx, P, cps, (int)splits);
 }
 
 using MultiFn = void (*)(const double2*, int64_t, int64_t, int64_t, const double2*, int64_t, double2*, int64_t,
