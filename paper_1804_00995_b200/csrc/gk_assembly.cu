@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <type_traits>
 
 #include "gk_internal.hpp"
@@ -36,6 +37,9 @@ namespace gk {
 
 namespace {
 
+#ifndef GK_GATHER_G
+#define GK_GATHER_G 4  // tile columns per gather work unit of symmetric tiles (even)
+#endif
 #ifndef GK_ASM_UNROLL
 #define GK_ASM_UNROLL 6  // measured (cfg 2 / cfg 3 ms): 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56
 #endif
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       ar = fresh ? w0 : ar + w0;
       ai = 0.0;
     }
-    if (SLOTS > 0 && p.off1 >= 0) {
+    if (SLOTS > 0 && p.off1 >= 0 && !(a.dbg & 8)) {  // (dbg 8: timing experiment, no second slot)
       const double w1 = SLOTS >= 2 ? w0 : p.c1 * rinv;
       double2* h = reinterpret_cast<double2*>(Hb + p.off1);
       double2 v = *h;
@@ -228,7 +232,8 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       fold(p, cs[0], sn[0], rinv[0]);
     }
   };
-  if (masked)  // uniform per CTA
+  if (a.dbg & 4) {  // timing experiment: no pair loop
+  } else if (masked)  // uniform per CTA
     pair_loop(std::true_type{});
   else
     pair_loop(std::false_type{});
@@ -314,97 +319,112 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
     }
     return;
   }
-  // Symmetric tiles: thread = (row ii, strip of columns).  The row's supports
-  // are loaded once into registers and feed every column of the strip; each
-  // entry is written to (i, j) — lanes along rows: one column segment per
-  // warp store (natural order: contiguous; RCB units of 4: 64-byte runs) —
-  // and to the mirror (j, i) — each lane down its own column, two entries per
-  // 32-byte store (STG.256) where two consecutive tile columns are adjacent
-  // rows of A and aligned.  Only entries with row <= column are formed.
-  constexpr int kSupCache = 6;  // P0 rules up to 6 points: all supports in registers
+  // Symmetric tiles: work unit = (row ii, strip of kG consecutive tile
+  // columns), units spread evenly over all threads (an x block of 128
+  // locations holds ~73 P0 rows: one row per thread left 55 threads idle and
+  // the others walking all 22 columns).  A unit loads its row's supports once,
+  // then issues all 3 kG H loads before any multiply-add (independent chains:
+  // the gather is latency-bound), and writes each entry to (i, j) — lanes
+  // along rows: one column segment per warp store (natural order: contiguous;
+  // RCB units of 4: 64-byte runs) — and to the mirror (j, i) — each lane down
+  // its own column, two entries per 32-byte store (STG.256) where two
+  // consecutive tile columns are adjacent, aligned rows of A (strips start on
+  // even absolute columns).  Only entries with row <= column are written, the
+  // diagonal once.
+  constexpr int kSupCache = 3;  // supports in registers (P0 3-point rows have exactly three)
+  constexpr int kG = GK_GATHER_G;
   if (a.dbg & 2) return;
-  const int nstrip = max(1, kAsmThreads / nIs);
-  const int ii = t % nIs, strip = t / nIs;
-  if (t >= nstrip * nIs || ii >= nI) return;
-  const int pi = i0 + ii;
-  const int jlo = max(strip * nJ / nstrip, pi - j0), jhi = (strip + 1) * nJ / nstrip;
-  if (jlo >= jhi) return;
-  const int sb = S.xs_start[ii] - xs0, ns = S.xs_start[ii + 1] - xs0 - sb;
-  // supports padded with coefficient 0 on a real location (finite H): the
-  // first three terms are unconditional (P0 3-point rows have exactly three),
-  // the next three run only for longer rows — no per-term branches
-  int su[kSupCache];
-  double sc[kSupCache];
-  const int u0 = ns > 0 ? S.xs_u[sb] : 0;  // rows without supports (constrained or oversized dofs): entries 0
+  const int par = j0 & 1;  // strip s covers tile columns [s kG - par, (s + 1) kG - par)
+  const int nstrips = (nJ + par + kG - 1) / kG;
+  const int units = nI * nstrips;
+  const int du_i = kAsmThreads % nIs, du_s = kAsmThreads / nIs;
+  const bool nat = a.natural != 0;
+  int ii = t % nIs, strip = t / nIs;
+  for (int u = t; u < units; u += kAsmThreads, ii += du_i, strip += du_s) {
+    if (ii >= nI) ii -= nI, ++strip;
+    const int pi = i0 + ii;
+    const int jb = strip * kG - par;  // tile column of slot q is jb + q
+    if (j0 + min(jb + kG, nJ) - 1 < pi) continue;  // the whole strip lies below the diagonal
+    const int sb = S.xs_start[ii] - xs0, ns = S.xs_start[ii + 1] - xs0 - sb;
+    // supports padded with coefficient 0 on a real location (finite H); rows
+    // without supports (constrained or oversized dofs) give entries 0
+    int su[kSupCache];
+    double sc[kSupCache];
+    const int u0 = ns > 0 ? S.xs_u[sb] : 0;
 #pragma unroll
-  for (int k = 0; k < kSupCache; ++k) {
-    su[k] = k < ns ? S.xs_u[sb + k] : u0;
-    sc[k] = k < ns ? S.xs_c[sb + k] : 0.0;
-  }
-  auto entry = [&](int j) {
-    const double2* Hr = S.H + j * kHS;
-    double re = 0.0, im = 0.0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double2 h = Hr[su[k]];
-      re = fma(sc[k], h.x, re);
-      im = fma(sc[k], h.y, im);
+    for (int k = 0; k < kSupCache; ++k) {
+      su[k] = k < ns ? S.xs_u[sb + k] : u0;
+      sc[k] = k < ns ? S.xs_c[sb + k] : 0.0;
     }
-    if (ns > 3) {
+    int jq[kG];
 #pragma unroll
-      for (int k = 3; k < kSupCache; ++k) {
-        const double2 h = Hr[su[k]];
-        re = fma(sc[k], h.x, re);
-        im = fma(sc[k], h.y, im);
+    for (int q = 0; q < kG; ++q) jq[q] = min(max(jb + q, 0), kJCap - 1);  // in-bounds H row (stale rows unused)
+    double2 h[kG][kSupCache];
+#pragma unroll
+    for (int q = 0; q < kG; ++q)
+#pragma unroll
+      for (int k = 0; k < kSupCache; ++k) h[q][k] = S.H[jq[q] * kHS + su[k]];
+    double re[kG], im[kG];
+#pragma unroll
+    for (int q = 0; q < kG; ++q) {
+      re[q] = sc[0] * h[q][0].x;
+      im[q] = sc[0] * h[q][0].y;
+#pragma unroll
+      for (int k = 1; k < kSupCache; ++k) {
+        re[q] = fma(sc[k], h[q][k].x, re[q]);
+        im[q] = fma(sc[k], h[q][k].y, im[q]);
       }
     }
-    for (int k = kSupCache; k < ns; ++k) {
-      const double c = S.xs_c[sb + k];
-      const double2 h = Hr[S.xs_u[sb + k]];
-      re = fma(c, h.x, re);
-      im = fma(c, h.y, im);
-    }
-    if (SLOTS == 3) {
-      const double f = S.ys[j];
-      re *= f;
-      im *= f;
-    }
-    return make_double2(re, im);
-  };
-  const bool nat = a.natural != 0;
-  auto ocol = [&](int j) -> long long { return nat ? (long long)(j0 + j) : (long long)S.ocol[j]; };
-  const long long oi = nat ? (long long)pi : (long long)S.orow[ii];
-  double2* const Arow = A + oi;        // direct (oi, oj) = Arow[oj * lda]
-  double2* const Acol = A + oi * lda;  // mirror (oj, oi) = Acol[oj]
-  int j = jlo;
-  if (j0 + j == pi) {  // diagonal entry: written once
-    Arow[ocol(j) * lda] = entry(j);
-    ++j;
-  }
-  // (A branch-free natural-order variant of this loop — six hoisted LDS.128
-  // per column pair, no per-pair checks — measured slower overall, 51.3 vs
-  // 47.7 ms on cfg 4: its faster bursts of loads and stores stretch the other
-  // CTAs' pair loops, which share the MIO/L1 pipe.)
-#pragma unroll 2
-  while (j < jhi) {
-    const long long oj = ocol(j);
-    double2* const m = Acol + oj;
-    const bool two = j + 1 < jhi && (reinterpret_cast<uintptr_t>(m) & 31) == 0 && ocol(j + 1) == oj + 1;
-    const double2 v0 = entry(j);
-    const double2 v1 = two ? entry(j + 1) : v0;
+    if (ns > kSupCache)  // longer rows (6-point P0, P1 rows): the remaining supports in order
+      for (int k = kSupCache; k < ns; ++k) {
+        const double c = S.xs_c[sb + k];
+        const int uk = S.xs_u[sb + k];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+          const double2 hv = S.H[jq[q] * kHS + uk];
+          re[q] = fma(c, hv.x, re[q]);
+          im[q] = fma(c, hv.y, im[q]);
+        }
+      }
+    if (SLOTS == 3)
+#pragma unroll
+      for (int q = 0; q < kG; ++q) {
+        const double f = S.ys[jq[q]];
+        re[q] *= f;
+        im[q] *= f;
+      }
     if (a.dbg & 1) {  // timing experiment: no stores (keep the values live)
-      if (v0.x == 1234.5 && v1.y == 6.5) Arow[0] = v0;
-      j += two ? 2 : 1;
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < kG; ++q) acc += re[q] + im[q];
+      if (acc == 1234.5) A[0] = make_double2(acc, acc);
       continue;
     }
-    Arow[oj * lda] = v0;
-    if (two) {
-      Arow[(oj + 1) * lda] = v1;
-      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(m), "d"(v0.x), "d"(v0.y), "d"(v1.x), "d"(v1.y));
-      j += 2;
-    } else {
-      *m = v0;
-      ++j;
+    const long long oi = nat ? (long long)pi : (long long)S.orow[ii];
+    double2* const Arow = A + oi;        // direct (oi, oj) = Arow[oj * lda]
+    double2* const Acol = A + oi * lda;  // mirror (oj, oi) = Acol[oj]
+    long long oj[kG];
+    bool ok[kG], off[kG];  // ok: entry in the tile and on/above the diagonal; off: strictly above
+#pragma unroll
+    for (int q = 0; q < kG; ++q) {
+      const int j = jb + q;
+      ok[q] = j >= 0 && j < nJ && j0 + j >= pi;
+      off[q] = ok[q] && j0 + j != pi;
+      oj[q] = nat ? (long long)(j0 + j) : (long long)S.ocol[jq[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < kG; ++q)
+      if (ok[q]) Arow[oj[q] * lda] = make_double2(re[q], im[q]);
+#pragma unroll
+    for (int q = 0; q < kG; q += 2) {
+      double2* const m = Acol + oj[q];
+      if (q + 1 < kG && off[q] && off[q + 1] && oj[q + 1] == oj[q] + 1 && (reinterpret_cast<uintptr_t>(m) & 31) == 0) {
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(m), "d"(re[q]), "d"(im[q]), "d"(re[q + 1]),
+                     "d"(im[q + 1]));
+      } else {
+        if (off[q]) *m = make_double2(re[q], im[q]);
+        if (q + 1 < kG && off[q + 1]) Acol[oj[q + 1]] = make_double2(re[q + 1], im[q + 1]);
+      }
     }
   }
 }
