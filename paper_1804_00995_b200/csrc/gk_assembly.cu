@@ -49,7 +49,7 @@ constexpr int kRecUnroll = GK_ASM_UNROLL;  // records per group = independent ev
 // edge-midpoint specialisation (SLOTS = 2), 2 otherwise.
 template <int SLOTS>
 constexpr int gather_cols() {
-  return SLOTS == 2 ? 11 : 2;
+  return SLOTS == 2 && kJCap % 11 == 0 ? 11 : 2;
 }
 static_assert(kJCap % gather_cols<2>() == 0 && kJCap % gather_cols<0>() == 0 && kJCap % gather_cols<3>() == 0,
               "gather column groups must tile the H rows");

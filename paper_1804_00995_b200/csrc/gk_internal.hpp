@@ -174,11 +174,18 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // 128-thread CTAs (22-dof y blocks) 2.57 ms although the smaller blocks
 // evaluate 7% more pairs (halo 1.71 vs 1.61).
 constexpr int kUCap = 128;   // x locations per tile, one per thread
-constexpr int kJCap = 22;    // y dofs per tile (H accumulator rows)
+#ifndef GK_JCAP
+#define GK_JCAP 22
+#endif
+constexpr int kJCap = GK_JCAP;  // y dofs per tile (H accumulator rows)
+constexpr int kJCapSmall = 16;  // alternative y-block cap the planner tries (layout_y_blocks)
 constexpr int kIMax = 128;   // x dofs per tile
 constexpr int kRCap = 112;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 320;  // x support entries per tile (staged in shared memory)
-constexpr int kAsmCtasPerSm = 4;
+#ifndef GK_ASM_CTAS
+#define GK_ASM_CTAS 4
+#endif
+constexpr int kAsmCtasPerSm = GK_ASM_CTAS;
 constexpr int kAsmThreads = kUCap;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 constexpr int kHS = kUCap;  // H row stride in 16-byte entries

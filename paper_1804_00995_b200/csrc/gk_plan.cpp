@@ -421,7 +421,8 @@ void layout_x_blocks(const Locations& X, BlockLayout& B) {
   }
 }
 
-void layout_y_blocks(const Locations& Y, BlockLayout& B) {
+namespace {
+void layout_y_blocks_cap(const Locations& Y, BlockLayout& B, int64_t cap) {
   const int64_t ncols = Y.nfree;
   B.yb.clear();
   B.yrec.clear();
@@ -448,7 +449,7 @@ void layout_y_blocks(const Locations& Y, BlockLayout& B) {
   };
   B.yb.push_back(0);
   for (int64_t q0 = 0; q0 < ncols;) {
-    int64_t q1 = std::min<int64_t>(ncols, q0 + std::min<int64_t>(kJCap, (int64_t)env_frac("GK_JCAP", kJCap)));
+    int64_t q1 = std::min<int64_t>(ncols, q0 + cap);
     int64_t nrec = count_records(q0, q1);
     while (nrec > kRCap && q1 - q0 > 1) {
       q1 = q0 + std::max<int64_t>(1, (q1 - q0) * 7 / 8);
@@ -465,6 +466,31 @@ void layout_y_blocks(const Locations& Y, BlockLayout& B) {
     B.yb.push_back((int32_t)q1);
     B.yrec.push_back((int32_t)nrec);
     q0 = q1;
+  }
+}
+
+}  // namespace
+
+// y blocks of at most kJCap dofs, or of at most kJCapSmall when that needs
+// fewer records in total (records x x locations = evaluated pairs): on a
+// subdivided mesh in natural order, 16 dofs are one 4^2 subtree (P0 L6, cfg 4:
+// y halo 1.25 instead of 1.34, 7% fewer evaluated pairs, measured 46.2 ->
+// 44.6 ms), while P1 vertex blocks (cfg 2) keep 22.
+void layout_y_blocks(const Locations& Y, BlockLayout& B) {
+  if (std::getenv("GK_JCAP")) {  // diagnostics: a fixed cap
+    layout_y_blocks_cap(Y, B, std::max<int64_t>(1, std::min<int64_t>(kJCap, (int64_t)env_frac("GK_JCAP", kJCap))));
+    return;
+  }
+  layout_y_blocks_cap(Y, B, kJCap);
+  if (kJCapSmall >= kJCap) return;
+  BlockLayout S;
+  layout_y_blocks_cap(Y, S, kJCapSmall);
+  int64_t rb = 0, rs = 0;
+  for (int32_t r : B.yrec) rb += r;
+  for (int32_t r : S.yrec) rs += r;
+  if (rs < rb) {
+    B.yb = std::move(S.yb);
+    B.yrec = std::move(S.yrec);
   }
 }
 
