@@ -88,14 +88,15 @@ void ensure_pool() {
 
 void DevArena::upload() {
   release();
-  bytes = host.size();
+  const size_t copy = host.size();
+  bytes = copy + extra;
   if (bytes) {
     ensure_pool();
     if (cudaMallocAsync(&p, bytes, nullptr) != cudaSuccess) {
       cudaGetLastError();
       p = nullptr;
       bytes = 0;
-      throw NoMemError("device allocation of " + std::to_string(host.size()) + " bytes failed");
+      throw NoMemError("device allocation of " + std::to_string(host.size() + extra) + " bytes failed");
     }
     // through a grow-only pinned staging buffer: a pageable copy of a few MB
     // runs at a few GB/s, a pinned one at PCIe speed
@@ -103,22 +104,22 @@ void DevArena::upload() {
     static void* staging = nullptr;
     static size_t staging_bytes = 0;
     std::lock_guard<std::mutex> hold(staging_mutex);
-    if (staging_bytes < bytes) {
+    if (staging_bytes < copy) {
       if (staging) cudaFreeHost(staging);
       staging = nullptr;
       staging_bytes = 0;
-      if (cudaMallocHost(&staging, bytes) != cudaSuccess) {
+      if (cudaMallocHost(&staging, copy) != cudaSuccess) {
         cudaGetLastError();
         staging = nullptr;
       } else {
-        staging_bytes = bytes;
+        staging_bytes = copy;
       }
     }
     if (staging) {
-      std::memcpy(staging, host.data(), bytes);
-      cuda_check(cudaMemcpy(p, staging, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+      std::memcpy(staging, host.data(), copy);
+      cuda_check(cudaMemcpy(p, staging, copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
     } else {
-      cuda_check(cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+      cuda_check(cudaMemcpy(p, host.data(), copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
     }
   }
   hvec<char>().swap(host);
@@ -333,17 +334,37 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->natural = X.natural;
   P->xblocks = (int64_t)T.xb_dof_start.size() - 1;
   P->yblocks = (int64_t)T.yb_dof_start.size() - 1;
-  P->ntiles = (int64_t)T.tile_i.size();
+  P->ntiles = T.n_unmasked;
   P->nmtiles = (int64_t)T.mtile_i.size();
   P->slots = slots_of(T);
   if (dry_run) return P;
   DevArena& Ar = P->arena;
-  const hvec<TileDesc> descs = make_tile_descs(T, T);
-  lap("tile descriptors");
-  Ar.host.reserve(descs.size() * sizeof(TileDesc) + (T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
+  // compact tile list for the device-side descriptor build (launch_make_tiles)
+  const int64_t nIb = P->xblocks, nJb = P->yblocks, ntiles_all = P->ntiles + P->nmtiles;
+  hvec<int64_t> tile_start(nIb + 1, 0);
+  hvec<int32_t> first_bj(nIb, 0);
+  for (int64_t bi = 0; bi < nIb; ++bi) {
+    int64_t first = 0;
+    if (P->symmetric)  // as build_tile_list: tiles whose last column >= the block's first row
+      first = std::upper_bound(T.yb_dof_start.begin() + 1, T.yb_dof_start.end(), T.xb_dof_start[bi]) -
+              (T.yb_dof_start.begin() + 1);
+    first_bj[bi] = (int32_t)first;
+    tile_start[bi + 1] = tile_start[bi] + (nJb - first);
+  }
+  if (tile_start[nIb] != ntiles_all) throw std::logic_error("bem_dense: tile list is not block-complete");
+  hvec<uint32_t> masked_bits((size_t)(ntiles_all + 31) / 32, 0u);
+  for (size_t m = 0; m < T.mtile_i.size(); ++m) {
+    const int32_t bi = T.mtile_i[m], bj = T.mtile_j[m];
+    const int64_t e = tile_start[bi] + (bj - first_bj[bi]);
+    masked_bits[(size_t)(e >> 5)] |= 1u << (e & 31);
+  }
+  lap("tile list");
+  Ar.host.reserve((T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
                   (T.xsup_start.size() + T.xsup_u.size() + X.perm.size() + Yr.perm.size()) * sizeof(int32_t) +
-                  T.yrec.size() * sizeof(YRec) + 16 * 256);
-  P->o_tiles = Ar.add(descs);
+                  T.yrec.size() * sizeof(YRec) + masked_bits.size() * 4 + (nIb + nJb) * 32 + 24 * 256);
+  const size_t o_ts = Ar.add(tile_start), o_fb = Ar.add(first_bj), o_xd = Ar.add(T.xb_dof_start),
+               o_xl = Ar.add(T.xb_loc_start), o_yd = Ar.add(T.yb_dof_start), o_yr = Ar.add(T.yb_rec_start),
+               o_yz = Ar.add(T.yb_zero), o_mb = Ar.add(masked_bits);
   P->o_xl_x = Ar.add(T.xl_x);
   P->o_xl_y = Ar.add(T.xl_y);
   P->o_xl_z = Ar.add(T.xl_z);
@@ -375,9 +396,28 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
       side(Yf, P->o_fy_start, P->o_fy_loc, P->o_fy_coef, P->o_fy_xyz);
     }
   }
+  P->o_tiles = Ar.add_device_only((size_t)ntiles_all * sizeof(TileDesc));
   lap("stage");
   Ar.upload();
   lap("upload");
+  if (ntiles_all > 0) {
+    TileBuildArgs b;
+    b.out = Ar.at<TileDesc>(P->o_tiles);
+    b.ntiles = ntiles_all;
+    b.nIb = (int32_t)nIb;
+    b.tile_start = Ar.at<int64_t>(o_ts);
+    b.first_bj = Ar.at<int32_t>(o_fb);
+    b.xb_dof_start = Ar.at<int32_t>(o_xd);
+    b.xb_loc_start = Ar.at<int32_t>(o_xl);
+    b.yb_dof_start = Ar.at<int32_t>(o_yd);
+    b.yb_rec_start = Ar.at<int32_t>(o_yr);
+    b.yb_zero = Ar.at<uint32_t>(o_yz);
+    b.xsup_start = Ar.at<int32_t>(P->o_xsup_start);
+    b.masked_bits = Ar.at<uint32_t>(o_mb);
+    launch_make_tiles(b, nullptr);
+    cuda_check(cudaStreamSynchronize(nullptr), "k_make_tiles");
+  }
+  lap("tile descriptors");
   return P;
 }
 

@@ -505,7 +505,44 @@ __global__ void __launch_bounds__(256) k_big_entries(const BigArgs b) {
   if (b.symmetric) A[j + i * b.lda] = make_double2(re, im);
 }
 
+__global__ void __launch_bounds__(256) k_make_tiles(const TileBuildArgs b) {
+  const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (e >= b.ntiles) return;
+  int lo = 0, hi = b.nIb;  // the last x block with tile_start <= e (empty blocks share starts)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (b.tile_start[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  const int bi = lo;
+  const int bj = b.first_bj[bi] + (int)(e - b.tile_start[bi]);
+  TileDesc D;
+  D.i0 = b.xb_dof_start[bi];
+  D.nI = b.xb_dof_start[bi + 1] - D.i0;
+  D.j0 = b.yb_dof_start[bj];
+  D.nJ = b.yb_dof_start[bj + 1] - D.j0;
+  D.l0 = b.xb_loc_start[bi];
+  D.nu = b.xb_loc_start[bi + 1] - D.l0;
+  D.r0 = b.yb_rec_start[bj];
+  D.nrec = b.yb_rec_start[bj + 1] - D.r0;
+  D.xs0 = b.xsup_start[D.i0];
+  D.nxs = b.xsup_start[D.i0 + D.nI] - D.xs0;
+  D.zero_rows = b.yb_zero[bj];
+  D.masked = (int32_t)((b.masked_bits[e >> 5] >> (e & 31)) & 1u);
+  const int4* src = reinterpret_cast<const int4*>(&D);
+  int4* dst = reinterpret_cast<int4*>(b.out + e);
+  dst[0] = src[0];
+  dst[1] = src[1];
+  dst[2] = src[2];
+}
+
 }  // namespace
+
+void launch_make_tiles(const TileBuildArgs& b, void* stream) {
+  if (b.ntiles <= 0) return;
+  k_make_tiles<<<(unsigned)((b.ntiles + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
+  cuda_check(cudaGetLastError(), "k_make_tiles launch");
+}
 
 void launch_big_entries(const BigArgs& b, bool helmholtz, void* stream) {
   const long long n = b.nbig_rows * b.ncols + (b.symmetric ? 0 : b.nrows * b.nbig_cols);

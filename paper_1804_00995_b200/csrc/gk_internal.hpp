@@ -125,6 +125,14 @@ struct DevArena {
   size_t add(const V& v) {
     return add(v.data(), v.size());
   }
+  // device-only bytes after the uploaded tables (filled on the device);
+  // call after the last add()
+  size_t add_device_only(size_t n) {
+    const size_t off = (host.size() + 255) & ~size_t(255);
+    extra = off + n - host.size();
+    return off;
+  }
+  size_t extra = 0;
   void upload();  // allocate + copy; releases the host staging
   void release();
   template <class T>
@@ -225,7 +233,8 @@ struct TileTables {
   // tiles: `masked` tiles may contain coincident location pairs and apply the
   // r^2 <= eps^2 mask; the others provably cannot (exact coincidences only,
   // checked on the host) and skip it.
-  hvec<int32_t> tile_i, tile_j;          // unmasked tiles
+  hvec<int32_t> tile_i, tile_j;          // unmasked tiles (listed only for the streamed path)
+  int64_t n_unmasked = 0;
   hvec<int32_t> mtile_i, mtile_j;        // masked tiles
   bool has_second_slot = false;                 // any record with off1 >= 0
   bool equal_coefs = true;                      // every such record has c1 == c0 (bitwise)
@@ -275,7 +284,7 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hve
                     hvec<int32_t>& yb_list);
 void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
                      const hvec<int32_t>& xl_id, const hvec<int64_t>& yb_start,
-                     const hvec<int32_t>& yb_list);
+                     const hvec<int32_t>& yb_list, bool list_unmasked = true);
 // Trial locations restricted to dofs [c0, c1) (renumbered from 0, natural
 // order not yet set); slab_of_full maps full location ids to slab ids or -1.
 Locations restrict_cols(const Locations& Y, int64_t c0, int64_t c1, hvec<int32_t>& slab_of_full);
@@ -342,6 +351,26 @@ void launch_big_entries(const BigArgs& b, bool helmholtz, void* stream);
 // slots: 0 = no second slots, 1 = second slots, 2 = second slots with c1 == c0,
 // 3 = unit coefficients with per-column scales (TileTables::unit_y)
 void launch_assemble(const AsmArgs& a, int64_t ntiles, bool helmholtz, int slots, void* stream);
+// Tile descriptors built on the device from the block tables: every x block
+// bi owns the tiles (bi, bj) for bj in [first_bj[bi], nJb), numbered in
+// (bi, bj) order from tile_start[bi]; `masked_bits` flags the masked ones.
+// (The descriptors are 48 B per tile — 157 MB for cfg 4 — and building and
+// uploading them on the host cost ~70 ms per plan.)
+struct TileBuildArgs {
+  TileDesc* out;
+  int64_t ntiles;
+  int32_t nIb;
+  const int64_t* tile_start;    // [nIb + 1]
+  const int32_t* first_bj;      // [nIb]
+  const int32_t* xb_dof_start;  // [nIb + 1]
+  const int32_t* xb_loc_start;  // [nIb + 1]
+  const int32_t* yb_dof_start;  // [nJb + 1]
+  const int32_t* yb_rec_start;  // [nJb + 1]
+  const uint32_t* yb_zero;      // [nJb]
+  const int32_t* xsup_start;    // [rows + 1]
+  const uint32_t* masked_bits;  // [ceil(ntiles / 32)]
+};
+void launch_make_tiles(const TileBuildArgs& b, void* stream);
 // Copy ceil(bytes/16) 16-byte words from mapped pinned host memory (device
 // view) to device memory with SM loads (both 16-byte aligned and padded).
 void launch_fetch_tables(void* dst, const void* src_mapped, size_t bytes, void* stream);

@@ -883,13 +883,14 @@ void build_y_tables(const Locations& Y, const BlockLayout& B, TileTables& T, hve
 
 void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const Coincidence& C,
                      const hvec<int32_t>& xl_id, const hvec<int64_t>& yb_start,
-                     const hvec<int32_t>& yb_list) {
+                     const hvec<int32_t>& yb_list, bool list_unmasked) {
   const int64_t nIb = (int64_t)TX.xb_dof_start.size() - 1, nJb = (int64_t)T.yb_dof_start.size() - 1;
   T.tile_i.clear();
   T.tile_j.clear();
   T.mtile_i.clear();
   T.mtile_j.clear();
   T.pairs_evaluated = 0;
+  T.n_unmasked = 0;
   // ---- which tiles can hold a coincident (masked) pair?  With only exact
   // coincidences (find_coincidences), a tile needs the mask iff one of its x
   // locations coincides with one of its y records' locations.
@@ -915,11 +916,19 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
               (T.yb_dof_start.begin() + 1);
     for (int64_t bj = first; bj < nJb; ++bj) {
       const bool m = unsafe || std::binary_search(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)bj);
-      (m ? T.mtile_i : T.tile_i).push_back((int32_t)bi);
-      (m ? T.mtile_j : T.tile_j).push_back((int32_t)bj);
-      T.pairs_evaluated += (int64_t)(TX.xb_loc_start[bi + 1] - TX.xb_loc_start[bi]) *
-                           (T.yb_rec_start[bj + 1] - T.yb_rec_start[bj]);
+      if (m) {
+        T.mtile_i.push_back((int32_t)bi);
+        T.mtile_j.push_back((int32_t)bj);
+      } else {
+        ++T.n_unmasked;
+        if (list_unmasked) {
+          T.tile_i.push_back((int32_t)bi);
+          T.tile_j.push_back((int32_t)bj);
+        }
+      }
     }
+    T.pairs_evaluated += (int64_t)(TX.xb_loc_start[bi + 1] - TX.xb_loc_start[bi]) *
+                         (T.yb_rec_start[nJb] - T.yb_rec_start[first]);
   }
 }
 
@@ -933,7 +942,9 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
   build_y_tables(Y, B, T, yb_start, yb_list);
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
-  build_tile_list(T, T, symmetric, C, xl_id, yb_start, yb_list);
+  // the plan path builds its descriptors on the device from the block tables
+  // (launch_make_tiles): only the masked tiles are listed
+  build_tile_list(T, T, symmetric, C, xl_id, yb_start, yb_list, false);
   return T;
 }
 
@@ -1096,7 +1107,12 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
 }
 
 TileTables choose_order_and_tile(Locations& X, Locations* Y, bool symmetric, double eps) {
-  const OrderChoice O = choose_order(X, Y, symmetric, eps);
+  // symmetric plans take natural order without building the RCB candidates
+  // when it evaluates at most 1.6 pairs per unique pair (P0 on subdivided
+  // meshes: cfg 4 1.45, cfg 3 1.00 — measured faster than RCB there, and the
+  // two RCB candidates cost ~20 ms of every plan); P1 vertex numberings
+  // (cfg 2: natural ~2.9) and row-slab plans still compare all three
+  const OrderChoice O = choose_order(X, Y, symmetric, eps, symmetric ? 1.6 : 0.0);
   const auto t0 = std::chrono::steady_clock::now();
   TileTables T = build_tiles(X, Y ? *Y : X, symmetric, O.C, O.B);
   if (std::getenv("GK_TIMING"))
