@@ -444,6 +444,21 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
     mv_ms = m0.elapsed_time(m1) / 5
     pairs_ref = info["pairs_reference"]
     value = aggregate_value(pairs_ref, world, ms_step)
+    # the assembly alone, back to back, under its own clock sampler: the SM
+    # clock the kernel itself runs at (the step's median also covers the
+    # matvecs; a power-capped box clocks FP64 + store-heavy work lower than
+    # the DFMA microbenchmark)
+    asm_alone = None
+    if rank == 0:
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        with ClockSampler(dev.index or 0) as aclk:
+            q0.record(stream)
+            for _ in range(reps):
+                plan.assemble(A.data_ptr(), n, sp)
+            q1.record(stream)
+            torch.cuda.synchronize(dev)
+        asm_alone = {"ms": q0.elapsed_time(q1) / reps, "clocks": aclk.summary()}
     nf_2h = None
     if nf and rank == 0:
         # BASELINE words cfg 3's near field as "pairs closer than 2 hbar"; the
@@ -498,6 +513,9 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
                          "work": "pairs_unique (twins merged, symmetric half) x %.0f flops/pair = canonical libdevice "
                                  "probe F_pair (SURVEY 8d)" % F_PAIR_PROBE_FLOPS[helm],
                          "frac_executed_pairs_production_formula": exec_prod / sustained,
+                         "assembly_alone": asm_alone,
+                         "peak_at_kernel_clock": burst * kernel_clock_ratio(asm_alone, sus_clk),
+                         "frac_at_kernel_clock": achieved / (burst * kernel_clock_ratio(asm_alone, sus_clk)),
                          "ncu_fp64_pipe_pct": prof.get("fp64_pipe_pct"),
                          "ncu_sfu_xu_pipe_pct": prof.get("xu_pipe_pct")},
             "roofline_matvec": {"bound": "hbm", "kernel": "k_matvec_partial + k_matvec_reduce (K4)",
@@ -518,6 +536,17 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
     if with_cpu and rank == 0 and world == 1:
         out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
     return out
+
+
+def kernel_clock_ratio(alone, ref_clk):
+    """SM clock the assembly ran at (median, sampled while it ran alone) over
+    the maximum SM clock the burst DFMA peak is quoted at."""
+    try:
+        f = alone["clocks"]["sm_mhz"]
+        fmax = alone["clocks"]["sm_max_mhz"] or ref_clk.get("sm_max_mhz") or 1965.0
+        return min(1.0, float(f) / float(fmax)) if f else 1.0
+    except Exception:
+        return 1.0
 
 
 def matvec_multi_roofline(n, nmv, ms, hbm, peaks_fp64):

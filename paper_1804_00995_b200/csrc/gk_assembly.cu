@@ -232,12 +232,17 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       fold(p, cs[0], sn[0], rinv[0]);
     }
   };
-  if (a.dbg & 4) {  // timing experiment: no pair loop
+  // lanes without an x location (t >= nu: ~13% of the lanes of a cfg-4 x
+  // block) skip the pair loop instead of evaluating a far dummy point: their
+  // H column is never read, and predicated-off lanes draw no FP64 power
+  // (the kernel runs under the board power cap)
+  const bool active = t < nu;
+  if ((a.dbg & 4) || !active) {  // (dbg 4: timing experiment, no pair loop)
   } else if (masked)  // uniform per CTA
     pair_loop(std::true_type{});
   else
     pair_loop(std::false_type{});
-  if (nrec > 0) flush();
+  if (nrec > 0 && active) flush();
   cp_async_wait<0>();
   __syncthreads();
   // diagnostics (GK_ASM_PROF=1): per-tile cycles of staging / pair loop / gather
