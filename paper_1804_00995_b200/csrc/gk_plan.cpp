@@ -906,6 +906,7 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
             masked_j[bi].insert(masked_j[bi].end(), yb_list.begin() + yb_start[v], yb_list.begin() + yb_start[v + 1]);
         }
         std::sort(masked_j[bi].begin(), masked_j[bi].end());
+        masked_j[bi].erase(std::unique(masked_j[bi].begin(), masked_j[bi].end()), masked_j[bi].end());
       }
     });
   // ---- tiles (symmetric: skip tiles strictly below the diagonal)
@@ -914,18 +915,27 @@ void build_tile_list(const TileTables& TX, TileTables& T, bool symmetric, const 
     if (symmetric)
       first = std::upper_bound(T.yb_dof_start.begin() + 1, T.yb_dof_start.end(), TX.xb_dof_start[bi]) -
               (T.yb_dof_start.begin() + 1);
-    for (int64_t bj = first; bj < nJb; ++bj) {
-      const bool m = unsafe || std::binary_search(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)bj);
-      if (m) {
-        T.mtile_i.push_back((int32_t)bi);
-        T.mtile_j.push_back((int32_t)bj);
-      } else {
-        ++T.n_unmasked;
-        if (list_unmasked) {
-          T.tile_i.push_back((int32_t)bi);
-          T.tile_j.push_back((int32_t)bj);
+    if (list_unmasked || unsafe) {
+      for (int64_t bj = first; bj < nJb; ++bj) {
+        const bool m = unsafe || std::binary_search(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)bj);
+        if (m) {
+          T.mtile_i.push_back((int32_t)bi);
+          T.mtile_j.push_back((int32_t)bj);
+        } else {
+          ++T.n_unmasked;
+          if (list_unmasked) {
+            T.tile_i.push_back((int32_t)bi);
+            T.tile_j.push_back((int32_t)bj);
+          }
         }
       }
+    } else {  // count the unmasked tiles, list only the masked ones (sorted, unique)
+      const auto lo = std::lower_bound(masked_j[bi].begin(), masked_j[bi].end(), (int32_t)first);
+      for (auto it = lo; it != masked_j[bi].end(); ++it) {
+        T.mtile_i.push_back((int32_t)bi);
+        T.mtile_j.push_back(*it);
+      }
+      T.n_unmasked += (nJb - first) - (int64_t)(masked_j[bi].end() - lo);
     }
     T.pairs_evaluated += (int64_t)(TX.xb_loc_start[bi + 1] - TX.xb_loc_start[bi]) *
                          (T.yb_rec_start[nJb] - T.yb_rec_start[first]);
@@ -938,13 +948,24 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
   hvec<int32_t> xl_id;
   hvec<int64_t> yb_start;
   hvec<int32_t> yb_list;
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gk_plan]     %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   build_x_tables(X, B, T, xl_id);
+  lap("x tables");
   build_y_tables(Y, B, T, yb_start, yb_list);
+  lap("y tables");
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
   // the plan path builds its descriptors on the device from the block tables
   // (launch_make_tiles): only the masked tiles are listed
   build_tile_list(T, T, symmetric, C, xl_id, yb_start, yb_list, false);
+  lap("tile list");
   return T;
 }
 
