@@ -523,7 +523,10 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
                                 "unit": "GB/s", "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm,
                                 "traffic": prof.get("k_matvec_dram_bytes_per_call"),
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
-            "roofline_matvec_multi": matvec_multi_roofline(n, nmv, mvs_ms, hbm, peaks_fp64) if multi else None,
+            "roofline_matvec_multi": (matvec_multi_roofline(n, nmv, mvs_ms, hbm, peaks_fp64)
+                                      | {"traffic": prof.get("k_matvec_multi_dram_bytes_per_call"),
+                                         "ncu_fp64_pipe_pct": prof.get("k_matvec_multi_fp64_pipe_pct")})
+            if multi else None,
             "step_share": {"assembly": asm_ms / ms_step, "nearfield": (nf_ms or 0.0) / ms_step,
                            "matvecs": mvs_ms / ms_step},
             "clocks": clk.summary(),
