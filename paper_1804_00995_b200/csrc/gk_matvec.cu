@@ -106,27 +106,45 @@ void plan(int64_t rows, int64_t cols, int64_t& splits, int64_t& cps) {
 // bound the pass about equally, so the A stream must never wait on the FP64
 // work.  A register-prefetch version stalled on its loads (long_scoreboard 66%,
 // FP64 pipe 44%), so the stream is asynchronous: one elected thread per CTA
-// issues bulk copies (cp.async.bulk, the TMA engine; one contiguous 4 KB
-// column segment of the CTA's 256 rows per column, L2 evict-first) into a
-// ring of shared-memory stages completed on mbarriers, while all 256 threads
+// issues bulk copies (cp.async.bulk, the TMA engine; one contiguous
+// column segment of the CTA's rows per column, L2 evict-first) into a
+// ring of shared-memory stages completed on mbarriers, while all threads
 // multiply the stage that has landed (thread = row; A from shared memory,
 // conflict-free; x values broadcast from the stage's copy of X).  Each
 // (row, right-hand side) sums its columns in order in one chain; the same
 // split-K + fixed-order reduce as above: deterministic, and column r of Y does
 // not depend on the other columns.
-constexpr int kBkStages = 3;  // stages in the ring (2 CTAs x ~99 KB per SM)
+#ifndef GK_MM_STAGES
+#define GK_MM_STAGES 2
+#endif
+#ifndef GK_MM_MINB
+#define GK_MM_MINB 3
+#endif
+#ifndef GK_MM_STAGE_KB
+#define GK_MM_STAGE_KB 28
+#endif
+#ifndef GK_MM_THREADS
+#define GK_MM_THREADS 128
+#endif
+// CTA shape (sweep on cfg 4, 10 vectors; threads / stages / KB of A per stage
+// / min CTAs per SM -> ms): 256/3/32/2 24.0, 128/3/32/2 25.3, 128/2/32/2 22.7,
+// 128/2/24/2 22.3, 128/2/24/4 23.5, 128/2/48/2 24.6, 64/2/32/2 28.3,
+// 128/3/16/2 31.2, 128/2/28/3 21.9 (kept: three CTAs of four warps per SM,
+// each with one stage landing while the other is multiplied)
+constexpr int kBkStages = GK_MM_STAGES;
+constexpr int kMmThreads = GK_MM_THREADS;
 constexpr int kMmMaxR = 10;   // right-hand sides per pass (larger counts: several passes)
 // Rows per thread: 2 for many right-hand sides (each broadcast x value then
 // feeds two rows: 9 instead of 14 shared-memory wavefronts per 32 rows and
-// column at R = 10), 1 otherwise.  A stage holds 256 RPT rows x 8 / RPT
-// columns (32 KB).
+// column at R = 10), 1 otherwise.  A stage holds kMmThreads RPT rows x as
+// many columns as fit in GK_MM_STAGE_KB.
 template <int R>
 constexpr int mm_rpt() {
   return R >= 6 ? 2 : 1;
 }
 template <int RPT>
 struct MmSmem {
-  static constexpr int kRows = kMvThreads * RPT, kCols = 8 / RPT;
+  static constexpr int kRows = kMmThreads * RPT, kCols = GK_MM_STAGE_KB * 64 / kRows;  // KB of A per stage
   double2 a[kBkStages][kCols][kRows];
   double2 x[kBkStages][kMmMaxR][kCols];
   unsigned long long full[kBkStages];
@@ -160,7 +178,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 template <int R>
-__global__ void __launch_bounds__(kMvThreads, 2)
+__global__ void __launch_bounds__(kMmThreads, GK_MM_MINB)
     k_matvec_multi_partial(const double2* __restrict__ A, long long rows, long long cols, long long lda,
                            const double2* __restrict__ X, long long ldx, double2* __restrict__ P, long long cps,
                            int splits) {
@@ -200,11 +218,11 @@ __global__ void __launch_bounds__(kMvThreads, 2)
     for (int r = 0; r < R; ++r) re[k][r] = im[k][r] = 0.0;
   bool act[RPT];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) act[k] = t + k * kMvThreads < nr;
+  for (int k = 0; k < RPT; ++k) act[k] = t + k * kMmThreads < nr;
   auto column = [&](int buf, int c) {
     double2 v[RPT];
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) v[k] = S.a[buf][c][t + k * kMvThreads];  // rows past nr: stale, never stored
+    for (int k = 0; k < RPT; ++k) v[k] = S.a[buf][c][t + k * kMmThreads];  // rows past nr: stale, never stored
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double2 xj = S.x[buf][r][c];
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(kMvThreads, 2)
     if (act[k])
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        P[((long long)r * splits + blockIdx.y) * rows + ib + t + k * kMvThreads] = make_double2(re[k][r], im[k][r]);
+        P[((long long)r * splits + blockIdx.y) * rows + ib + t + k * kMmThreads] = make_double2(re[k][r], im[k][r]);
 }
 
 __global__ void k_matvec_multi_reduce(const double2* __restrict__ P, long long rows, int splits, int nr,
@@ -271,7 +289,7 @@ void launch_multi_r(const double2* A, int64_t rows, int64_t cols, int64_t lda, c
                "cudaFuncSetAttribute");
     configured |= 1ull << dev;
   }
-  k_matvec_multi_partial<R><<<grid, kMvThreads, smem, s>>>(A, rows, cols, lda, X, ldx, P, cps, (int)splits);
+  k_matvec_multi_partial<R><<<grid, kMmThreads, smem, s>>>(A, rows, cols, lda, X, ldx, P, cps, (int)splits);
 }
 
 using MultiFn = void (*)(const double2*, int64_t, int64_t, int64_t, const double2*, int64_t, double2*, int64_t,
