@@ -26,6 +26,7 @@
 // every record — the P1 edge-midpoint rule — so c*rinv is formed once).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <type_traits>
@@ -117,61 +118,15 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// The pair loop of one tile for thread t (its x location u = (ux, uy, uz)):
+// G(u, v) for every record v of the tile, folded into the thread's column Hb
+// of the y-side accumulator H (see k_assemble).
 template <bool HELM, int SLOTS>
-__global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const AsmArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
-  const int t = threadIdx.x;
-  if (a.prof && t == 0) S.prof[0] = clock64(), S.prof_done = 0;
-  const int4* dp = reinterpret_cast<const int4*>(a.tiles + blockIdx.x);
-  const int4 d0 = __ldg(dp), d1 = __ldg(dp + 1), d2 = __ldg(dp + 2);
-  const int i0 = d0.x, nI = d0.y, j0 = d0.z, nJ = d0.w;
-  const int l0 = d1.x, nu = d1.y, r0 = d1.z, nrec = d1.w;
-  const int xs0 = d2.x, nxs = d2.y;
-  const uint32_t zero_rows = (uint32_t)d2.z;
-  const bool masked = d2.w != 0;
-
-  // stage with cp.async (no register staging): group 0 = the records the pair
-  // loop needs now; group 1 = the x support lists and dof maps the gather
-  // needs only after the pair loop, so their latency hides behind it.
-  // Each H row is first written by its own run flush (a plain store; the
-  // host orders the runs so that every read-modify-write of a row comes
-  // after it); only rows without a run (host bitmask) are zero-filled.
-  // each thread zero-fills its own column of the rows without a run (the
-  // pair loop touches only that column; the gather comes after a barrier)
-  for (uint32_t m = zero_rows; m; m &= m - 1) S.H[(__ffs(m) - 1) * kHS + t] = make_double2(0.0, 0.0);
-  constexpr int kRW = rec_words<SLOTS>();
-  // (records read straight from global memory by warp-uniform loads instead
-  // of staged here measured 59.4 vs 44.6 ms on cfg 4)
-  const double2* const recs = reinterpret_cast<const double2*>(S.rec);
-  {
-    const double2* src = reinterpret_cast<const double2*>(a.yrec) + (long long)r0 * kRW;
-    double2* dst = reinterpret_cast<double2*>(S.rec);
-    for (int e = t; e < nrec * kRW; e += kAsmThreads) cp_async16(dst + e, src + e);
-  }
-  cp_async_commit();
-  for (int e = t; e < nxs; e += kAsmThreads) {
-    cp_async8(S.xs_c + e, a.xsup_c + xs0 + e);
-    cp_async4(S.xs_u + e, a.xsup_u + xs0 + e);
-  }
-  for (int e = t; e <= nI; e += kAsmThreads) cp_async4(S.xs_start + e, a.xsup_start + i0 + e);  // global offsets
-  if (!a.natural) {  // natural order: A's row/column index is the permuted one (no maps)
-    for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
-    for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
-  }
-  if (SLOTS == 3)
-    for (int e = t; e < nJ; e += kAsmThreads) cp_async8(S.ys + e, a.yscale + j0 + e);
-  cp_async_commit();
-  // my x location; idle columns are far away (finite, never gathered)
-  const double ux = t < nu ? __ldg(a.xl_x + l0 + t) : 1e100;
-  const double uy = t < nu ? __ldg(a.xl_y + l0 + t) : 0.0;
-  const double uz = t < nu ? __ldg(a.xl_z + l0 + t) : 0.0;
-  cp_async_wait<1>();
-  __syncthreads();
-  if (a.prof && t == 0) S.prof[1] = clock64();
-
+__device__ __forceinline__ void pair_phase(const AsmArgs& a, const double2* const recs, const int nrec, const int nu,
+                                           const bool masked, const int t, const double ux, const double uy,
+                                           const double uz, char* const Hb) {
   const double eps2 = a.eps2, kappa = a.kappa;
-  char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
+  constexpr int kRW = rec_words<SLOTS>();
   // run accumulator of the current first slot; cur starts at the first
   // record's slot so that the fold below needs no "first run" case
   int cur = nrec > 0 ? load_rec<SLOTS>(recs).off0 : 0;  // byte offset of the run's slot row
@@ -245,30 +200,24 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   else
     pair_loop(std::false_type{});
   if (nrec > 0 && active) flush();
-  cp_async_wait<0>();
-  __syncthreads();
-  // diagnostics (GK_ASM_PROF=1): per-tile cycles of staging / pair loop / gather
-  struct PhaseProf {
-    const AsmArgs& a;
-    AsmSmem& S;
-    __device__ ~PhaseProf() {
-      if (!a.prof) return;
-      // no barrier: threads leave the gather at different points; the last
-      // one to finish records the end of the tile
-      __threadfence_block();
-      if (atomicAdd(&S.prof_done, 1u) == blockDim.x - 1) {
-        unsigned long long* o = a.prof + 4ull * blockIdx.x;
-        o[0] = (unsigned long long)(S.prof[1] - S.prof[0]);
-        o[1] = (unsigned long long)(S.prof[2] - S.prof[1]);
-        o[2] = (unsigned long long)(clock64() - S.prof[2]);
-        unsigned smid;
-        asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        o[3] = smid;
-      }
-    }
-  } prof_guard{a, S};
-  if (a.prof && t == 0) S.prof[2] = clock64();
+}
 
+// Shared-memory tables of one tile's x-side contraction.
+struct GatherView {
+  const double2* H;
+  const double* xs_c;
+  const int32_t* xs_u;
+  const int32_t* xs_start;
+  const int32_t* orow;
+  const int32_t* ocol;
+  const double* ys;
+};
+
+// The x-side contraction and matrix writes of one tile by the 128 threads
+// t = 0..127 of a group (see k_assemble).
+template <int SLOTS>
+__device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView& S, const int i0, const int nI,
+                                             const int j0, const int nJ, const int xs0, const int t) {
   constexpr int kGC = gather_cols<SLOTS>();
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
   // the row's support entries are read once per item and feed kGC independent
@@ -434,6 +383,88 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
       }
     }
   }
+}
+
+template <bool HELM, int SLOTS>
+__global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const AsmArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
+  const int t = threadIdx.x;
+  if (a.prof && t == 0) S.prof[0] = clock64(), S.prof_done = 0;
+  const int4* dp = reinterpret_cast<const int4*>(a.tiles + blockIdx.x);
+  const int4 d0 = __ldg(dp), d1 = __ldg(dp + 1), d2 = __ldg(dp + 2);
+  const int i0 = d0.x, nI = d0.y, j0 = d0.z, nJ = d0.w;
+  const int l0 = d1.x, nu = d1.y, r0 = d1.z, nrec = d1.w;
+  const int xs0 = d2.x, nxs = d2.y;
+  const uint32_t zero_rows = (uint32_t)d2.z;
+  const bool masked = d2.w != 0;
+
+  // stage with cp.async (no register staging): group 0 = the records the pair
+  // loop needs now; group 1 = the x support lists and dof maps the gather
+  // needs only after the pair loop, so their latency hides behind it.
+  // Each H row is first written by its own run flush (a plain store; the
+  // host orders the runs so that every read-modify-write of a row comes
+  // after it); only rows without a run (host bitmask) are zero-filled.
+  // each thread zero-fills its own column of the rows without a run (the
+  // pair loop touches only that column; the gather comes after a barrier)
+  for (uint32_t m = zero_rows; m; m &= m - 1) S.H[(__ffs(m) - 1) * kHS + t] = make_double2(0.0, 0.0);
+  constexpr int kRW = rec_words<SLOTS>();
+  // (records read straight from global memory by warp-uniform loads instead
+  // of staged here measured 59.4 vs 44.6 ms on cfg 4)
+  const double2* const recs = reinterpret_cast<const double2*>(S.rec);
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.yrec) + (long long)r0 * kRW;
+    double2* dst = reinterpret_cast<double2*>(S.rec);
+    for (int e = t; e < nrec * kRW; e += kAsmThreads) cp_async16(dst + e, src + e);
+  }
+  cp_async_commit();
+  for (int e = t; e < nxs; e += kAsmThreads) {
+    cp_async8(S.xs_c + e, a.xsup_c + xs0 + e);
+    cp_async4(S.xs_u + e, a.xsup_u + xs0 + e);
+  }
+  for (int e = t; e <= nI; e += kAsmThreads) cp_async4(S.xs_start + e, a.xsup_start + i0 + e);  // global offsets
+  if (!a.natural) {  // natural order: A's row/column index is the permuted one (no maps)
+    for (int e = t; e < nI; e += kAsmThreads) cp_async4(S.orow + e, a.xperm + i0 + e);
+    for (int e = t; e < nJ; e += kAsmThreads) cp_async4(S.ocol + e, a.yperm + j0 + e);
+  }
+  if (SLOTS == 3)
+    for (int e = t; e < nJ; e += kAsmThreads) cp_async8(S.ys + e, a.yscale + j0 + e);
+  cp_async_commit();
+  // my x location; idle columns are far away (finite, never gathered)
+  const double ux = t < nu ? __ldg(a.xl_x + l0 + t) : 1e100;
+  const double uy = t < nu ? __ldg(a.xl_y + l0 + t) : 0.0;
+  const double uz = t < nu ? __ldg(a.xl_z + l0 + t) : 0.0;
+  cp_async_wait<1>();
+  __syncthreads();
+  if (a.prof && t == 0) S.prof[1] = clock64();
+
+  char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
+  pair_phase<HELM, SLOTS>(a, recs, nrec, nu, masked, t, ux, uy, uz, Hb);
+  cp_async_wait<0>();
+  __syncthreads();
+  // diagnostics (GK_ASM_PROF=1): per-tile cycles of staging / pair loop / gather
+  struct PhaseProf {
+    const AsmArgs& a;
+    AsmSmem& S;
+    __device__ ~PhaseProf() {
+      if (!a.prof) return;
+      // no barrier: threads leave the gather at different points; the last
+      // one to finish records the end of the tile
+      __threadfence_block();
+      if (atomicAdd(&S.prof_done, 1u) == blockDim.x - 1) {
+        unsigned long long* o = a.prof + 4ull * blockIdx.x;
+        o[0] = (unsigned long long)(S.prof[1] - S.prof[0]);
+        o[1] = (unsigned long long)(S.prof[2] - S.prof[1]);
+        o[2] = (unsigned long long)(clock64() - S.prof[2]);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        o[3] = smid;
+      }
+    }
+  } prof_guard{a, S};
+  if (a.prof && t == 0) S.prof[2] = clock64();
+
+  gather_phase<SLOTS>(a, GatherView{S.H, S.xs_c, S.xs_u, S.xs_start, S.orow, S.ocol, S.ys}, i0, nI, j0, nJ, xs0, t);
 }
 
 template <bool HELM, int SLOTS>
