@@ -146,6 +146,7 @@ struct gk_plan {
   double x_halo = 0.0, y_halo = 0.0;
   bool natural = false;
   int64_t xblocks = 0, yblocks = 0;
+  int32_t jmax = 0;  // widest y block (dofs): selects the k_assemble shape
   int slots = 1;  // k_assemble SLOTS specialisation (0 none, 1 second slots, 2 with c1 == c0, 3 unit + scales)
   // device tables in one arena: TileDesc per tile ((x block, y block) order,
   // masked ones flagged), x locations, x supports, y records, dof maps
@@ -334,6 +335,8 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->natural = X.natural;
   P->xblocks = (int64_t)T.xb_dof_start.size() - 1;
   P->yblocks = (int64_t)T.yb_dof_start.size() - 1;
+  for (int64_t bj = 0; bj < P->yblocks; ++bj)
+    P->jmax = std::max<int32_t>(P->jmax, T.yb_dof_start[bj + 1] - T.yb_dof_start[bj]);
   P->ntiles = T.n_unmasked;
   P->nmtiles = (int64_t)T.mtile_i.size();
   P->slots = slots_of(T);
@@ -447,6 +450,7 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.natural = P->natural ? 1 : 0;
   a.prof = nullptr;
   a.dbg = std::getenv("GK_ASM_DBG") ? std::atoi(std::getenv("GK_ASM_DBG")) : 0;
+  a.jmax = P->jmax;
   if (P->nbig_rows || P->nbig_cols) {
     BigArgs b;
     b.rows = Ar.at<int32_t>(P->o_big_rows);
@@ -781,6 +785,7 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     a.natural = 0;
     a.prof = nullptr;
     a.dbg = 0;
+    a.jmax = kJCap;  // slabs: the 22-row shape serves every y block
     double wait_ms = 0.0;
     for (int64_t s = 0; s < nslab; ++s) {
       {

@@ -41,29 +41,47 @@ namespace {
 #ifndef GK_GATHER_G
 #define GK_GATHER_G 4  // tile columns per gather work unit of symmetric tiles (even)
 #endif
-#ifndef GK_ASM_UNROLL
-#define GK_ASM_UNROLL 6  // measured (cfg 2 / cfg 3 ms): 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56
-#endif
-constexpr int kRecUnroll = GK_ASM_UNROLL;  // records per group = independent evaluations per thread
-// gather: columns per work item (divides kJCap).  Measured (cfg 2 P1 / cfg 3 P0
+// Two kernel shapes, chosen per launch by the plan's widest y block:
+//  - JC = 22 (y blocks of up to 22 dofs; P1 vertex blocks, cfg 2): 4 CTAs per
+//    SM, six records per lockstep group (cfg 2 / cfg 3 ms by records per
+//    group: 2: 2.69 / 19.56, 4: 2.55 / 19.32, 6: 2.53 / 19.22, 8: 2.76 / 19.56);
+//  - JC = 16 (every y block <= 16 dofs; P0 subtree blocks, cfg 4): H is 32 KB,
+//    so 5 CTAs (20 warps) fit per SM, at <= 102 registers: three records per
+//    group (96 registers, no spills).  cfg 4 by (CTAs, records per group):
+//    (4, 6) 44.6, (4, 3) 46.1, (5, 2) 44.4, (5, 3) 43.3, (5, 4) 47.2,
+//    (5, 5) 46.3 ms.
+template <int JC>
+struct AsmShape;
+template <>
+struct AsmShape<22> {
+  static constexpr int ctas = 4, unroll = 6;
+};
+template <>
+struct AsmShape<16> {
+  static constexpr int ctas = 5, unroll = 3;
+};
+static_assert(kJCap == 22 && kJCapSmall == 16, "the kernel shapes cover the planner's two y-block caps");
+// gather: columns per work item (divides JC).  Measured (cfg 2 P1 / cfg 3 P0
 // ms): 1: 2.54 / 19.09, 2: 2.53 / 19.20, 11: 2.50 / 19.45 -> 11 for the P1
 // edge-midpoint specialisation (SLOTS = 2), 2 otherwise.
-template <int SLOTS>
+template <int SLOTS, int JC>
 constexpr int gather_cols() {
-  return SLOTS == 2 && kJCap % 11 == 0 ? 11 : 2;
+  return SLOTS == 2 && JC % 11 == 0 ? 11 : 2;
 }
-static_assert(kJCap % gather_cols<2>() == 0 && kJCap % gather_cols<0>() == 0 && kJCap % gather_cols<3>() == 0,
+static_assert(22 % gather_cols<2, 22>() == 0 && 16 % gather_cols<2, 16>() == 0 && 22 % gather_cols<0, 22>() == 0 &&
+                  16 % gather_cols<0, 16>() == 0,
               "gather column groups must tile the H rows");
 
+template <int JC>
 struct AsmSmem {
-  double2 H[kJCap * kHS];  // y-side partial sums H[j][u]
+  double2 H[JC * kHS];  // y-side partial sums H[j][u]
   YRec rec[kRCap];
   double xs_c[kXsCap];
   int32_t xs_u[kXsCap];
   int32_t xs_start[kIMax + 1];
   int32_t orow[kIMax];  // original row index of each tile row
-  int32_t ocol[kJCap];  // original column index of each tile column
-  double ys[kJCap];      // per-column scale (SLOTS == 3)
+  int32_t ocol[JC];  // original column index of each tile column
+  double ys[JC];      // per-column scale (SLOTS == 3)
   long long prof[3];     // diagnostics (GK_ASM_PROF): phase start clocks
   unsigned prof_done;    // threads finished (the last one records the end)
 };
@@ -121,7 +139,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // The pair loop of one tile for thread t (its x location u = (ux, uy, uz)):
 // G(u, v) for every record v of the tile, folded into the thread's column Hb
 // of the y-side accumulator H (see k_assemble).
-template <bool HELM, int SLOTS>
+template <bool HELM, int SLOTS, int kRecUnroll>
 __device__ __forceinline__ void pair_phase(const AsmArgs& a, const double2* const recs, const int nrec, const int nu,
                                            const bool masked, const int t, const double ux, const double uy,
                                            const double uz, char* const Hb) {
@@ -215,10 +233,10 @@ struct GatherView {
 
 // The x-side contraction and matrix writes of one tile by the 128 threads
 // t = 0..127 of a group (see k_assemble).
-template <int SLOTS>
+template <int SLOTS, int JC>
 __device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView& S, const int i0, const int nI,
                                              const int j0, const int nJ, const int xs0, const int t) {
-  constexpr int kGC = gather_cols<SLOTS>();
+  constexpr int kGC = gather_cols<SLOTS, JC>();
   // x-side contraction + write.  Work item = (row ii, kGC consecutive columns):
   // the row's support entries are read once per item and feed kGC independent
   // H loads; lanes run along rows (coalesced columns of the direct block).
@@ -244,7 +262,7 @@ __device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView&
     if (SLOTS == 3)
 #pragma unroll
       for (int q = 0; q < kGC; ++q) {
-        const double f = S.ys[min(jb + q, kJCap - 1)];
+        const double f = S.ys[min(jb + q, JC - 1)];
         re[q] *= f;
         im[q] *= f;
       }
@@ -314,7 +332,7 @@ __device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView&
     }
     int jq[kG];
 #pragma unroll
-    for (int q = 0; q < kG; ++q) jq[q] = min(max(jb + q, 0), kJCap - 1);  // in-bounds H row (stale rows unused)
+    for (int q = 0; q < kG; ++q) jq[q] = min(max(jb + q, 0), JC - 1);  // in-bounds H row (stale rows unused)
     double2 h[kG][kSupCache];
 #pragma unroll
     for (int q = 0; q < kG; ++q)
@@ -385,10 +403,10 @@ __device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView&
   }
 }
 
-template <bool HELM, int SLOTS>
-__global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const AsmArgs a) {
+template <bool HELM, int SLOTS, int JC>
+__global__ void __launch_bounds__(kAsmThreads, AsmShape<JC>::ctas) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
+  AsmSmem<JC>& S = *reinterpret_cast<AsmSmem<JC>*>(smem_raw);
   const int t = threadIdx.x;
   if (a.prof && t == 0) S.prof[0] = clock64(), S.prof_done = 0;
   const int4* dp = reinterpret_cast<const int4*>(a.tiles + blockIdx.x);
@@ -439,13 +457,13 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   if (a.prof && t == 0) S.prof[1] = clock64();
 
   char* const Hb = reinterpret_cast<char*>(S.H) + t * 16;  // my column of H
-  pair_phase<HELM, SLOTS>(a, recs, nrec, nu, masked, t, ux, uy, uz, Hb);
+  pair_phase<HELM, SLOTS, AsmShape<JC>::unroll>(a, recs, nrec, nu, masked, t, ux, uy, uz, Hb);
   cp_async_wait<0>();
   __syncthreads();
   // diagnostics (GK_ASM_PROF=1): per-tile cycles of staging / pair loop / gather
   struct PhaseProf {
     const AsmArgs& a;
-    AsmSmem& S;
+    AsmSmem<JC>& S;
     __device__ ~PhaseProf() {
       if (!a.prof) return;
       // no barrier: threads leave the gather at different points; the last
@@ -464,22 +482,32 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmCtasPerSm) k_assemble(const A
   } prof_guard{a, S};
   if (a.prof && t == 0) S.prof[2] = clock64();
 
-  gather_phase<SLOTS>(a, GatherView{S.H, S.xs_c, S.xs_u, S.xs_start, S.orow, S.ocol, S.ys}, i0, nI, j0, nJ, xs0, t);
+  gather_phase<SLOTS, JC>(a, GatherView{S.H, S.xs_c, S.xs_u, S.xs_start, S.orow, S.ocol, S.ys}, i0, nI, j0, nJ, xs0,
+                          t);
 }
 
-template <bool HELM, int SLOTS>
-void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
-  const size_t smem = sizeof(AsmSmem);
+template <bool HELM, int SLOTS, int JC>
+void launch_shape(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
+  const size_t smem = sizeof(AsmSmem<JC>);
   // the dynamic shared memory attribute is per device context: one flag per
   // device and instantiation
   static std::atomic<uint64_t> configured{0};
   const int dev = current_device();
   if (!((configured.load() >> dev) & 1u)) {
-    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    cuda_check(cudaFuncSetAttribute(k_assemble<HELM, SLOTS, JC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem),
                "cudaFuncSetAttribute");
     configured |= 1ull << dev;
   }
-  k_assemble<HELM, SLOTS><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+  k_assemble<HELM, SLOTS, JC><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
+}
+
+template <bool HELM, int SLOTS>
+void launch_one(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
+  if (a.jmax <= 16)
+    launch_shape<HELM, SLOTS, 16>(a, ntiles, s);
+  else
+    launch_shape<HELM, SLOTS, 22>(a, ntiles, s);
 }
 
 template <bool HELM>

@@ -182,18 +182,11 @@ double guard_radius_pts(int64_t na, const double* ax, const double* ay, const do
 // 128-thread CTAs (22-dof y blocks) 2.57 ms although the smaller blocks
 // evaluate 7% more pairs (halo 1.71 vs 1.61).
 constexpr int kUCap = 128;   // x locations per tile, one per thread
-#ifndef GK_JCAP
-#define GK_JCAP 22
-#endif
-constexpr int kJCap = GK_JCAP;  // y dofs per tile (H accumulator rows)
+constexpr int kJCap = 22;       // y dofs per tile (H accumulator rows)
 constexpr int kJCapSmall = 16;  // alternative y-block cap the planner tries (layout_y_blocks)
 constexpr int kIMax = 128;   // x dofs per tile
 constexpr int kRCap = 112;   // y records per tile (staged in shared memory)
 constexpr int kXsCap = 320;  // x support entries per tile (staged in shared memory)
-#ifndef GK_ASM_CTAS
-#define GK_ASM_CTAS 4
-#endif
-constexpr int kAsmCtasPerSm = GK_ASM_CTAS;
 constexpr int kAsmThreads = kUCap;
 constexpr int kAlign = 16;   // natural-order block alignment (4^2 subdivision subtrees)
 constexpr int kHS = kUCap;  // H row stride in 16-byte entries
@@ -324,6 +317,7 @@ struct AsmArgs {
   int32_t symmetric;
   int32_t natural;  // dof orders are the identity: A's indices are the permuted ones (no perm lookups)
   unsigned long long* prof;  // diagnostics: [tile][4] phase cycles + SM id, or null
+  int32_t jmax;              // widest y block of the launch (dofs): selects the kernel shape (16 or 22)
   int32_t dbg;               // timing experiments only (GK_ASM_DBG; results invalid when set): 1 no stores, 2 no gather, 4 no pair loop, 8 no second-slot read-modify-write
 };
 // Entries of oversized dofs (rows `rows` x all columns, all rows x columns
