@@ -5,10 +5,10 @@
 //    64-bit getrf/getrs (a library factorisation, loaded on first use).
 //  * gk_gmres: restarted GMRES of linsolve.cpp:19-121 with the stored matrix
 //    as the operator (LinearOperator::from_matrix, linsolve.hpp:20-23).  The
-//    Krylov basis stays in HBM; each iteration is one K4 matvec, a classical
-//    Gram-Schmidt pass applied twice (CGS2: numerically equivalent to the
-//    reference's modified Gram-Schmidt, but two multi-dot / multi-axpy
-//    kernels instead of 2(j+1) dependent ones) and a norm.  The tiny
+//    Krylov basis stays in HBM; each iteration is one K4 matvec, the
+//    reference's modified Gram-Schmidt (linsolve.cpp:59-63: j + 1 dependent
+//    dot / axpy pairs, each dot a two-stage fixed-order reduction left on the
+//    device for the axpy that follows) and a norm.  The tiny
 //    Hessenberg least-squares problem (Givens rotations, back substitution)
 //    runs on the host exactly as in the reference.  All reductions are
 //    two-stage with a fixed order: results are deterministic.
@@ -176,11 +176,6 @@ __global__ void k_normalize(const double2* __restrict__ in, const double2* __res
   out[r] = make_double2(in[r].x / s, in[r].y / s);
 }
 
-// h[i] += h2[i]
-__global__ void k_add(double2* __restrict__ h, const double2* __restrict__ h2, int k) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) h[i] = make_double2(h[i].x + h2[i].x, h[i].y + h2[i].y);
-}
 
 // r = b - r
 __global__ void k_bminus(const double2* __restrict__ b, double2* __restrict__ r, long long n) {
@@ -290,17 +285,15 @@ gk_status gk_gmres(const gk_cplx* A, int64_t n, int64_t lda, const gk_cplx* b, g
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int m = restart;
     Krylov K(n, s);
-    DevBuf Vb, wb, rb, hb, h2b;
+    DevBuf Vb, wb, rb, hb;
     Vb.alloc(sizeof(double2) * (size_t)n * (m + 1));
     wb.alloc(sizeof(double2) * (size_t)n);
     rb.alloc(sizeof(double2) * (size_t)n);
     hb.alloc(sizeof(double2) * (size_t)(m + 2));
-    h2b.alloc(sizeof(double2) * (size_t)(m + 1));
     double2* V = Vb.as<double2>();
     double2* w = wb.as<double2>();
     double2* r = rb.as<double2>();
     double2* h = hb.as<double2>();     // [0..j]: projections, [m+1]: squared norm
-    double2* h2 = h2b.as<double2>();   // second Gram-Schmidt pass
     double2* X = reinterpret_cast<double2*>(x);
     const double2* B = reinterpret_cast<const double2*>(b);
     const double2* Ad = reinterpret_cast<const double2*>(A);
@@ -344,12 +337,11 @@ gk_status gk_gmres(const gk_cplx* A, int64_t n, int64_t lda, const gk_cplx* b, g
       int j = 0;
       for (; j < m && total < maxit; ++j, ++total) {
         launch_matvec(Ad, n, n, lda, V + (size_t)j * n, w, s);
-        // CGS2: h = V^H w, w -= V h, then once more with h2 (h += h2)
-        K.dots(V, n, j + 1, w, h, false);
-        K.axpys(V, n, j + 1, h, -1.0, w);
-        K.dots(V, n, j + 1, w, h2, false);
-        K.axpys(V, n, j + 1, h2, -1.0, w);
-        k_add<<<(j + 64) / 64, 64, 0, s>>>(h, h2, j + 1);
+        // modified Gram-Schmidt as linsolve.cpp:59-63: h_i = V_i^H w, w -= h_i V_i
+        for (int i = 0; i <= j; ++i) {
+          K.dots(V + (size_t)i * n, n, 1, w, h + i, false);
+          K.axpys(V + (size_t)i * n, n, 1, h + i, -1.0, w);
+        }
         K.dots(w, n, 1, w, h + m + 1, false);
         fetch(j + 1);
         for (int i = 0; i <= j; ++i) Hij(i, j) = cd(hh[i].x, hh[i].y);
