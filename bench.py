@@ -537,7 +537,13 @@ def run_dense(args, g, torch, dev, rank, world, dist, cfg, steps, warmup, peaks_
         torch.cuda.empty_cache()
         out["e2e"] = e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup, multi)
     if with_cpu and rank == 0 and world == 1:
-        out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
+        R = load_ref_module() if cfg in (1, 2, 4) else None
+        if R is not None:  # the reference's own code, one thread, four slices of the mesh (~10-20 s)
+            r = reference_arm_compiled(args, R, cfg, threads=1, steps=4, warmup=0)
+            out["cpu_baseline"] = {"value": r["value"], "unit": "pairs/s", "cores": 1, "kind": "reference",
+                                   "sample": r["sample"]}
+        else:
+            out["cpu_baseline"] = cpu_baseline(load_oracle(), cfg, args.cpu_chunks if cfg == 4 else 2, threads=1)
     return out
 
 
@@ -818,7 +824,7 @@ def mem_available_bytes():
     return 16 << 30
 
 
-def reference_arm_compiled(args, R, cfg):
+def reference_arm_compiled(args, R, cfg, threads=None, steps=None, warmup=None):
     """The reference's own bem_product (assembly.cpp:192-222, through bem_dense
     :313-320, single-threaded as written) on the box's host cores: each step,
     every worker thread runs the reference on its own contiguous slice of test
@@ -841,7 +847,9 @@ def reference_arm_compiled(args, R, cfg):
     N = nv if fam == 1 else ne
     M = ne * g
     R.rule(g)  # the reference's rule cache (a std::map) is filled before the threads start
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
     # per-thread slice: about 96 test triangles (288 points, well under the
     # reference's 1024-point chunk) — a few seconds of single-core work
     per = max(1, min(96, ne // threads))
@@ -883,10 +891,10 @@ def reference_arm_compiled(args, R, cfg):
         return wall * M / pts + t_mv * N / rows.shape[0], wall, t_mv, rows.shape[0]
 
     one_step()  # warm-up (page faults, thread start)
-    for _ in range(max(0, min(args.warmup, 1) - 1)):
+    for _ in range(max(0, min(warmup, 1) - 1)):
         one_step()
     ests, walls = [], []
-    for _ in range(args.steps):
+    for _ in range(steps):
         est, wall, t_mv, nrows = one_step()
         ests.append(est)
         walls.append(wall)
