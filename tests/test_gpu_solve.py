@@ -73,10 +73,13 @@ def test_gmres_bem_system_matches_oracle(galerk, cuda_device, name, k, restart, 
     # output reaches 1e-2 in the history by iteration ~18), so the iterates
     # agree to rounding only over the first ~10 iterations; after that the
     # checks are on the converged solution and the iteration count.
+    # both sides orthogonalise by modified Gram-Schmidt (linsolve.cpp:59-63):
+    # measured, the first 10 entries agree to <= 1e-14 and the iteration
+    # counts are equal on the shifted systems (510 vs 516 on the unshifted one)
     ne = min(10, len(h), len(ho))
     assert ne >= 3
-    assert np.allclose(h[:ne], ho[:ne], rtol=1e-8, atol=0)
-    assert abs(info["iterations"] - io["iterations"]) <= max(2, 0.1 * io["iterations"])
+    assert np.allclose(h[:ne], ho[:ne], rtol=1e-12, atol=0)
+    assert abs(info["iterations"] - io["iterations"]) <= (1 if shifted else max(2, 0.02 * io["iterations"]))
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= (1e-5 if shifted else 1e-2)
     assert all(h[i] <= h[i - 1] * (1 + 1e-10) + 1e-14 for i in range(1, len(h)))
 
