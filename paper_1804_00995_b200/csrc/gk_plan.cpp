@@ -956,10 +956,11 @@ TileTables build_tiles(const Locations& X, const Locations& Y, bool symmetric, c
     std::fprintf(stderr, "[gk_plan]     %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
+  // the x and y tables are independent (disjoint members of T): built concurrently
+  auto ytab = std::async(std::launch::async, [&] { build_y_tables(Y, B, T, yb_start, yb_list); });
   build_x_tables(X, B, T, xl_id);
-  lap("x tables");
-  build_y_tables(Y, B, T, yb_start, yb_list);
-  lap("y tables");
+  ytab.get();
+  lap("x + y tables");
   T.x_halo = X.size() ? (double)T.xl_x.size() / (double)X.size() : 0.0;
   T.y_halo = Y.size() ? (double)T.yrec.size() / (double)Y.size() : 0.0;
   // the plan path builds its descriptors on the device from the block tables
