@@ -647,6 +647,8 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
     t = float(np.mean(ts))
     return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d_tables[0] + 16 * n * nmv),
             "d2h_bytes_per_step": int(16 * n * nmv), "s_per_step": t, "s_per_step_median": float(np.median(ts)),
+            "s_per_step_min": float(np.min(ts)), "s_per_step_max": float(np.max(ts)),
+            "s_per_step_all": [round(x, 4) for x in ts],
             "steps": steps,
             "path": "C-ABI through the host API: host mesh tables -> gk_plan_create (host plan + table upload) -> "
                     "gk_plan_assemble (device-resident A)%s -> %s; wall clock"

@@ -5,9 +5,9 @@
 # cfg-4 bench.
 mkdir -p gpurun_out
 TAG=${TAG:-f}
-rm -f gpurun_out/parity_$TAG.jsonl
+if [ -z "$NOPARITY" ]; then rm -f gpurun_out/parity_$TAG.jsonl
 GK_PARITY_LOG=gpurun_out/parity_$TAG.jsonl timeout 2400 python -m pytest -q -x -s tests/test_gpu_full_parity.py > gpurun_out/pytest_parity_$TAG.log 2>&1
-echo "parity rc=$?"; tail -2 gpurun_out/pytest_parity_$TAG.log
+echo "parity rc=$?"; tail -2 gpurun_out/pytest_parity_$TAG.log; fi
 timeout 300 python scripts/asm_probe.py --n 10242 --fam P0 --once > /dev/null 2>&1 &&
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_assemble -c 1 \
   -o gpurun_out/r02_k_assemble_p0l5_$TAG -f python scripts/asm_probe.py --n 10242 --fam P0 --once > gpurun_out/ncu_p0l5_$TAG.log 2>&1
