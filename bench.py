@@ -616,9 +616,13 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
     sp = stream.cuda_stream
     h2d_tables = [0]
 
-    def one():
+    def one(ev=None):
+        t_a = time.perf_counter()
         plan = g.AssemblyPlan(dom, dom, space, kern, space, opts)
         h2d_tables[0] = plan.info()["device_bytes"]
+        if ev:
+            ev[2] = time.perf_counter() - t_a  # host planning + table upload
+            ev[0].record(stream)
         plan.assemble(A.data_ptr(), n, sp)
         if cfg == 3:
             nf = g.NearField(dom, dom, space, "[1/r]", space)
@@ -633,22 +637,31 @@ def e2e_dense(g, torch, dev, cfg, pp, opts, n, nmv, xs, pairs_ref, steps, warmup
                 xd[0].copy_(xh[i], non_blocking=True)
                 g.matvec(A.data_ptr(), n, n, n, xd[0].data_ptr(), yd[0].data_ptr(), sp)
                 yh[i].copy_(yd[0], non_blocking=True)
+        if ev:
+            ev[1].record(stream)
         torch.cuda.synchronize(dev)
 
     for _ in range(max(1, min(3, warmup))):
         one()
     ts = []
-    for _ in range(steps):
-        t = time.perf_counter()
-        one()
-        ts.append(time.perf_counter() - t)
+    evs = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), 0.0] for _ in range(steps)]
+    with ClockSampler(dev.index or 0) as clk:
+        for i in range(steps):
+            t = time.perf_counter()
+            one(evs[i])
+            ts.append(time.perf_counter() - t)
     del A
     torch.cuda.empty_cache()
     t = float(np.mean(ts))
+    dev_ms = [e[0].elapsed_time(e[1]) for e in evs]
     return {"value": pairs_ref / t, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d_tables[0] + 16 * n * nmv),
             "d2h_bytes_per_step": int(16 * n * nmv), "s_per_step": t, "s_per_step_median": float(np.median(ts)),
             "s_per_step_min": float(np.min(ts)), "s_per_step_max": float(np.max(ts)),
             "s_per_step_all": [round(x, 4) for x in ts],
+            # where a step's time goes: the host planner + table upload, then the device work
+            # (assembly, copies and matvecs, CUDA events), and the board's clocks over the leg
+            "plan_s_all": [round(e[2], 4) for e in evs], "device_s_all": [round(x * 1e-3, 4) for x in dev_ms],
+            "clocks": clk.summary(),
             "steps": steps,
             "path": "C-ABI through the host API: host mesh tables -> gk_plan_create (host plan + table upload) -> "
                     "gk_plan_assemble (device-resident A)%s -> %s; wall clock"

@@ -79,7 +79,10 @@ void ensure_pool() {
   if ((done >> dev) & 1u) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = 256ull << 20;
+    // (256 MB measured too small: with two cfg-4 plans alive (2 x 171 MB) the pool
+    // handed its free blocks back at every synchronize, and re-acquiring them
+    // stalled about one one-shot step in six by 0.1-0.5 s)
+    uint64_t keep = 1024ull << 20;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   cudaGetLastError();

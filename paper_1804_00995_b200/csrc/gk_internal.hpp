@@ -140,7 +140,7 @@ struct DevArena {
     return reinterpret_cast<T*>(static_cast<char*>(p) + off);
   }
 };
-void ensure_pool();  // default memory pool keeps up to 256 MB cached (per device)
+void ensure_pool();  // default memory pool keeps up to 1 GB cached (per device)
 constexpr int kMaxDevices = 64;  // process-wide device caches are per device index
 int current_device();            // cudaGetDevice, checked against kMaxDevices
 

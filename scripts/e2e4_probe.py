@@ -27,7 +27,7 @@ xd = torch.empty((10, n), dtype=torch.complex128, device="cuda")
 yd = torch.empty((10, n), dtype=torch.complex128, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 print("nproc", os.cpu_count(), flush=True)
-for it in range(4):
+for it in range(int(os.environ.get("E2E_STEPS", "4"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan = g.AssemblyPlan(dom, dom, sp, kern, sp, o)
