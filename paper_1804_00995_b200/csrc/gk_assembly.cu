@@ -388,7 +388,8 @@ __device__ __forceinline__ void gather_phase(const AsmArgs& a, const GatherView&
     }
 #pragma unroll
     for (int q = 0; q < kG; ++q)
-      if (ok[q]) Arow[oj[q] * lda] = make_double2(re[q], im[q]);
+      if (ok[q] && !(a.dbg & 16)) Arow[oj[q] * lda] = make_double2(re[q], im[q]);  // (dbg 16: no direct stores)
+    if (a.dbg & 32) continue;  // (dbg 32: no mirror stores)
 #pragma unroll
     for (int q = 0; q < kG; q += 2) {
       double2* const m = Acol + oj[q];
