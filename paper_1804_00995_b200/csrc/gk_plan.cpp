@@ -164,38 +164,63 @@ bool sides_identical(const gk_side& a, const gk_side& b) {
 }
 
 Locations build_locations(const gk_side& s, const char* who) {
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gk_plan]   %-20s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   validate(s, who);
+  lap("validate");
   Locations L;
   L.npts = s.npts;
   L.nfree = s.nfree;
   L.point_loc.resize(s.npts);
   // open-addressing table of location ids keyed by the coordinate bit
-  // patterns (linear probing, load <= 1/2); ids in first-seen point order
+  // patterns (linear probing, load <= 1/2); ids in first-seen point order.
+  // The table is far larger than the host caches (cfg 4: 4 MB for 245,760
+  // points), so the hashes are formed in a first pass and each probe's slot is
+  // prefetched a few points ahead; a slot holds the id and 32 hash bits that
+  // filter out nearly every foreign key without touching the key array.
   size_t cap = 16;
   while (cap < 2 * (size_t)s.npts) cap <<= 1;
-  hvec<int64_t> slot(cap, -1);
+  struct Slot {
+    int32_t id;
+    uint32_t tag;
+  };
+  hvec<Slot> slot(cap, Slot{-1, 0u});
   hvec<Key> keys;
   keys.reserve((size_t)s.npts);
   L.x.reserve((size_t)s.npts);
   L.y.reserve((size_t)s.npts);
   L.z.reserve((size_t)s.npts);
   const KeyHash hasher;
+  hvec<uint64_t> hs((size_t)s.npts);
+  for (int64_t k = 0; k < s.npts; ++k) hs[(size_t)k] = hasher(Key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])});
+  constexpr int64_t kAhead = 16;
   for (int64_t k = 0; k < s.npts; ++k) {
+    if (k + kAhead < s.npts) __builtin_prefetch(&slot[hs[(size_t)(k + kAhead)] & (cap - 1)], 1);
     const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
-    size_t h = hasher(key) & (cap - 1);
-    while (slot[h] >= 0 && !(keys[(size_t)slot[h]] == key)) h = (h + 1) & (cap - 1);
-    if (slot[h] < 0) {
+    const uint64_t hv = hs[(size_t)k];
+    const uint32_t tag = (uint32_t)(hv >> 32);
+    size_t h = hv & (cap - 1);
+    while (slot[h].id >= 0 && !(slot[h].tag == tag && keys[(size_t)slot[h].id] == key)) h = (h + 1) & (cap - 1);
+    if (slot[h].id < 0) {
       const int64_t u = (int64_t)L.x.size();
-      slot[h] = u;
+      slot[h] = Slot{(int32_t)u, tag};
       keys.push_back(key);
       L.x.push_back(s.x[k]);
       L.y.push_back(s.y[k]);
       L.z.push_back(s.z[k]);
       L.point_loc[k] = u;
     } else {
-      L.point_loc[k] = slot[h];
+      L.point_loc[k] = slot[h].id;
     }
   }
+  lap("location ids");
   const int64_t U = L.size();
   // contributions: (dof, w_k * phi) for nonzero basis values of free dofs
   // (femspace.cpp:476-484 skips exact zeros and constrained dofs), merged per
@@ -238,7 +263,9 @@ Locations build_locations(const gk_side& s, const char* who) {
       L.cdof[L.cstart[u] + i] = tdof[cnt[u] + i];
       L.ccoef[L.cstart[u] + i] = tcoef[cnt[u] + i];
     }
+  lap("contributions");
   set_order(L, true);
+  lap("natural order");
   return L;
 }
 
@@ -991,7 +1018,35 @@ Coincidence find_coincidences(const Locations& X, const Locations& Y, bool same,
   for (int64_t u = 0; u < X.size(); ++u) pts.push_back({X.x[u], (int32_t)u, 0});
   if (!same)
     for (int64_t v = 0; v < Y.size(); ++v) pts.push_back({Y.x[v], (int32_t)v, 1});
-  std::sort(pts.begin(), pts.end(), [](const P& a, const P& b) { return a.x < b.x || (a.x == b.x && a.side < b.side); });
+  // sorted by x: chunks sorted on the planner's threads, then merged pairwise
+  // (the order among equal keys is immaterial: every pair inside the window
+  // is examined whatever it is)
+  auto before = [](const P& a, const P& b) { return a.x < b.x || (a.x == b.x && a.side < b.side); };
+  {
+    const size_t n = pts.size();
+    const int nt = t_serial ? 1 : (int)std::min<size_t>((size_t)host_threads(), n / 8192);
+    if (nt <= 1) {
+      std::sort(pts.begin(), pts.end(), before);
+    } else {
+      auto bound = [&](int c) { return n * (size_t)std::min(c, nt) / (size_t)nt; };
+      auto fan = [&](int tasks, auto&& fn) {
+        std::vector<std::thread> pool;
+        for (int t = 1; t < tasks; ++t) pool.emplace_back([&fn, t] { fn(t); });
+        fn(0);
+        for (auto& th : pool) th.join();
+      };
+      fan(nt, [&](int c) { std::sort(pts.begin() + bound(c), pts.begin() + bound(c + 1), before); });
+      hvec<P> tmp(n);
+      for (int w = 1; w < nt; w *= 2) {
+        const int pairs = (nt + 2 * w - 1) / (2 * w);
+        fan(pairs, [&](int q) {
+          const size_t a = bound(2 * w * q), m = bound(2 * w * q + w), e = bound(2 * w * q + 2 * w);
+          std::merge(pts.begin() + a, pts.begin() + m, pts.begin() + m, pts.begin() + e, tmp.begin() + a, before);
+        });
+        pts.swap(tmp);
+      }
+    }
+  }
   auto coord = [&](const P& p, double& x, double& y, double& z) {
     const Locations& L = p.side ? Y : X;
     x = L.x[p.id];
@@ -1037,7 +1092,14 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
   // The coincidence sweep and the candidate orders are independent (the
   // sweep reads coordinates only; the candidates work on copies), so they run
   // concurrently; build_locations left X and Y in natural order.
-  auto sweep = std::async(std::launch::async, [&] { return find_coincidences(X, Y ? *Y : X, Y == nullptr, eps); });
+  auto sweep = std::async(std::launch::async, [&] {
+    const auto s0 = std::chrono::steady_clock::now();
+    Coincidence C = find_coincidences(X, Y ? *Y : X, Y == nullptr, eps);
+    if (timing)
+      std::fprintf(stderr, "[gk_plan]     %-18s %8.2f ms (concurrent)\n", "coincidence sweep",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count());
+    return C;
+  });
   auto layout_of = [&](Locations& Lx, Locations* Ly) { return layout_blocks(Lx, Ly ? *Ly : Lx, symmetric); };
   OrderChoice O;
   O.natural = true;
@@ -1077,6 +1139,7 @@ OrderChoice choose_order(Locations& X, Locations* Y, bool symmetric, double eps,
     // most accept_natural pairs per unique pair (callers whose kernel time
     // hides under a larger cost, like the PCIe-bound streamed path)
     BlockLayout B = layout_of(X, Y);
+    lap("  natural layout");
     const double unique = (double)X.size() * (double)(Y ? Y->size() : X.size()) * (symmetric ? 0.5 : 1.0);
     if ((double)B.pairs <= accept_natural * unique) {
       O.C = sweep.get();

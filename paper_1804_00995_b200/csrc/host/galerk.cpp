@@ -598,13 +598,16 @@ AssemblyPlan::AssemblyPlan(const Domain& dom_x, const Domain& dom_y, const FemSp
                            const FemSpace& trial, const BemOptions& opts, int symmetric, int64_t row_begin,
                            int64_t row_end) {
   SideTables tst = make_side_tables(dom_x, test);
-  const SideTables tri = make_side_tables(dom_y, trial);
   const bool slab = row_begin != 0 || (row_end >= 0 && row_end != tst.nfree);
+  // bem_dense(dom, dom, V, k, V) without a slab: one side-table build serves both sides
+  const bool same = !slab && &dom_x == &dom_y && &test == &trial;
+  const SideTables tri_own = same ? SideTables{} : make_side_tables(dom_y, trial);
   if (slab) {
     tst = row_slab(tst, row_begin, row_end < 0 ? tst.nfree : row_end);
     if (symmetric == 1) throw std::invalid_argument("AssemblyPlan: a row slab is not symmetric");
     symmetric = 0;
   }
+  const SideTables& tri = same ? tst : tri_own;
   const gk_side a = tst.abi(), b = tri.abi();
   const gk_kernel k = kernel.abi();
   const gk_options o = abi_options(opts, symmetric);
