@@ -89,9 +89,65 @@ void ensure_pool() {
   done |= 1ull << dev;
 }
 
+namespace {
+// grow-only pinned staging buffer shared by the process's arenas: a pageable
+// copy of a few MB runs at a few GB/s, a pinned one at PCIe speed
+struct PinnedStaging {
+  std::mutex m;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  bool ensure(size_t n) {  // with m held
+    if (bytes >= n) return true;
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    bytes = 0;
+    if (cudaMallocHost(&buf, n) != cudaSuccess) {
+      cudaGetLastError();
+      buf = nullptr;
+      return false;
+    }
+    bytes = n;
+    return true;
+  }
+};
+PinnedStaging& pinned_staging() {
+  static PinnedStaging S;
+  return S;
+}
+}  // namespace
+
+void DevArena::begin_pinned(size_t upper_bound) {
+  if (pinned || !host.empty() || upper_bound == 0) return;
+  PinnedStaging& S = pinned_staging();
+  S.m.lock();
+  if (!S.ensure(upper_bound)) {
+    S.m.unlock();
+    return;  // no pinned memory: stage in `host`
+  }
+  pinned = static_cast<char*>(S.buf);
+  pinned_cap = S.bytes;
+  pinned_used = 0;
+}
+
+void DevArena::unlock_pinned() {
+  if (!pinned) return;
+  pinned = nullptr;
+  pinned_cap = pinned_used = 0;
+  pinned_staging().m.unlock();
+}
+
+void DevArena::spill_pinned() {
+  host.assign(pinned, pinned + pinned_used);
+  unlock_pinned();
+}
+
 void DevArena::upload() {
-  release();
-  const size_t copy = host.size();
+  if (p) {
+    cudaDeviceSynchronize();  // the tables may still be read by work on any stream
+    cudaFreeAsync(p, nullptr);
+    p = nullptr;
+  }
+  const size_t copy = used();
   bytes = copy + extra;
   if (bytes) {
     ensure_pool();
@@ -99,32 +155,25 @@ void DevArena::upload() {
       cudaGetLastError();
       p = nullptr;
       bytes = 0;
-      throw NoMemError("device allocation of " + std::to_string(host.size() + extra) + " bytes failed");
+      unlock_pinned();
+      throw NoMemError("device allocation of " + std::to_string(copy + extra) + " bytes failed");
     }
-    // through a grow-only pinned staging buffer: a pageable copy of a few MB
-    // runs at a few GB/s, a pinned one at PCIe speed
-    static std::mutex staging_mutex;
-    static void* staging = nullptr;
-    static size_t staging_bytes = 0;
-    std::lock_guard<std::mutex> hold(staging_mutex);
-    if (staging_bytes < copy) {
-      if (staging) cudaFreeHost(staging);
-      staging = nullptr;
-      staging_bytes = 0;
-      if (cudaMallocHost(&staging, copy) != cudaSuccess) {
-        cudaGetLastError();
-        staging = nullptr;
+    if (pinned) {
+      const cudaError_t e = cudaMemcpy(p, pinned, copy, cudaMemcpyHostToDevice);
+      unlock_pinned();
+      cuda_check(e, "cudaMemcpy H2D");
+    } else {
+      PinnedStaging& S = pinned_staging();
+      std::lock_guard<std::mutex> hold(S.m);
+      if (S.ensure(copy)) {
+        std::memcpy(S.buf, host.data(), copy);
+        cuda_check(cudaMemcpy(p, S.buf, copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
       } else {
-        staging_bytes = copy;
+        cuda_check(cudaMemcpy(p, host.data(), copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
       }
     }
-    if (staging) {
-      std::memcpy(staging, host.data(), copy);
-      cuda_check(cudaMemcpy(p, staging, copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-    } else {
-      cuda_check(cudaMemcpy(p, host.data(), copy, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-    }
   }
+  unlock_pinned();
   hvec<char>().swap(host);
 }
 
@@ -135,6 +184,7 @@ void DevArena::release() {
   }
   p = nullptr;
   bytes = 0;
+  unlock_pinned();  // (an arena dropped between begin_pinned and upload)
 }
 
 }  // namespace gk
@@ -365,9 +415,10 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
     masked_bits[(size_t)(e >> 5)] |= 1u << (e & 31);
   }
   lap("tile list");
-  Ar.host.reserve((T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
+  Ar.begin_pinned((T.xl_x.size() * 3 + T.xsup_c.size()) * sizeof(double) +
                   (T.xsup_start.size() + T.xsup_u.size() + X.perm.size() + Yr.perm.size()) * sizeof(int32_t) +
-                  T.yrec.size() * sizeof(YRec) + masked_bits.size() * 4 + (nIb + nJb) * 32 + 24 * 256);
+                  T.yrec.size() * sizeof(YRec) + T.yscale.size() * sizeof(double) + masked_bits.size() * 4 +
+                  (nIb + nJb) * 32 + 24 * 256);
   const size_t o_ts = Ar.add(tile_start), o_fb = Ar.add(first_bj), o_xd = Ar.add(T.xb_dof_start),
                o_xl = Ar.add(T.xb_loc_start), o_yd = Ar.add(T.yb_dof_start), o_yr = Ar.add(T.yb_rec_start),
                o_yz = Ar.add(T.yb_zero), o_mb = Ar.add(masked_bits);

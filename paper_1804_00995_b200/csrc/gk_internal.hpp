@@ -114,11 +114,24 @@ struct DevArena {
   DevArena(const DevArena&) = delete;
   DevArena& operator=(const DevArena&) = delete;
   ~DevArena() { release(); }
+  // Optional: stage straight into the process-wide pinned buffer (held, with
+  // its lock, until upload() or release()), so that each table is copied once
+  // instead of into `host` (zero-filled first) and from there into the pinned
+  // buffer.  `upper_bound` covers every later add(); a larger total falls back
+  // to `host`.  Without this call add() stages in `host`.
+  void begin_pinned(size_t upper_bound);
   template <class T>
   size_t add(const T* data, size_t n) {
-    const size_t off = (host.size() + 255) & ~size_t(255);
-    host.resize(off + n * sizeof(T));
-    if (n) std::memcpy(host.data() + off, data, n * sizeof(T));
+    const size_t off = (used() + 255) & ~size_t(255);
+    const size_t end = off + n * sizeof(T);
+    if (pinned && end > pinned_cap) spill_pinned();
+    if (pinned) {
+      if (n) std::memcpy(pinned + off, data, n * sizeof(T));
+      pinned_used = end;
+    } else {
+      host.resize(end);
+      if (n) std::memcpy(host.data() + off, data, n * sizeof(T));
+    }
     return off;
   }
   template <class V>
@@ -128,8 +141,8 @@ struct DevArena {
   // device-only bytes after the uploaded tables (filled on the device);
   // call after the last add()
   size_t add_device_only(size_t n) {
-    const size_t off = (host.size() + 255) & ~size_t(255);
-    extra = off + n - host.size();
+    const size_t off = (used() + 255) & ~size_t(255);
+    extra = off + n - used();
     return off;
   }
   size_t extra = 0;
@@ -139,6 +152,13 @@ struct DevArena {
   T* at(size_t off) const {
     return reinterpret_cast<T*>(static_cast<char*>(p) + off);
   }
+
+ private:
+  char* pinned = nullptr;  // the shared pinned staging buffer while this arena holds its lock
+  size_t pinned_cap = 0, pinned_used = 0;
+  size_t used() const { return pinned ? pinned_used : host.size(); }
+  void spill_pinned();   // move what is staged into `host` and give the pinned buffer back
+  void unlock_pinned();
 };
 void ensure_pool();  // default memory pool keeps up to 1 GB cached (per device)
 constexpr int kMaxDevices = 64;  // process-wide device caches are per device index

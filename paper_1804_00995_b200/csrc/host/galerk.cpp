@@ -4,6 +4,10 @@
 // the reference algorithm; all pair/contraction work goes to the device.
 #include "galerk.hpp"
 
+namespace gk {
+int host_threads();  // gk_plan.cpp: GK_THREADS / hardware threads shared among the node's ranks, at most 16
+}
+
 #include <sys/mman.h>
 
 #include <algorithm>
@@ -13,6 +17,7 @@
 #include <limits>
 #include <map>
 #include <sstream>
+#include <thread>
 
 namespace galerk {
 
@@ -256,17 +261,29 @@ QuadratureSet quadrature(const Domain& dom) {
   qs.z.resize(ne * g);
   qs.weights.resize(ne * g);
   qs.element_of.resize(ne * g);
-  for (int64_t e = 0; e < ne; ++e) {
-    const double measure = mesh.element_measure(e);
-    for (int q = 0; q < g; ++q) {
-      Vec3 p{0, 0, 0};
-      for (int c = 0; c < 3; ++c) p = add(p, scale(rule.barycentric[q][c], mesh.vertex(mesh.elements[3 * e + c])));
-      qs.x[e * g + q] = p.x;
-      qs.y[e * g + q] = p.y;
-      qs.z[e * g + q] = p.z;
-      qs.weights[e * g + q] = rule.weights[q] * measure;
-      qs.element_of[e * g + q] = (int32_t)e;
+  auto fill = [&](int64_t e0, int64_t e1) {
+    for (int64_t e = e0; e < e1; ++e) {
+      const double measure = mesh.element_measure(e);
+      for (int q = 0; q < g; ++q) {
+        Vec3 p{0, 0, 0};
+        for (int c = 0; c < 3; ++c) p = add(p, scale(rule.barycentric[q][c], mesh.vertex(mesh.elements[3 * e + c])));
+        qs.x[e * g + q] = p.x;
+        qs.y[e * g + q] = p.y;
+        qs.z[e * g + q] = p.z;
+        qs.weights[e * g + q] = rule.weights[q] * measure;
+        qs.element_of[e * g + q] = (int32_t)e;
+      }
     }
+  };
+  // elements are independent: large meshes are filled on the planner's host threads
+  const int nt = (int)std::min<int64_t>(gk::host_threads(), ne / 8192);
+  if (nt <= 1) {
+    fill(0, ne);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(fill, ne * t / nt, ne * (t + 1) / nt);
+    fill(0, ne / nt);
+    for (auto& th : pool) th.join();
   }
   return qs;
 }
