@@ -98,6 +98,7 @@ size_t plan_cache_bytes() {
 }
 
 namespace {
+thread_local bool t_serial = false;  // set by callers that already run one task per thread
 struct Key {
   uint64_t a, b, c;
   bool operator==(const Key& o) const { return a == o.a && b == o.b && c == o.c; }
@@ -150,6 +151,7 @@ static void validate(const gk_side& s, const char* who) {
   if (s.npts > 0 && (!s.x || !s.y || !s.z || !s.w || !s.elem_dofs || !s.basis))
     throw std::invalid_argument(std::string(who) + ": null array");
   if (s.nfree > INT32_MAX) throw std::invalid_argument(std::string(who) + ": too many dofs");
+  if (s.npts > INT32_MAX) throw std::invalid_argument(std::string(who) + ": too many quadrature points");
 }
 
 bool sides_identical(const gk_side& a, const gk_side& b) {
@@ -179,45 +181,112 @@ Locations build_locations(const gk_side& s, const char* who) {
   L.npts = s.npts;
   L.nfree = s.nfree;
   L.point_loc.resize(s.npts);
-  // open-addressing table of location ids keyed by the coordinate bit
-  // patterns (linear probing, load <= 1/2); ids in first-seen point order.
-  // The table is far larger than the host caches (cfg 4: 4 MB for 245,760
-  // points), so the hashes are formed in a first pass and each probe's slot is
-  // prefetched a few points ahead; a slot holds the id and 32 hash bits that
-  // filter out nearly every foreign key without touching the key array.
-  size_t cap = 16;
-  while (cap < 2 * (size_t)s.npts) cap <<= 1;
-  struct Slot {
-    int32_t id;
-    uint32_t tag;
-  };
-  hvec<Slot> slot(cap, Slot{-1, 0u});
-  hvec<Key> keys;
-  keys.reserve((size_t)s.npts);
-  L.x.reserve((size_t)s.npts);
-  L.y.reserve((size_t)s.npts);
-  L.z.reserve((size_t)s.npts);
-  const KeyHash hasher;
-  hvec<uint64_t> hs((size_t)s.npts);
-  for (int64_t k = 0; k < s.npts; ++k) hs[(size_t)k] = hasher(Key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])});
-  constexpr int64_t kAhead = 16;
-  for (int64_t k = 0; k < s.npts; ++k) {
-    if (k + kAhead < s.npts) __builtin_prefetch(&slot[hs[(size_t)(k + kAhead)] & (cap - 1)], 1);
-    const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
-    const uint64_t hv = hs[(size_t)k];
-    const uint32_t tag = (uint32_t)(hv >> 32);
-    size_t h = hv & (cap - 1);
-    while (slot[h].id >= 0 && !(slot[h].tag == tag && keys[(size_t)slot[h].id] == key)) h = (h + 1) & (cap - 1);
-    if (slot[h].id < 0) {
-      const int64_t u = (int64_t)L.x.size();
-      slot[h] = Slot{(int32_t)u, tag};
-      keys.push_back(key);
-      L.x.push_back(s.x[k]);
-      L.y.push_back(s.y[k]);
-      L.z.push_back(s.z[k]);
-      L.point_loc[k] = u;
-    } else {
-      L.point_loc[k] = slot[h].id;
+  // Location ids in first-seen point order.  Large sides: hash-sharded on the
+  // planner's threads — thread q owns the keys whose hash falls in its slice,
+  // scans all points in order and records for each of its points the first
+  // point with the same key (its own small table stays in cache); the ids are
+  // then the ranks of the first occurrences, exactly the serial numbering.
+  const int nth = t_serial ? 1 : (int)std::min<int64_t>(host_threads(), s.npts / 16384);
+  if (nth > 1) {
+    const size_t n = (size_t)s.npts;
+    hvec<uint64_t> hs(n);
+    hvec<int32_t> rep(n);  // first point with the same coordinates
+    auto fan = [&](auto&& fn) {
+      std::vector<std::thread> pool;
+      for (int q = 1; q < nth; ++q) pool.emplace_back([&fn, q] { fn(q); });
+      fn(0);
+      for (auto& th : pool) th.join();
+    };
+    const KeyHash hasher;
+    fan([&](int q) {
+      for (size_t k = n * q / nth; k < n * (q + 1) / nth; ++k)
+        hs[k] = hasher(Key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])});
+    });
+    fan([&](int q) {
+      // slice of the hash space by the top bits; table of >= 2x the expected keys
+      size_t cap = 16;
+      while (cap < 3 * n / (size_t)nth) cap <<= 1;
+      hvec<int32_t> slot(cap, -1);
+      for (size_t k = 0; k < n; ++k) {
+        const uint64_t hv = hs[k];
+        if ((int)(((hv >> 40) * (uint64_t)nth) >> 24) != q) continue;
+        const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
+        size_t h = hv & (cap - 1);
+        for (;;) {
+          const int32_t f = slot[h];
+          if (f < 0) {
+            slot[h] = (int32_t)k;
+            rep[k] = (int32_t)k;
+            break;
+          }
+          if (hs[(size_t)f] == hv && bits(s.x[f]) == key.a && bits(s.y[f]) == key.b && bits(s.z[f]) == key.c) {
+            rep[k] = f;
+            break;
+          }
+          h = (h + 1) & (cap - 1);
+        }
+      }
+    });
+    int64_t U = 0;
+    for (size_t k = 0; k < n; ++k)
+      if (rep[k] == (int32_t)k) L.point_loc[k] = U++;
+    L.x.resize((size_t)U);
+    L.y.resize((size_t)U);
+    L.z.resize((size_t)U);
+    fan([&](int q) {
+      for (size_t k = n * q / nth; k < n * (q + 1) / nth; ++k) {
+        const int32_t f = rep[k];
+        if (f == (int32_t)k) {
+          const int64_t u = L.point_loc[k];
+          L.x[(size_t)u] = s.x[k];
+          L.y[(size_t)u] = s.y[k];
+          L.z[(size_t)u] = s.z[k];
+        } else {
+          L.point_loc[k] = L.point_loc[(size_t)f];  // f < k: a first occurrence, numbered by the serial pass
+        }
+      }
+    });
+  } else {
+    // open-addressing table of location ids keyed by the coordinate bit
+    // patterns (linear probing, load <= 1/2); ids in first-seen point order.
+    // The table is far larger than the host caches (cfg 4: 4 MB for 245,760
+    // points), so the hashes are formed in a first pass and each probe's slot is
+    // prefetched a few points ahead; a slot holds the id and 32 hash bits that
+    // filter out nearly every foreign key without touching the key array.
+    size_t cap = 16;
+    while (cap < 2 * (size_t)s.npts) cap <<= 1;
+    struct Slot {
+      int32_t id;
+      uint32_t tag;
+    };
+    hvec<Slot> slot(cap, Slot{-1, 0u});
+    hvec<Key> keys;
+    keys.reserve((size_t)s.npts);
+    L.x.reserve((size_t)s.npts);
+    L.y.reserve((size_t)s.npts);
+    L.z.reserve((size_t)s.npts);
+    const KeyHash hasher;
+    hvec<uint64_t> hs((size_t)s.npts);
+    for (int64_t k = 0; k < s.npts; ++k) hs[(size_t)k] = hasher(Key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])});
+    constexpr int64_t kAhead = 16;
+    for (int64_t k = 0; k < s.npts; ++k) {
+      if (k + kAhead < s.npts) __builtin_prefetch(&slot[hs[(size_t)(k + kAhead)] & (cap - 1)], 1);
+      const Key key{bits(s.x[k]), bits(s.y[k]), bits(s.z[k])};
+      const uint64_t hv = hs[(size_t)k];
+      const uint32_t tag = (uint32_t)(hv >> 32);
+      size_t h = hv & (cap - 1);
+      while (slot[h].id >= 0 && !(slot[h].tag == tag && keys[(size_t)slot[h].id] == key)) h = (h + 1) & (cap - 1);
+      if (slot[h].id < 0) {
+        const int64_t u = (int64_t)L.x.size();
+        slot[h] = Slot{(int32_t)u, tag};
+        keys.push_back(key);
+        L.x.push_back(s.x[k]);
+        L.y.push_back(s.y[k]);
+        L.z.push_back(s.z[k]);
+        L.point_loc[k] = u;
+      } else {
+        L.point_loc[k] = slot[h].id;
+      }
     }
   }
   lap("location ids");
@@ -559,7 +628,6 @@ int host_threads() {
 }
 
 namespace {
-thread_local bool t_serial = false;  // set by callers that already run one task per thread
 // Static-partition parallel loop over [0, n) on up to host_threads() threads;
 // fn(begin, end) per chunk.
 template <class F>
