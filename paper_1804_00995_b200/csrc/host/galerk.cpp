@@ -11,7 +11,9 @@ int host_threads();  // gk_plan.cpp: GK_THREADS / hardware threads shared among 
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -614,6 +616,8 @@ SpMat regularize_radiation(const std::vector<Vec3>& points, const Domain& dom_y,
 AssemblyPlan::AssemblyPlan(const Domain& dom_x, const Domain& dom_y, const FemSpace& test, const Kernel& kernel,
                            const FemSpace& trial, const BemOptions& opts, int symmetric, int64_t row_begin,
                            int64_t row_end) {
+  const bool timing = std::getenv("GK_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   SideTables tst = make_side_tables(dom_x, test);
   const bool slab = row_begin != 0 || (row_end >= 0 && row_end != tst.nfree);
   // bem_dense(dom, dom, V, k, V) without a slab: one side-table build serves both sides
@@ -628,7 +632,12 @@ AssemblyPlan::AssemblyPlan(const Domain& dom_x, const Domain& dom_y, const FemSp
   const gk_side a = tst.abi(), b = tri.abi();
   const gk_kernel k = kernel.abi();
   const gk_options o = abi_options(opts, symmetric);
+  const auto t1 = std::chrono::steady_clock::now();
   throw_status(gk_plan_create(&a, &b, &k, &o, &plan_));
+  if (timing)
+    std::fprintf(stderr, "[AssemblyPlan] side tables %.2f ms, gk_plan_create %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
 }
 
 AssemblyPlan::~AssemblyPlan() {
