@@ -72,6 +72,14 @@ gk_status gk_diag_nearfield_pairs(const gk_nearfield* nf, int32_t* ex, int32_t* 
 gk_status gk_diag_plan_info(const gk_side* test, const gk_side* trial, const gk_kernel* kernel,
                             const gk_options* opts, gk_plan_info* info);
 
+/* Host-only: the planner's location numbering of one side (twins merged, ids
+ * in first-seen point order).  point_loc[npts] receives each point's location
+ * id, xyz[3 * n_locations] (may be NULL) the location coordinates.  serial != 0
+ * forces the one-thread path; the threaded, hash-sharded path used for large
+ * sides must give the same ids (tests/test_host_cpu.py). */
+gk_status gk_diag_location_ids(const gk_side* side, int32_t serial, int64_t* point_loc, int64_t* n_locations,
+                               double* xyz);
+
 #ifdef __cplusplus
 }
 #endif

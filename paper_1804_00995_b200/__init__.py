@@ -74,6 +74,7 @@ diag_fp64_peak = _native.diag_fp64_peak
 diag_fp64_sustained = _native.diag_fp64_sustained
 plan_info_dry = _native.plan_info_dry
 plan_info_dry_rows = _native.plan_info_dry_rows
+location_ids = _native.location_ids
 diag_probe_pairs = _native.diag_probe_pairs
 diag_probe_analytic = _native.diag_probe_analytic
 diag_math = _native.diag_math

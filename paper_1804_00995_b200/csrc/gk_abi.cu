@@ -950,6 +950,27 @@ gk_status gk_diag_plan_info(const gk_side* test, const gk_side* trial, const gk_
   return gk_plan_get_info(P.get(), info);
 }
 
+gk_status gk_diag_location_ids(const gk_side* side, int32_t serial, int64_t* point_loc, int64_t* n_locations,
+                               double* xyz) {
+  return guard([&] {
+    if (!side || !point_loc || !n_locations) throw std::invalid_argument("gk_diag_location_ids: null argument");
+    struct Serial {  // the planner's per-thread switch, restored on every exit
+      bool on;
+      explicit Serial(bool s) : on(s) {
+        if (on) planner_serial(true);
+      }
+      ~Serial() {
+        if (on) planner_serial(false);
+      }
+    } hold(serial != 0);
+    const Locations L = build_locations(*side, "gk_diag_location_ids");
+    for (int64_t k = 0; k < side->npts; ++k) point_loc[k] = L.point_loc[(size_t)k];
+    *n_locations = L.size();
+    if (xyz)
+      for (int64_t u = 0; u < L.size(); ++u) xyz[3 * u] = L.x[u], xyz[3 * u + 1] = L.y[u], xyz[3 * u + 2] = L.z[u];
+  });
+}
+
 gk_status gk_plan_get_info(const gk_plan* P, gk_plan_info* info) {
   return guard([&] {
     if (!P || !info) throw std::invalid_argument("gk_plan_get_info: null argument");

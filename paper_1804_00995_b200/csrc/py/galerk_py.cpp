@@ -516,6 +516,18 @@ PYBIND11_MODULE(_galerk, m) {
       py::arg("dom_x"), py::arg("dom_y"), py::arg("test"), py::arg("kernel"), py::arg("trial"),
       py::arg("opts") = BemOptions{}, py::arg("symmetric") = -1);
   m.def(
+      "location_ids",
+      [](const Domain& d, const FemSpace& sp, bool serial) {
+        const SideTables t = make_side_tables(d, sp);
+        const gk_side s = t.abi();
+        py::array_t<int64_t> loc(s.npts);
+        py::array_t<double> xyz(3 * s.npts);
+        int64_t n = 0;
+        throw_status(gk_diag_location_ids(&s, serial ? 1 : 0, loc.mutable_data(), &n, xyz.mutable_data()));
+        return py::make_tuple(loc, n, xyz);
+      },
+      py::arg("dom"), py::arg("space"), py::arg("serial") = false);
+  m.def(
       "plan_info_dry_rows",
       [](const Domain& dx, const Domain& dy, const FemSpace& t, const Kernel& k, const FemSpace& u,
          const BemOptions& o, int64_t r0, int64_t r1) {

@@ -115,3 +115,29 @@ def test_no_cpu_fallback(galerk):
     p1 = galerk.make_fem(m, "P1")
     with pytest.raises(RuntimeError, match="no CUDA device"):
         galerk.bem_dense(dom, dom, p1, galerk.green_kernel("[1/r]", 0.0), p1)
+
+
+@pytest.mark.parametrize("nv,fam,gauss", [(40962, "P0", 3), (10242, "P1", 7), (2562, "P1", 3)])
+def test_threaded_location_numbering_equals_serial(galerk, nv, fam, gauss):
+    """Large sides number their locations on several host threads (hash-sharded,
+    gk_plan.cpp build_locations); the ids must be the serial first-seen ones,
+    so plans (and matrices) do not depend on the host's thread count."""
+    import numpy as np
+
+    g = galerk
+    mesh = g.build_sphere(nv, 1.0)
+    dom = g.make_domain(mesh, gauss)
+    sp = g.make_fem(mesh, fam)
+    loc_t, n_t, xyz_t = g.location_ids(dom, sp, False)
+    loc_s, n_s, xyz_s = g.location_ids(dom, sp, True)
+    assert n_t == n_s
+    assert np.array_equal(loc_t, loc_s)
+    assert np.array_equal(np.asarray(xyz_t)[: 3 * n_t], np.asarray(xyz_s)[: 3 * n_s])
+    # first-seen order: ids appear in increasing order of their first point
+    first = np.full(n_s, -1, dtype=np.int64)
+    ids = np.asarray(loc_s)
+    _, idx = np.unique(ids, return_index=True)
+    assert np.array_equal(np.sort(idx), idx)  # id u's first point precedes id u+1's
+    pts, _, _ = g.quadrature(dom)
+    pts = np.asarray(pts).reshape(-1, 3)
+    assert np.array_equal(np.asarray(xyz_s)[: 3 * n_s].reshape(-1, 3)[ids], pts + 0.0)
