@@ -175,3 +175,19 @@ def test_regularized_collocation_at_vertices_reference_test(galerk, oracle):
     assert np.all(np.abs(pot - 1.0) < 0.02)
     _, _, ov = oracle.regularize_radiation(pts, v, e, 3, P1, "[1/r]")
     assert np.any(np.isnan(ov))  # the restated reference algorithm
+
+
+def test_degenerate_trial_triangle_raises_before_any_device_work(galerk):
+    """kernels.cpp:156-157: analytic_triangle_integrals throws on a degenerate y
+    triangle.  The device path checks the (purely geometric) condition on the
+    host when the near-field object is created, so compute, apply and triplets
+    all fail like the reference instead of adding inf/NaN into A."""
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [2, 0, 0.0]])
+    e = np.array([[0, 1, 2], [0, 1, 3]], dtype=np.int32)  # second triangle: three collinear vertices
+    m = galerk.Mesh(v, e)
+    dom = galerk.make_domain(m, 3)
+    p0 = galerk.make_fem(m, "P0")
+    with pytest.raises(ValueError, match="degenerate triangle"):
+        nf = galerk.NearField(dom, dom, p0, "[1/r]", p0)
+        nf.compute(0)
+        nf.triplets()
