@@ -503,6 +503,8 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   a.kappa = 2.0 * P->k / M_PI;
   a.symmetric = P->symmetric ? 1 : 0;
   a.natural = P->natural ? 1 : 0;
+  a.l2_window = nullptr;
+  a.l2_window_bytes = 0;
   a.prof = nullptr;
   a.dbg = std::getenv("GK_ASM_DBG") ? std::atoi(std::getenv("GK_ASM_DBG")) : 0;
   a.jmax = P->jmax;
@@ -535,12 +537,15 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
   if (!std::getenv("GK_ASM_PROF")) {
     // Matrices far larger than L2 (>= 4 GB): the plan tables — everything
     // before the tile descriptors, 14 MB on cfg 4 — sit in a persisting L2
-    // window for this launch, so that the matrix write stream does not evict
-    // them (cfg 4: table re-reads from DRAM 2.82 -> 0.18 GB, DRAM traffic
-    // 1.026x -> 1.001x the matrix write; GK_L2_PERSIST=0 turns it off).  The
-    // device's persisting carve-out is raised to 32 MB if it is smaller.
+    // window for this launch (a launch attribute), so that the matrix write
+    // stream does not evict them (cfg 4: table re-reads from DRAM 2.82 ->
+    // 0.18 GB, DRAM traffic 1.026x -> 1.001x the matrix write;
+    // GK_L2_PERSIST=0 turns it off).  Smaller matrices do not gain: cfg 2's
+    // 0.44 GB of DRAM reads are sector fills behind its permuted 16-byte
+    // stores, not table re-reads (unchanged by the window, and the launch ran
+    // 0.5% slower with it).  The device's persisting carve-out is raised to
+    // 32 MB if smaller.
     static const bool allow = !(std::getenv("GK_L2_PERSIST") && std::atoi(std::getenv("GK_L2_PERSIST")) == 0);
-    const cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const bool persist = allow && (double)P->rows * (double)P->cols * 16.0 >= 4e9 && P->o_tiles > 0 &&
                          P->o_tiles <= (32u << 20);
     if (persist) {
@@ -550,24 +555,14 @@ void assemble(gk_plan* P, gk_cplx* A, int64_t lda, gk_stream stream) {
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
         if (cur < (32u << 20)) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 32u << 20);
-        cudaGetLastError();  // (a device without the feature: the window below is then ignored)
+        cudaGetLastError();  // (a device without the feature ignores the window)
         limit_set |= 1ull << dev;
       }
-      cudaStreamAttrValue av{};
-      av.accessPolicyWindow.base_ptr = Ar.p;
-      av.accessPolicyWindow.num_bytes = P->o_tiles;
-      av.accessPolicyWindow.hitRatio = 1.0f;
-      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      if (cudaStreamSetAttribute(cs, cudaStreamAttributeAccessPolicyWindow, &av) != cudaSuccess) cudaGetLastError();
+      a.l2_window = Ar.p;
+      a.l2_window_bytes = P->o_tiles;
       P->l2_window = true;
     }
     launch_assemble(a, P->ntiles + P->nmtiles, P->helmholtz, P->slots, stream);
-    if (persist) {
-      cudaStreamAttrValue av{};
-      av.accessPolicyWindow.num_bytes = 0;
-      cudaStreamSetAttribute(cs, cudaStreamAttributeAccessPolicyWindow, &av);
-    }
     return;
   }
   // diagnostics: per-tile phase cycles (staging / pair loop / gather + stores)
@@ -872,6 +867,8 @@ void bem_dense_streamed(const gk_side* test, const gk_side* trial, const gk_kern
     a.kappa = 2.0 * k / M_PI;
     a.symmetric = 0;
     a.natural = 0;
+    a.l2_window = nullptr;
+    a.l2_window_bytes = 0;
     a.prof = nullptr;
     a.dbg = 0;
     a.jmax = kJCap;  // slabs: the 22-row shape serves every y block

@@ -500,6 +500,26 @@ void launch_shape(const AsmArgs& a, int64_t ntiles, cudaStream_t s) {
                "cudaFuncSetAttribute");
     configured |= 1ull << dev;
   }
+  if (a.l2_window && a.l2_window_bytes) {
+    // the plan tables in a persisting L2 window for this launch only (a launch
+    // attribute: no stream state to set and clear)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)ntiles);
+    cfg.blockDim = dim3(kAsmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.l2_window);
+    at[0].val.accessPolicyWindow.num_bytes = (size_t)a.l2_window_bytes;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, k_assemble<HELM, SLOTS, JC>, a), "k_assemble launch");
+    return;
+  }
   k_assemble<HELM, SLOTS, JC><<<(unsigned)ntiles, kAsmThreads, smem, s>>>(a);
 }
 

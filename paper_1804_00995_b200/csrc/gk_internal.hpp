@@ -338,6 +338,8 @@ struct AsmArgs {
   int32_t natural;  // dof orders are the identity: A's indices are the permuted ones (no perm lookups)
   unsigned long long* prof;  // diagnostics: [tile][4] phase cycles + SM id, or null
   int32_t jmax;              // widest y block of the launch (dofs): selects the kernel shape (16 or 22)
+  const void* l2_window;     // host side only: tables to keep in a persisting L2 window for the launch (or null)
+  uint64_t l2_window_bytes;
   int32_t dbg;               // timing experiments only (GK_ASM_DBG; results invalid when set): 1 no stores, 2 no gather, 4 no pair loop, 8 no second-slot read-modify-write, 16 no direct stores, 32 no mirror stores
 };
 // Entries of oversized dofs (rows `rows` x all columns, all rows x columns
