@@ -429,7 +429,26 @@ std::unique_ptr<gk_plan> make_plan(const gk_side* test, const gk_side* trial, co
   P->o_xsup_start = Ar.add(T.xsup_start);
   P->o_xsup_u = Ar.add(T.xsup_u);
   P->o_xsup_c = Ar.add(T.xsup_c);
-  P->o_yrec = Ar.add(device_records(T.yrec, P->slots == 3));
+  if (P->slots == 3) {
+    // unit-coefficient records (32 bytes) written straight into the staging area, on a few threads
+    const size_t n = T.yrec.size();
+    YRecU* const u = Ar.alloc<YRecU>(n, P->o_yrec);
+    const YRec* const r = T.yrec.data();
+    auto fill = [=](size_t i0, size_t i1) {
+      for (size_t i = i0; i < i1; ++i) u[i] = {r[i].x, r[i].y, r[i].z, r[i].off0, r[i].off1};
+    };
+    const int nt = (int)std::min<size_t>((size_t)std::min(host_threads(), 4), n / 16384);
+    if (nt <= 1) {
+      fill(0, n);
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(fill, n * t / nt, n * (t + 1) / nt);
+      fill(0, n / nt);
+      for (auto& th : pool) th.join();
+    }
+  } else {
+    P->o_yrec = Ar.add(T.yrec);
+  }
   P->o_xperm = Ar.add(X.perm);
   P->o_yperm = Ar.add(Yr.perm);
   P->o_yscale = Ar.add(T.yscale);

@@ -138,6 +138,20 @@ struct DevArena {
   size_t add(const V& v) {
     return add(v.data(), v.size());
   }
+  // n uninitialised elements to be written in place before the next add()
+  // (which may move the staging area)
+  template <class T>
+  T* alloc(size_t n, size_t& off) {
+    off = (used() + 255) & ~size_t(255);
+    const size_t end = off + n * sizeof(T);
+    if (pinned && end > pinned_cap) spill_pinned();
+    if (pinned) {
+      pinned_used = end;
+      return reinterpret_cast<T*>(pinned + off);
+    }
+    host.resize(end);
+    return reinterpret_cast<T*>(host.data() + off);
+  }
   // device-only bytes after the uploaded tables (filled on the device);
   // call after the last add()
   size_t add_device_only(size_t n) {
